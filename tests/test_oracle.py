@@ -1,0 +1,385 @@
+"""Pins for the CPU oracle (oracle/) against what the paper and mathematics fix.
+
+Nothing here re-types the oracle's formulas: every check is a closed form, an
+invariant (Arnoldi relation, orthogonality, minimal-residual property), a
+textbook/library routine on a tiny case (dense LU / least squares via numpy),
+or a worked example from SPEC.md (cited).  Each is chosen so that a dropped
+term, wrong sign/index or transposed operand in the oracle fails at least one.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle as O
+
+# ------------------------------------------------------------------ helpers
+
+
+def csr_from_dense(D):
+    n = D.shape[0]
+    rp = [0]
+    cols, vals = [], []
+    for i in range(n):
+        nz = np.nonzero(D[i])[0]
+        cols.extend(nz.tolist())
+        vals.extend(D[i, nz].tolist())
+        rp.append(len(cols))
+    return inputs.CSR(np.array(rp, np.int32), np.array(cols, np.int32), np.array(vals, np.float64))
+
+
+def random_dd(n, seed, density=0.3, plus=1.0):
+    """F1 fixture: random sparse, strictly diagonally dominant."""
+    rng = np.random.default_rng(seed)
+    D = rng.standard_normal((n, n)) * (rng.random((n, n)) < density)
+    np.fill_diagonal(D, 0.0)
+    np.fill_diagonal(D, 1.1 * np.abs(D).sum(axis=1) + plus)
+    return D
+
+
+def lapl1d(n):
+    return np.diag(2.0 * np.ones(n)) - np.diag(np.ones(n - 1), 1) - np.diag(np.ones(n - 1), -1)
+
+
+# ------------------------------------------------------------------- SpMV
+
+
+def test_spmv_worked_examples():
+    # I₃·[1,2,3] = [1,2,3]; tridiag(-1,2,-1)·1 = [1,0,0,1]
+    assert np.array_equal(O.spmv64(csr_from_dense(np.eye(3)), np.array([1.0, 2, 3])), [1, 2, 3])
+    assert np.array_equal(O.spmv64(csr_from_dense(lapl1d(4)), np.ones(4)), [1, 0, 0, 1])
+
+
+@pytest.mark.parametrize("n,seed", [(8, 0), (33, 1), (64, 2)])
+def test_spmv64_dense(n, seed):
+    rng = np.random.default_rng(seed)
+    D = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.5)
+    x = rng.standard_normal(n)
+    y = O.spmv64(csr_from_dense(D), x)
+    assert np.linalg.norm(y - D @ x) <= 1e-14 * np.linalg.norm(D @ x) * 10
+
+
+def test_spmv32_componentwise_bound():
+    # |ŷ_i − y_i| ≤ γ_k (|A||x|)_i, γ_k = k u/(1 − k u), u = 2⁻²⁴ (any summation order)
+    rng = np.random.default_rng(3)
+    A = inputs.randdd(2000, 11, kmax=200)
+    a32 = A.val.astype(np.float32)
+    x32 = rng.uniform(-1, 1, A.n).astype(np.float32)
+    y = O.spmv32(A, a32, x32)
+    u = 2.0 ** -24
+    for i in range(0, A.n, 7):
+        s, e = A.row_ptr[i], A.row_ptr[i + 1]
+        prods = a32[s:e].astype(np.float64) * x32[A.col[s:e]].astype(np.float64)  # exact in fp64
+        exact = math.fsum(prods)
+        k = e - s
+        gam = k * u / (1 - k * u)
+        assert abs(float(y[i]) - exact) <= gam * np.abs(prods).sum() + 1e-45
+
+
+def test_jacobi_spmv_scales_rows():
+    # M = diag(A): M⁻¹A has unit diagonal, so M⁻¹A e_i has 1 in row i
+    D = random_dd(12, 4)
+    A = csr_from_dense(D)
+    aW, dW = O.working_copy(A, O.FP64)
+    for i in (0, 5, 11):
+        e = np.zeros(12); e[i] = 1.0
+        w = O.jacobi_spmv(O.FP64, A, aW, dW, e)
+        assert np.allclose(w, D[:, i] / np.diag(D), rtol=1e-15, atol=0)
+        assert w[i] == 1.0
+
+
+# ----------------------------------------------------------- dot / norm
+
+
+def test_dot_examples():
+    # dot([1,0],[0,1]) = 0 ; norm2([3,4]) = 5
+    assert O.dot(O.FP64, np.array([1.0, 0.0]), np.array([0.0, 1.0])) == 0.0
+    assert math.sqrt(O.dot(O.FP64, np.array([3.0, 4.0]), np.array([3.0, 4.0]))) == 5.0
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(10000).astype(np.float32)
+    y = rng.standard_normal(10000).astype(np.float32)
+    exact = math.fsum((x.astype(np.float64) * y.astype(np.float64)).tolist())
+    bound = 10000 * 2.0 ** -53 * float(np.abs(x.astype(np.float64) * y).sum())
+    assert abs(O.dot(O.MIXED, x, y) - exact) <= bound  # fp64 accumulator (reading R9)
+
+
+# ---------------------------------------------------------------- Givens
+
+
+def test_givens_examples():
+    # rot(1,0) = (1,0); rot(3,4) = (0.6,0.8), ρ = 5
+    assert O.givens(1.0, 0.0) == (1.0, 0.0, 1.0)
+    c, s, r = O.givens(3.0, 4.0)
+    assert (c, s, r) == pytest.approx((0.6, 0.8, 5.0), rel=1e-15)
+    rng = np.random.default_rng(6)
+    for a, b in rng.standard_normal((50, 2)):
+        c, s, r = O.givens(a, b)
+        assert c * c + s * s == pytest.approx(1.0, abs=1e-15)
+        assert c * a + s * b == pytest.approx(r, rel=1e-14)
+        assert -s * a + c * b == pytest.approx(0.0, abs=1e-14 * abs(r))
+
+
+def test_hess_step_matches_lstsq():
+    # |s_{j+1}| = min_y ‖β e₁ − H̄_j y‖ at every j (Prop. 6.9 cited at PAPER.md:243)
+    rng = np.random.default_rng(7)
+    m, beta = 12, 2.5
+    H = np.triu(rng.standard_normal((m + 1, m)), -1)
+    cs, sn, s = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+    s[0] = beta
+    for j in range(1, m + 1):
+        h = np.zeros(m + 1)
+        h[:j + 1] = H[:j + 1, j - 1]
+        res = O.hess_step(j, h, cs, sn, s)
+        Hj = H[:j + 1, :j]
+        rhs = np.zeros(j + 1); rhs[0] = beta
+        y, *_ = np.linalg.lstsq(Hj, rhs, rcond=None)
+        ls = np.linalg.norm(rhs - Hj @ y)
+        assert res == pytest.approx(ls, rel=1e-10, abs=1e-14)
+        assert h[j] == 0.0
+    # the rotated columns form R = Qᵀ H̄ (upper triangular): |det| and column norms preserved
+    assert np.all(np.abs(s) <= beta)
+
+
+def test_backsolve():
+    # R = [2], s = [4] → y = 2 ; random upper triangular vs LAPACK solve
+    assert np.allclose(O.backsolve(np.array([[2.0]]), np.array([4.0])), [2.0])
+    rng = np.random.default_rng(8)
+    R = np.triu(rng.standard_normal((20, 20))) + 5 * np.eye(20)
+    s = rng.standard_normal(20)
+    assert np.allclose(O.backsolve(R, s), np.linalg.solve(R, s), rtol=1e-13, atol=1e-13)
+
+
+def test_xupdate():
+    rng = np.random.default_rng(9)
+    V = rng.standard_normal((100, 7)).astype(np.float32)
+    y = rng.standard_normal(7)
+    x = rng.standard_normal(100)
+    out = O.xupdate(O.MIXED, V, y, x)
+    exact = x + V.astype(np.float64) @ y
+    assert np.allclose(out, exact, rtol=1e-14, atol=1e-14)
+
+
+# ------------------------------------------------------------- MGS / CGSR
+
+
+@pytest.mark.parametrize("proc", ["mgs", "cgsr"])
+def test_ortho_worked_examples(proc):
+    f = getattr(O, proc)
+    # V = [e₁], w = [1,1,0] → h₁ = 1, w' = [0,1,0]
+    V = np.array([[1.0], [0.0], [0.0]])
+    w, h = f(O.FP64, V, np.array([1.0, 1.0, 0.0]))
+    assert np.array_equal(w, [0.0, 1.0, 0.0]) and np.array_equal(h, [1.0])
+    # w ⟂ span(V) → h = 0, w unchanged
+    V = np.array([[1.0, 0.0], [0.0, 1.0], [0.0, 0.0], [0.0, 0.0]])
+    w0 = np.array([0.0, 0.0, 3.0, -2.0])
+    w, h = f(O.FP64, V, w0)
+    assert np.array_equal(w, w0) and np.array_equal(h, [0.0, 0.0])
+
+
+@pytest.mark.parametrize("proc", ["mgs", "cgsr"])
+@pytest.mark.parametrize("prec,tol", [(O.FP64, 1e-13), (O.MIXED, 2e-5)])
+def test_ortho_invariants(proc, prec, tol):
+    rng = np.random.default_rng(10)
+    n, j = 300, 9
+    Q, _ = np.linalg.qr(rng.standard_normal((n, j)))
+    Vw = Q.astype(O.wdtype(prec))
+    V = Vw.astype(np.float64)
+    w0 = rng.standard_normal(n).astype(O.wdtype(prec))
+    w, h = getattr(O, proc)(prec, Vw, w0)
+    w = w.astype(np.float64)
+    nw = np.linalg.norm(w0)
+    assert np.abs(V.T @ w).max() <= tol * nw                      # w' ⟂ V
+    assert np.linalg.norm(w0 - (w + V @ h)) <= tol * nw            # w = w' + V h (no dropped term)
+    assert np.linalg.norm(h - V.T @ w0.astype(np.float64)) <= tol * nw  # h = Vᵀw for orthonormal V
+
+
+def test_cgsr_reorthogonalisation_restores_orthogonality():
+    # F2: V 10×3 orthonormal, w = V c + τ g, τ = 1e-12.
+    fails1 = 0
+    for seed in range(20):
+        rng = np.random.default_rng(100 + seed)
+        V, _ = np.linalg.qr(rng.standard_normal((10, 3)))
+        c = rng.standard_normal(3); c /= np.linalg.norm(c)
+        g = rng.standard_normal(10); g /= np.linalg.norm(g)
+        w0 = V @ c + 1e-12 * g
+        w1, _ = O.cgsr(O.FP64, V, w0, passes=1)
+        w2, _ = O.cgsr(O.FP64, V, w0, passes=2)
+        fails1 += np.linalg.norm(V.T @ w1) / np.linalg.norm(w1) >= 1e-6
+        assert np.linalg.norm(V.T @ w2) <= 1e-13 * np.linalg.norm(w2)
+    assert fails1 == 20  # a single CGS pass does not restore orthogonality
+
+
+# --------------------------------------------------------------- Arnoldi
+
+
+@pytest.mark.parametrize("ortho", [O.MGS, O.CGSR])
+def test_arnoldi_relation_and_orthogonality(ortho):
+    # ‖M⁻¹A V_J − V_{J+1} H̄_J‖_F ≤ 1e-12 ‖M⁻¹A‖_F ; ‖I − VᵀV‖_max ≤ 1e-12
+    n, m = 60, 20
+    D = random_dd(n, 21)
+    A = csr_from_dense(D)
+    MA = D / np.diag(D)[:, None]
+    r = np.random.default_rng(22).standard_normal(n)
+    cyc = O.arnoldi(O.FP64, ortho, A, r, m)
+    assert cyc.J == m and not cyc.breakdown
+    V = cyc.V
+    lhs = MA @ V[:, :m]
+    rhs = V @ cyc.Hbar
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(MA)
+    loss = [np.abs(np.eye(j + 1) - V[:, :j + 1].T @ V[:, :j + 1]).max() for j in range(1, m + 1)]
+    if ortho == O.CGSR:
+        assert max(loss) <= 1e-12  # CGSR keeps orthogonality
+    else:
+        # MGS: orthogonal while the basis is well conditioned, then loses orthogonality in
+        # inverse proportion to the Arnoldi residual (Paige et al.)
+        assert all(l <= 1e-12 for l, s in zip(loss, cyc.inner) if s >= 1e-3)
+        assert max(l * s for l, s in zip(loss, cyc.inner)) <= 1e-13
+    assert np.allclose(V[:, 0], r / np.linalg.norm(r), rtol=0, atol=1e-15)
+    # per-step |s_{j+1}|/β equals the dense least-squares residual
+    beta = np.linalg.norm(r)
+    for j in range(1, m + 1):
+        Hj = cyc.Hbar[:j + 1, :j]
+        rhs = np.zeros(j + 1); rhs[0] = beta
+        y, *_ = np.linalg.lstsq(Hj, rhs, rcond=None)
+        assert cyc.inner[j - 1] * beta == pytest.approx(np.linalg.norm(rhs - Hj @ y), rel=1e-9, abs=1e-13 * beta)
+    # monotone within the cycle (BASELINE.json)
+    assert np.all(np.diff(cyc.inner) <= 1e-14 * cyc.inner[:-1])
+
+
+@pytest.mark.parametrize("ortho", [O.MGS, O.CGSR])
+def test_minimal_residual_property(ortho):
+    # u = argmin_{u ∈ K_J} ‖M⁻¹(b − A u)‖, dense LS over a numpy Krylov basis
+    n, J = 30, 6
+    D = random_dd(n, 31)
+    MA = D / np.diag(D)[:, None]
+    b = np.random.default_rng(32).standard_normal(n)
+    A = csr_from_dense(D)
+    res = O.solve(A, b, m=J, tol=1e-300, ortho=ortho, prec=O.FP64, max_cycles=1)
+    u = res.x
+    r0 = b / np.diag(D)
+    K = np.empty((n, J))
+    K[:, 0] = r0
+    for i in range(1, J):
+        K[:, i] = MA @ K[:, i - 1]
+    Q, _ = np.linalg.qr(K)
+    c, *_ = np.linalg.lstsq(MA @ Q, r0, rcond=None)
+    best = np.linalg.norm(r0 - MA @ Q @ c)
+    got = np.linalg.norm(r0 - MA @ u)
+    assert got == pytest.approx(best, rel=1e-8)
+    assert np.linalg.norm(u - Q @ c) <= 1e-8 * np.linalg.norm(u)
+
+
+# --------------------------------------------------------------- solves
+
+
+@pytest.mark.parametrize("ortho", [O.MGS, O.CGSR])
+@pytest.mark.parametrize("n,seed", [(5, 100), (10, 101), (30, 102), (64, 103), (200, 104)])
+def test_solve_matches_dense_lu(ortho, n, seed):
+    D = random_dd(n, seed)
+    xt = np.random.default_rng(seed + 1).uniform(-1, 1, n)
+    b = D @ xt
+    A = csr_from_dense(D)
+    res = O.solve(A, b, m=min(n, 30), tol=1e-12, ortho=ortho, prec=O.FP64)
+    assert res.status == O.OK
+    x_lu = np.linalg.solve(D, b)
+    assert np.linalg.norm(res.x - x_lu) <= 1e-8 * np.linalg.norm(x_lu)
+    assert np.linalg.norm(b - D @ res.x) <= 1e-10 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("ortho", [O.MGS, O.CGSR])
+def test_exact_convergence_in_n_steps(ortho):
+    # unrestarted (m ≥ n) fp64 GMRES on a tiny system terminates within n inner steps
+    for seed, n in [(200, 8), (201, 15), (202, 25)]:
+        D = random_dd(n, seed, density=0.8, plus=0.0) + np.triu(np.ones((n, n)), 1) * 0.3
+        b = np.random.default_rng(seed).standard_normal(n)
+        A = csr_from_dense(D)
+        res = O.solve(A, b, m=n, tol=1e-12, ortho=ortho, prec=O.FP64, max_cycles=1)
+        assert res.cycles == 1 and res.inner_iters <= n
+        assert np.linalg.norm(res.x - np.linalg.solve(D, b)) <= 1e-10 * np.linalg.norm(res.x)
+
+
+def test_special_cases():
+    n = 6
+    b = np.arange(1.0, n + 1)
+    # A = I → one inner step with lucky breakdown h_{2,1} = 0
+    I = csr_from_dense(np.eye(n))
+    cyc = O.arnoldi(O.FP64, O.MGS, I, b, 5)
+    assert cyc.J == 1 and cyc.breakdown and cyc.Hbar[1, 0] == 0.0
+    res = O.solve(I, b, m=5, prec=O.FP64)
+    assert res.cycles == 1 and res.inner_iters == 1 and np.allclose(res.x, b, rtol=1e-15)
+    # diagonal A with Jacobi: M⁻¹A = I → one step
+    # mixed (power-of-two diagonal so that dinv32·a32 = 1 exactly): every cycle is one
+    # inner step; the fp32 rounding of v₁ is removed by one more refinement cycle
+    Dg = csr_from_dense(np.diag([2.0, 4.0, 8.0, 0.5, 16.0, 0.25]))
+    res = O.solve(Dg, b, m=5, prec=O.MIXED)
+    assert res.status == O.OK and res.cycles == 2 and res.inner_iters == 2
+    Dg = csr_from_dense(np.diag([2.0, 4.0, 8.0, 3.0, 5.0, 7.0]))
+    res = O.solve(Dg, b, m=5, prec=O.FP64)
+    assert res.cycles == 1 and res.inner_iters == 1
+    # diag(2,4)·[1,1] = [2,4]
+    res = O.solve(csr_from_dense(np.diag([2.0, 4.0])), np.array([2.0, 4.0]), m=2, prec=O.FP64)
+    assert np.allclose(res.x, [1.0, 1.0], rtol=1e-15)
+    # b = 0 → x = 0, 0 cycles
+    P = inputs.make("C1", 8)
+    res = O.solve(P.A, np.zeros(P.A.n), m=5)
+    assert res.cycles == 0 and not res.x.any()
+    # x0 already meets tol → 0 cycles
+    res = O.solve(P.A, P.b, x0=P.x_true, m=5)
+    assert res.cycles == 0 and res.history[0] <= 1e-10
+
+
+def test_invalid_inputs():
+    D = random_dd(5, 1)
+    D[2, 2] = 0.0
+    A = csr_from_dense(D)
+    with pytest.raises(RuntimeError):
+        O.solve(A, np.ones(5), m=3)
+    with pytest.raises(ZeroDivisionError, match="row 2"):
+        O.dinv(A)
+    bad = inputs.CSR(np.array([0, 2, 3], np.int32), np.array([1, 0, 1], np.int32), np.ones(3))
+    with pytest.raises(RuntimeError):
+        O.solve(bad, np.ones(2), m=2)
+    with pytest.raises(OverflowError):
+        O.cast32(np.array([1e39]))
+
+
+# ------------------------------------------------------ mixed-precision claims
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return inputs.make("C1")
+
+
+@pytest.mark.parametrize("ortho", [O.MGS, O.CGSR])
+def test_mixed_reaches_double_accuracy(c1, ortho):
+    # fp64 residual + update, fp32 elsewhere, reaches fp64 accuracy
+    m = O.solve(c1.A, c1.b, m=30, ortho=ortho, prec=O.MIXED)
+    d = O.solve(c1.A, c1.b, m=30, ortho=ortho, prec=O.FP64)
+    assert m.status == O.OK and m.final_relres <= 1e-10
+    assert d.status == O.OK and d.final_relres <= 1e-10
+    # forced-restart regime: mixed and double take the same number of cycles
+    assert m.cycles == d.cycles
+    # iterative refinement view: ρ_K ≤ (max δ_k)^K ρ_0, slack ×10
+    h = m.history
+    dk = h[1:] / h[:-1]
+    assert np.all(dk < 1)
+    assert h[-1] <= 10 * dk.max() ** (len(h) - 1) * h[0]
+    # history matches the recomputed true residual
+    assert m.final_relres == pytest.approx(np.linalg.norm(c1.b - O.spmv64(c1.A, m.x)) / np.linalg.norm(c1.b),
+                                           rel=1e-6)
+
+
+@pytest.mark.parametrize("flags", [O.F_RESID32 | O.F_UPDATE32, O.F_RESID32, O.F_UPDATE32])
+def test_fp32_refinement_variables_cap_accuracy(c1, flags):
+    # fp32 residual or fp32 update cannot improve past single-precision accuracy
+    r = O.solve(c1.A, c1.b, m=30, ortho=O.CGSR, prec=O.MIXED, flags=flags, max_cycles=40)
+    assert r.status == O.NOT_CONVERGED
+    assert r.history.min() > 1e-8
+
+
+def test_single_cgs_pass_still_converges_in_mixed(c1):
+    # the correction variables alone in fp32 still converge: fp32 accumulators too
+    r = O.solve(c1.A, c1.b, m=30, ortho=O.MGS, prec=O.MIXED, flags=O.F_ACC32)
+    assert r.status == O.OK and r.final_relres <= 1e-10
