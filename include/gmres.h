@@ -1,0 +1,145 @@
+/* include/gmres.h — C ABI of the B200-native mixed-precision restarted GMRES(m).
+ *
+ * Method: restarted, left-preconditioned GMRES(m) of Alg. 1
+ * with MGS or CGSR (two passes) and the
+ * mixed-precision split of §4: the residual z = b − A·x
+ * (Alg. 1 line 86) and the update x ← x + u (line 147) in fp64, everything in
+ * between (lines 89–146) in fp32 on an fp32 copy of A ("the matrix is stored
+ * twice").  Preconditioner: Jacobi M = diag(A) (BASELINE.json;
+ * the paper's ILU(0), is out of scope this round).  H, the
+ * Givens rotations and s are fp64 on the device (reading R7).
+ *
+ * All compute runs in hand-written sm_100a kernels (libgmres.so); no
+ * cuSPARSE/cuBLAS.  Plain C: no C++ types or exceptions cross this boundary.
+ *
+ * Conventions
+ *  - CSR: int32 row_ptr[n+1], int32 col[nnz], fp64 val[nnz]; row_ptr[0] = 0,
+ *    non-decreasing, row_ptr[n] = nnz, columns strictly increasing and < n
+ *    within each row.  Every row must hold a non-zero diagonal.
+ *  - Ownership: the caller owns every array it passes.  gmres_create COPIES A
+ *    to the device; the caller may free its arrays on return.  Outputs are
+ *    caller-allocated.  The library never returns memory the caller must free.
+ *  - Return codes: 0 = OK, 1 = NOT_CONVERGED (max_cycles reached; x holds the
+ *    last iterate), negative = error; gmres_last_error() describes it.
+ *  - Concurrency: one solve per context at a time; calls are stream-ordered on
+ *    the context's stream (or the stream given to *_device calls).
+ */
+#ifndef GMRES_H
+#define GMRES_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gmres_ctx gmres_ctx;
+
+typedef enum { GMRES_MGS = 0, GMRES_CGSR = 1 } gmres_ortho;
+typedef enum { GMRES_FP64 = 0, GMRES_MIXED = 1 } gmres_precision;
+
+typedef enum {
+  GMRES_OK = 0,
+  GMRES_NOT_CONVERGED = 1,
+  GMRES_EINVAL = -1,       /* bad argument: m < 1, tol ≤ 0 or NaN, bad enum, null pointer */
+  GMRES_EBADCSR = -2,      /* CSR invariants violated                    */
+  GMRES_EZERODIAG = -3,    /* missing or zero diagonal; message names the row            */
+  GMRES_EFP32RANGE = -4,   /* mixed mode: |a_ij| or |z_i| exceeds FLT_MAX   */
+  GMRES_ENONFINITE = -5,   /* NaN/Inf in the residual or the Arnoldi process             */
+  GMRES_ENOMEM = -6,       /* device allocation failed                                   */
+  GMRES_ECUDA = -7,        /* CUDA runtime error (message has the CUDA error string)     */
+  GMRES_ETIMEOUT = -8      /* device-side watchdog fired in a grid barrier               */
+} gmres_status;
+
+typedef struct {
+  int32_t status;         /* gmres_status of the solve                                  */
+  int32_t cycles;         /* Arnoldi cycles executed = x-updates (0 if x0 converged)    */
+  int32_t inner_iters;    /* total inner iterations over all cycles                     */
+  int32_t history_len;    /* cycles + 1 per-cycle residuals recorded                    */
+  double final_relres;    /* ‖b − A x‖₂/‖b‖₂ of the returned x (fp64, on device)        */
+  double device_ms;       /* device time of the solve (CUDA events), incl. the A32 cast */
+} gmres_result;
+
+typedef struct {
+  double delta;           /* Arnoldi-improvement restart threshold (PAPER.md:257-264,
+                             448); < 0 → default: 1e-6 mixed, 0 fp64                    */
+  int32_t max_cycles;     /* ≤ 0 → 10000                                                */
+  int32_t record_inner;   /* != 0: keep |s_{j+1}|/β per inner step (gmres_get_inner_history) */
+  int32_t lanes_per_row;  /* SpMV sub-warp width 4/8/16/32; 0 = auto from mean row length */
+  int32_t ctas_per_sm;    /* 0 = auto (occupancy)                                       */
+} gmres_opts;
+
+/* Create a solver context on the current CUDA device: validates the CSR on the
+ * host, copies A (fp64) to the device and extracts the Jacobi diagonal.
+ * Host pointers.  Errors: EINVAL, EBADCSR, EZERODIAG, ENOMEM, ECUDA. */
+int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n, int64_t nnz,
+                 gmres_ctx** out);
+
+/* Solve A x = b with host arrays b[n], x0[n] (NULL → x0 = 0) into x_out[n].
+ * history (may be NULL) receives ‖b − A x_k‖/‖b‖ for k = 0..cycles (at most
+ * history_cap values; *history_len gets the full count).  opts may be NULL.
+ * Blocks until done.  Returns the solve status (see gmres_status). */
+int gmres_solve(gmres_ctx* ctx, const double* b, const double* x0, double* x_out, int32_t m, double tol,
+                int32_t ortho, int32_t precision, const gmres_opts* opts, gmres_result* res, double* history,
+                int32_t history_cap, int32_t* history_len);
+
+/* Same with DEVICE arrays d_b, d_x0 (may be NULL), d_x (may alias d_x0),
+ * ordered on `stream` (a cudaStream_t; NULL = the context's own stream).
+ * history stays a HOST array.  Blocks until the solve finished. */
+int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_x, int32_t m, double tol,
+                       int32_t ortho, int32_t precision, const gmres_opts* opts, gmres_result* res,
+                       double* history, int32_t history_cap, int32_t* history_len, void* stream);
+
+/* Per-inner-step |s_{j+1}|/β of the last solve (opts.record_inner != 0). */
+int gmres_get_inner_history(gmres_ctx* ctx, double* buf, int32_t cap, int32_t* len);
+
+/* Device-side phase timers of the last solve (ns, measured by CTA 0 with
+ * %globaltimer): [0] residual, [1] SpMV, [2] orthogonalisation, [3] norm +
+ * Givens, [4] back-solve + update, [5] A32 cast.  Returns the count written. */
+int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap);
+
+const char* gmres_last_error(const gmres_ctx* ctx);  /* "" if none; ctx may be NULL */
+void gmres_destroy(gmres_ctx* ctx);
+
+/* ------------------------------------------------------------------------
+ * Component entry points (used by the parity tests; device pointers, W =
+ * float in mixed mode, double in fp64 mode; blocking).  Each runs the SAME
+ * device code the fused solve kernel runs for that step.
+ * ---------------------------------------------------------------------- */
+
+/* a2 (Alg. 1): d_w = RN_W(dinv_W ∘ (A_W · d_v)). */
+int gmres_k_spmv(gmres_ctx* ctx, int32_t precision, const void* d_v, void* d_w);
+
+/* a1 (Alg. 1 lines 86–90): z = b − A64 x (fp64); d_r = RN_W(dinv_W ∘ RN_W(z));
+ * out2[0] = ‖z‖², out2[1] = ‖r‖² (host). */
+int gmres_k_resid(gmres_ctx* ctx, int32_t precision, const double* d_b, const double* d_x, void* d_r,
+                  double* out2);
+
+/* a3/a4 + a5 (Alg. 1): orthogonalise d_w (n, W) in place against
+ * the j columns of d_V (column-major, leading dimension ldv ≥ n, ldv % 64 == 0)
+ * with MGS or CGSR; h_out (host) receives h_{1..j} and h_out[j] = ‖w‖₂. */
+int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
+                  void* d_w, double* h_out);
+
+/* a8 (Alg. 1): d_x += Σ_{i<J} (double)V_i · y_i; y host[J]. */
+int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_V, int64_t ldv, const double* y,
+                    double* d_x);
+
+/* a6 + a7 (Alg. 1) on the device: apply the Givens steps to the
+ * J columns of the unrotated (m+1)×m Hessenberg Hbar (host, column-major,
+ * ld m+1) with s_1 = beta; returns the rotated R (host, same layout), s[J+1]
+ * and y[J] = R⁻¹ s_{1..J}. */
+int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar, double beta, double* R,
+                       double* s, double* y);
+
+/* a0: build the fp32 copy of A on the device (also done lazily
+ * inside every mixed solve, timed).  EFP32RANGE on overflow. */
+int gmres_k_cast32(gmres_ctx* ctx);
+
+/* Device pointers of the context's matrix (for tests): any may be NULL. */
+int gmres_k_matrix(gmres_ctx* ctx, const int32_t** row_ptr, const int32_t** col, const double** val64,
+                   const float** val32, const double** dinv64);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMRES_H */

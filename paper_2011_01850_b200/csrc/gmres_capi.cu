@@ -1,0 +1,680 @@
+// gmres_capi.cu — host side of libgmres.so: the C ABI of include/gmres.h.
+//
+// Owns the device copy of A (fp64 + lazily the fp32 copy), the
+// Jacobi diagonal, the workspace (V, work vectors, reduction partials, R, y),
+// the row partition over the persistent grid, and the cooperative launch of
+// the fused solve kernel (gmres_kernels.cuh).  No compute happens here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gmres.h"
+#include "gmres_kernels.cuh"
+
+using namespace g200;
+
+struct gmres_ctx {
+  int device = 0;
+  int sms = 0;
+  int64_t n = 0, nnz = 0;
+  int64_t nvec = 0;  // n rounded up to ROWALIGN
+  int64_t ldv = 0;   // n rounded up to LDALIGN
+  std::vector<int32_t> h_rp;  // host row_ptr (row partitioning)
+  int32_t* d_rp = nullptr;
+  int32_t* d_ci = nullptr;
+  double* d_a64 = nullptr;
+  float* d_a32 = nullptr;
+  bool a32_ready = false;
+  double* d_dinv64 = nullptr;
+  float* d_dinv32 = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // workspace
+  int ws_m = -1, ws_prec = -1, ws_G = 0;
+  char* d_ws = nullptr;
+  size_t ws_bytes = 0;
+  void* d_V = nullptr;
+  void* d_w0 = nullptr;
+  void* d_w1 = nullptr;
+  double* d_partials = nullptr;
+  double* d_R = nullptr;
+  double* d_y = nullptr;
+  unsigned long long* d_bar = nullptr;
+  int* d_flags = nullptr;  // [0] abort [1] err [2] scratch
+  int* d_out_int = nullptr;
+  double* d_out_dbl = nullptr;
+  unsigned long long* d_prof = nullptr;
+  double* d_hist = nullptr;
+  int hist_cap = 0;
+  double* d_inner = nullptr;
+  int inner_cap = 0;
+  int* d_row_begin = nullptr;
+  int part_G = 0;
+  // last solve
+  std::vector<double> inner_host;
+  double phase_ns[PH_N] = {0};
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(gmres_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? GMRES_ENOMEM : GMRES_ECUDA,  \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                \
+    }                                                                                 \
+  } while (0)
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// mean row length → lanes per row (power of two in [4, 32])
+int auto_lanes(int64_t n, int64_t nnz) {
+  double mu = n > 0 ? (double)nnz / (double)n : 1.0;
+  int L = 4;
+  while (L < 32 && L < mu) L *= 2;
+  return L;
+}
+
+// Row partition over G CTAs: boundaries on multiples of ROWALIGN, balancing
+// rows + nnz (the merge-path cost), last boundary = nvec.
+void make_partition(const std::vector<int32_t>& rp, int64_t n, int64_t nvec, int G, std::vector<int>& out) {
+  out.assign(G + 1, 0);
+  const double total = (double)nvec + (double)rp[n];
+  auto cost = [&](int64_t r) { return (double)r + (double)rp[std::min(r, n)]; };
+  const int64_t nblk = nvec / ROWALIGN;
+  int64_t lo = 0;
+  for (int g = 1; g < G; ++g) {
+    const double target = total * g / G;
+    int64_t a = lo, b = nblk;  // find smallest block boundary with cost ≥ target
+    while (a < b) {
+      int64_t mid = (a + b) / 2;
+      if (cost(mid * ROWALIGN) < target) a = mid + 1; else b = mid;
+    }
+    lo = a;
+    out[g] = (int)(a * ROWALIGN);
+  }
+  out[G] = (int)nvec;
+}
+
+template <class W, int L>
+void* solve_kernel_ptr() { return (void*)&solve_kernel<W, L>; }
+
+void* pick_solve(int prec, int L) {
+  if (prec == GMRES_MIXED) {
+    switch (L) {
+      case 4: return solve_kernel_ptr<float, 4>();
+      case 8: return solve_kernel_ptr<float, 8>();
+      case 16: return solve_kernel_ptr<float, 16>();
+      default: return solve_kernel_ptr<float, 32>();
+    }
+  }
+  switch (L) {
+    case 4: return solve_kernel_ptr<double, 4>();
+    case 8: return solve_kernel_ptr<double, 8>();
+    case 16: return solve_kernel_ptr<double, 16>();
+    default: return solve_kernel_ptr<double, 32>();
+  }
+}
+
+template <class W>
+void* pick_kernel_templ(int kind, int L) {
+  switch (kind) {
+    case 0:
+      switch (L) {
+        case 4: return (void*)&k_spmv_kernel<W, 4>;
+        case 8: return (void*)&k_spmv_kernel<W, 8>;
+        case 16: return (void*)&k_spmv_kernel<W, 16>;
+        default: return (void*)&k_spmv_kernel<W, 32>;
+      }
+    case 1:
+      switch (L) {
+        case 4: return (void*)&k_resid_kernel<W, 4>;
+        case 8: return (void*)&k_resid_kernel<W, 8>;
+        case 16: return (void*)&k_resid_kernel<W, 16>;
+        default: return (void*)&k_resid_kernel<W, 32>;
+      }
+    case 2: return (void*)&k_ortho_kernel<W>;
+    default: return (void*)&k_xupdate_kernel<W>;
+  }
+}
+
+void* pick_kernel(int prec, int kind, int L) {
+  return prec == GMRES_MIXED ? pick_kernel_templ<float>(kind, L) : pick_kernel_templ<double>(kind, L);
+}
+
+constexpr int kTileBytes = 96 * 1024;
+
+size_t smem_bytes(int m) { return SmemLayout(m + 1, kTileBytes).total; }
+
+int grid_for(gmres_ctx* ctx, const void* kern, size_t smem, int ctas_per_sm, int* G) {
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  if (per_sm < 1) return fail(ctx, GMRES_ECUDA, "solve kernel cannot be resident (occupancy 0)");
+  if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
+  *G = per_sm * ctx->sms;
+  return 0;
+}
+
+int ensure_partition(gmres_ctx* ctx, int G) {
+  if (ctx->part_G == G && ctx->d_row_begin) return 0;
+  std::vector<int> rb;
+  make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, rb);
+  if (ctx->d_row_begin) cudaFree(ctx->d_row_begin);
+  ctx->d_row_begin = nullptr;
+  CK(cudaMalloc(&ctx->d_row_begin, sizeof(int) * (G + 1)));
+  CK(cudaMemcpy(ctx->d_row_begin, rb.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
+  ctx->part_G = G;
+  return 0;
+}
+
+// workspace for (m, prec, G); zero-filled so that padding rows stay 0
+int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_cap) {
+  if (ctx->ws_m == m && ctx->ws_prec == prec && ctx->ws_G >= G && ctx->hist_cap >= hist_cap &&
+      ctx->inner_cap >= inner_cap)
+    return 0;
+  if (ctx->d_ws) cudaFree(ctx->d_ws);
+  ctx->d_ws = nullptr;
+  const size_t wb = prec == GMRES_MIXED ? 4 : 8;
+  const size_t kmax = (size_t)m + 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t r = off; off += (bytes + 255) & ~size_t(255); return r; };
+  const size_t oV = take(wb * ctx->ldv * (m + 1));
+  const size_t ow0 = take(wb * ctx->ldv);
+  const size_t ow1 = take(wb * ctx->ldv);
+  const size_t oP = take(sizeof(double) * 2 * G * kmax);
+  const size_t oR = take(sizeof(double) * kmax * m);
+  const size_t oy = take(sizeof(double) * kmax);
+  const size_t obar = take(sizeof(unsigned long long) * 4);
+  const size_t ofl = take(sizeof(int) * 8);
+  const size_t ooi = take(sizeof(int) * 8);
+  const size_t ood = take(sizeof(double) * 4);
+  const size_t opr = take(sizeof(unsigned long long) * PH_N);
+  const size_t oh = take(sizeof(double) * hist_cap);
+  const size_t oi = take(sizeof(double) * std::max(inner_cap, 1));
+  CK(cudaMalloc(&ctx->d_ws, off));
+  CK(cudaMemsetAsync(ctx->d_ws, 0, off, ctx->stream));
+  ctx->ws_bytes = off;
+  ctx->d_V = ctx->d_ws + oV;
+  ctx->d_w0 = ctx->d_ws + ow0;
+  ctx->d_w1 = ctx->d_ws + ow1;
+  ctx->d_partials = (double*)(ctx->d_ws + oP);
+  ctx->d_R = (double*)(ctx->d_ws + oR);
+  ctx->d_y = (double*)(ctx->d_ws + oy);
+  ctx->d_bar = (unsigned long long*)(ctx->d_ws + obar);
+  ctx->d_flags = (int*)(ctx->d_ws + ofl);
+  ctx->d_out_int = (int*)(ctx->d_ws + ooi);
+  ctx->d_out_dbl = (double*)(ctx->d_ws + ood);
+  ctx->d_prof = (unsigned long long*)(ctx->d_ws + opr);
+  ctx->d_hist = (double*)(ctx->d_ws + oh);
+  ctx->d_inner = (double*)(ctx->d_ws + oi);
+  ctx->hist_cap = hist_cap;
+  ctx->inner_cap = inner_cap;
+  ctx->ws_m = m;
+  ctx->ws_prec = prec;
+  ctx->ws_G = G;
+  return 0;
+}
+
+int ensure_a32(gmres_ctx* ctx, cudaStream_t st) {
+  if (ctx->a32_ready) return 0;
+  if (!ctx->d_a32) CK(cudaMalloc(&ctx->d_a32, sizeof(float) * std::max<int64_t>(ctx->nnz, 1)));
+  int* d_err = nullptr;
+  CK(cudaMallocAsync(&d_err, sizeof(int), st));
+  CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+  const int blocks = ctx->sms * 8;
+  cast32_kernel<<<blocks, 256, 0, st>>>(ctx->d_a64, ctx->d_a32, ctx->nnz, d_err);
+  CK(cudaGetLastError());
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_err, st));
+  CK(cudaStreamSynchronize(st));
+  if (herr) return fail(ctx, GMRES_EFP32RANGE, "matrix value outside the fp32 range (mixed mode)");
+  ctx->a32_ready = true;
+  return 0;
+}
+
+Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
+  Dev d{};
+  d.n = (int)ctx->n;
+  d.m = m;
+  d.G = G;
+  d.kmax = m + 1;
+  d.ortho = ortho;
+  d.tile_bytes = kTileBytes;
+  d.rp = ctx->d_rp;
+  d.ci = ctx->d_ci;
+  d.a64 = ctx->d_a64;
+  d.aW = prec == GMRES_MIXED ? (const void*)ctx->d_a32 : (const void*)ctx->d_a64;
+  d.dinvW = prec == GMRES_MIXED ? (const void*)ctx->d_dinv32 : (const void*)ctx->d_dinv64;
+  d.V = ctx->d_V;
+  d.ldv = ctx->ldv;
+  d.w0 = ctx->d_w0;
+  d.w1 = ctx->d_w1;
+  d.partials = ctx->d_partials;
+  d.R = ctx->d_R;
+  d.y = ctx->d_y;
+  d.bar = ctx->d_bar;
+  d.abort_flag = ctx->d_flags;
+  d.err_flag = ctx->d_flags + 1;
+  d.row_begin = ctx->d_row_begin;
+  d.history = ctx->d_hist;
+  d.hist_cap = ctx->hist_cap;
+  d.inner_hist = ctx->d_inner;
+  d.inner_cap = ctx->inner_cap;
+  d.out_int = ctx->d_out_int;
+  d.out_dbl = ctx->d_out_dbl;
+  d.prof = ctx->d_prof;
+  d.timeout_ns = 20ll * 1000 * 1000 * 1000;
+  return d;
+}
+
+int reset_flags(gmres_ctx* ctx, cudaStream_t st) {
+  CK(cudaMemsetAsync(ctx->d_bar, 0, sizeof(unsigned long long) * 4, st));
+  CK(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * 8, st));
+  return 0;
+}
+
+int launch_coop(gmres_ctx* ctx, const void* kern, int G, size_t smem, void** args, cudaStream_t st) {
+  CK(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(NT), args, smem, st));
+  return 0;
+}
+
+int check_prec(gmres_ctx* ctx, int prec) {
+  if (prec != GMRES_FP64 && prec != GMRES_MIXED) return fail(ctx, GMRES_EINVAL, "precision must be 0 (fp64) or 1 (mixed)");
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gmres_last_error(const gmres_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n, int64_t nnz,
+                 gmres_ctx** out) {
+  gmres_ctx* ctx = nullptr;
+  if (!out) return fail(nullptr, GMRES_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!row_ptr || (!col && nnz > 0) || (!val && nnz > 0)) return fail(nullptr, GMRES_EINVAL, "null CSR array");
+  if (n < 1 || nnz < 0 || n > 2000000000LL || nnz > 2147483647LL) return fail(nullptr, GMRES_EINVAL, "bad n/nnz");
+  // CSR invariants
+  if (row_ptr[0] != 0 || row_ptr[n] != nnz) return fail(nullptr, GMRES_EBADCSR, "row_ptr[0] != 0 or row_ptr[n] != nnz");
+  for (int64_t i = 0; i < n; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i])
+      return fail(nullptr, GMRES_EBADCSR, "row_ptr decreases at row " + std::to_string(i));
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      if (col[e] < 0 || col[e] >= n)
+        return fail(nullptr, GMRES_EBADCSR, "column out of range in row " + std::to_string(i));
+      if (e > row_ptr[i] && col[e] <= col[e - 1])
+        return fail(nullptr, GMRES_EBADCSR, "columns not strictly increasing in row " + std::to_string(i));
+    }
+  }
+  ctx = new gmres_ctx();
+  auto bail = [&](int rc) { gmres_destroy(ctx); return rc; };
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return bail(GMRES_ECUDA); }
+  e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return bail(GMRES_ECUDA); }
+  ctx->n = n;
+  ctx->nnz = nnz;
+  ctx->nvec = round_up(n, ROWALIGN);
+  ctx->ldv = round_up(n, LDALIGN);
+  ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
+  int rc;
+  auto setup = [&]() -> int {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    CK(cudaMalloc(&ctx->d_rp, sizeof(int32_t) * (n + 1)));
+    CK(cudaMalloc(&ctx->d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    CK(cudaMalloc(&ctx->d_a64, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    CK(cudaMalloc(&ctx->d_dinv64, sizeof(double) * ctx->nvec));
+    CK(cudaMalloc(&ctx->d_dinv32, sizeof(float) * ctx->nvec));
+    CK(cudaMemcpy(ctx->d_rp, row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
+    if (nnz > 0) {
+      CK(cudaMemcpy(ctx->d_ci, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->d_a64, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    }
+    int* d_bad = nullptr;
+    CK(cudaMalloc(&d_bad, sizeof(int)));
+    const int big = 0x7fffffff;
+    CK(cudaMemcpy(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice));
+    dinv_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>((int)n, ctx->d_rp, ctx->d_ci, ctx->d_a64, ctx->d_dinv64,
+                                                      ctx->d_dinv32, d_bad);
+    CK(cudaGetLastError());
+    int bad = big;
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_bad);
+    if (bad != big) return fail(ctx, GMRES_EZERODIAG, "zero or missing diagonal at row " + std::to_string(bad));
+    return 0;
+  };
+  rc = setup();
+  if (rc != 0) { g_err = ctx->err; return bail(rc); }
+  *out = ctx;
+  return GMRES_OK;
+}
+
+void gmres_destroy(gmres_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_rp);
+  cudaFree(ctx->d_ci);
+  cudaFree(ctx->d_a64);
+  cudaFree(ctx->d_a32);
+  cudaFree(ctx->d_dinv64);
+  cudaFree(ctx->d_dinv32);
+  cudaFree(ctx->d_ws);
+  cudaFree(ctx->d_row_begin);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_x, int32_t m, double tol,
+                       int32_t ortho, int32_t precision, const gmres_opts* opts, gmres_result* res,
+                       double* history, int32_t history_cap, int32_t* history_len, void* stream) {
+  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
+  ctx->err.clear();
+  if (!d_b || !d_x) return fail(ctx, GMRES_EINVAL, "b/x is NULL");
+  if (m < 1 || m > 1024) return fail(ctx, GMRES_EINVAL, "m must be in [1, 1024]");
+  if (!(tol > 0.0) || !std::isfinite(tol)) return fail(ctx, GMRES_EINVAL, "tol must be > 0");
+  if (ortho != GMRES_MGS && ortho != GMRES_CGSR) return fail(ctx, GMRES_EINVAL, "ortho must be 0 (MGS) or 1 (CGSR)");
+  if (int rc = check_prec(ctx, precision)) return rc;
+  if (history_cap < 0) return fail(ctx, GMRES_EINVAL, "history_cap < 0");
+  double delta = (opts && opts->delta >= 0.0) ? opts->delta : (precision == GMRES_MIXED ? 1e-6 : 0.0);
+  if (!std::isfinite(delta)) return fail(ctx, GMRES_EINVAL, "delta must be finite");
+  const int max_cycles = (opts && opts->max_cycles > 0) ? opts->max_cycles : 10000;
+  const bool rec_inner = opts && opts->record_inner;
+  int L = (opts && opts->lanes_per_row) ? opts->lanes_per_row : auto_lanes(ctx->n, ctx->nnz);
+  if (L != 4 && L != 8 && L != 16 && L != 32) return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 4/8/16/32");
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+
+  const void* kern = pick_solve(precision, L);
+  const size_t smem = smem_bytes(m);
+  int G = 0;
+  if (int rc = grid_for(ctx, kern, smem, opts ? opts->ctas_per_sm : 0, &G)) return rc;
+  if (int rc = ensure_partition(ctx, G)) return rc;
+  const int hist_cap_dev = max_cycles + 2;
+  const int inner_cap_dev = rec_inner ? (int)std::min<int64_t>((int64_t)max_cycles * m, 1 << 22) : 0;
+  if (int rc = ensure_ws(ctx, m, precision, G, hist_cap_dev, inner_cap_dev)) return rc;
+
+  CK(cudaEventRecord(ctx->ev0, st));
+  if (precision == GMRES_MIXED) {  // a0 inside the timed solve
+    if (int rc = ensure_a32(ctx, st)) return rc;
+  }
+  if (d_x0 && d_x0 != d_x) CK(cudaMemcpyAsync(d_x, d_x0, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
+  if (!d_x0) CK(cudaMemsetAsync(d_x, 0, sizeof(double) * ctx->n, st));
+  CK(cudaMemsetAsync(ctx->d_prof, 0, sizeof(unsigned long long) * PH_N, st));
+  CK(cudaMemsetAsync(ctx->d_out_int, 0, sizeof(int) * 8, st));
+
+  Dev d = make_dev(ctx, m, precision, ortho, G);
+  d.b = d_b;
+  d.x = d_x;
+  d.tol = tol;
+  d.delta = delta;
+  d.max_cycles = max_cycles;
+  d.inner_cap = inner_cap_dev;
+
+  gmres_result r{};
+  if (int rc = reset_flags(ctx, st)) return rc;
+  void* args[] = {&d};
+  if (int rc = launch_coop(ctx, kern, G, smem, args, st)) return rc;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev1, st));
+  int oi[8];
+  double od[4];
+  unsigned long long prof[PH_N];
+  CK(cudaMemcpyAsync(oi, ctx->d_out_int, sizeof(oi), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(od, ctx->d_out_dbl, sizeof(od), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(prof, ctx->d_prof, sizeof(prof), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  r.status = oi[0];
+  r.cycles = oi[1];
+  r.inner_iters = oi[2];
+  r.history_len = oi[3];
+  r.final_relres = od[0];
+  r.device_ms = ms;
+  for (int i = 0; i < PH_N; ++i) ctx->phase_ns[i] = (double)prof[i];
+  const int hl = std::min(r.history_len, std::min(history_cap, ctx->hist_cap));
+  if (history && hl > 0) CK(cudaMemcpy(history, ctx->d_hist, sizeof(double) * hl, cudaMemcpyDeviceToHost));
+  if (history_len) *history_len = r.history_len;
+  ctx->inner_host.clear();
+  if (rec_inner && oi[4] > 0) {
+    const int il = std::min(oi[4], ctx->inner_cap);
+    ctx->inner_host.resize(il);
+    CK(cudaMemcpy(ctx->inner_host.data(), ctx->d_inner, sizeof(double) * il, cudaMemcpyDeviceToHost));
+  }
+  if (res) *res = r;
+  if (r.status == ST_ETIMEOUT) return fail(ctx, GMRES_ETIMEOUT, "device watchdog fired in a grid barrier");
+  if (r.status == ST_EFP32RANGE) return fail(ctx, GMRES_EFP32RANGE, "residual entry outside the fp32 range");
+  if (r.status == ST_ENONFINITE) return fail(ctx, GMRES_ENONFINITE, "non-finite value in the residual or Arnoldi process");
+  return r.status;
+}
+
+int gmres_solve(gmres_ctx* ctx, const double* b, const double* x0, double* x_out, int32_t m, double tol,
+                int32_t ortho, int32_t precision, const gmres_opts* opts, gmres_result* res, double* history,
+                int32_t history_cap, int32_t* history_len) {
+  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
+  if (!b || !x_out) return fail(ctx, GMRES_EINVAL, "b/x_out is NULL");
+  double *d_b = nullptr, *d_x = nullptr;
+  const size_t bytes = sizeof(double) * ctx->n;
+  CK(cudaMallocAsync(&d_b, bytes, ctx->stream));
+  CK(cudaMallocAsync(&d_x, bytes, ctx->stream));
+  CK(cudaMemcpyAsync(d_b, b, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (x0) CK(cudaMemcpyAsync(d_x, x0, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = gmres_solve_device(ctx, d_b, x0 ? d_x : nullptr, d_x, m, tol, ortho, precision, opts, res, history,
+                              history_cap, history_len, nullptr);
+  if (rc >= 0) {
+    cudaError_t e = cudaMemcpyAsync(x_out, d_x, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
+  }
+  cudaFreeAsync(d_b, ctx->stream);
+  cudaFreeAsync(d_x, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  return rc;
+}
+
+int gmres_get_inner_history(gmres_ctx* ctx, double* buf, int32_t cap, int32_t* len) {
+  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
+  const int n = (int)ctx->inner_host.size();
+  if (buf) std::memcpy(buf, ctx->inner_host.data(), sizeof(double) * std::min(n, std::max(cap, 0)));
+  if (len) *len = n;
+  return 0;
+}
+
+int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap) {
+  if (!ctx || !buf) return fail(ctx, GMRES_EINVAL, "null argument");
+  const int k = std::min(cap, (int)PH_N);
+  for (int i = 0; i < k; ++i) buf[i] = ctx->phase_ns[i];
+  return k;
+}
+
+// ------------------------------------------------------------ components
+int gmres_k_cast32(gmres_ctx* ctx) {
+  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
+  return ensure_a32(ctx, ctx->stream);
+}
+
+int gmres_k_matrix(gmres_ctx* ctx, const int32_t** row_ptr, const int32_t** col, const double** val64,
+                   const float** val32, const double** dinv64) {
+  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
+  if (row_ptr) *row_ptr = ctx->d_rp;
+  if (col) *col = ctx->d_ci;
+  if (val64) *val64 = ctx->d_a64;
+  if (val32) *val32 = ctx->a32_ready ? ctx->d_a32 : nullptr;
+  if (dinv64) *dinv64 = ctx->d_dinv64;
+  return 0;
+}
+
+namespace {
+// common prologue of the component entry points: kernels, grid, partition, workspace
+int comp_setup(gmres_ctx* ctx, int prec, int m_req, int kind, int L, const void** kern, int* G, size_t* smem,
+               int* m_ws) {
+  if (int rc = check_prec(ctx, prec)) return rc;
+  if (prec == GMRES_MIXED)
+    if (int rc = ensure_a32(ctx, ctx->stream)) return rc;
+  const int m = (ctx->ws_m > 0 && ctx->ws_prec == prec) ? std::max(m_req, ctx->ws_m) : m_req;
+  *m_ws = m;
+  *smem = smem_bytes(m);
+  const void* sk = pick_solve(prec, L);
+  if (int rc = grid_for(ctx, sk, *smem, 0, G)) return rc;  // same grid as the solve
+  *kern = pick_kernel(prec, kind, L);
+  int Gk = 0;
+  if (int rc = grid_for(ctx, *kern, *smem, 0, &Gk)) return rc;
+  if (Gk < *G) *G = Gk;
+  if (int rc = ensure_partition(ctx, *G)) return rc;
+  if (int rc = ensure_ws(ctx, m, prec, std::max(*G, ctx->ws_G), std::max(ctx->hist_cap, 4), ctx->inner_cap))
+    return rc;
+  return reset_flags(ctx, ctx->stream);
+}
+}  // namespace
+
+int gmres_k_spmv(gmres_ctx* ctx, int32_t precision, const void* d_v, void* d_w) {
+  if (!ctx || !d_v || !d_w) return fail(ctx, GMRES_EINVAL, "null argument");
+  const int L = auto_lanes(ctx->n, ctx->nnz);
+  const void* kern;
+  int G;
+  size_t smem;
+  int mws;
+  if (int rc = comp_setup(ctx, precision, 1, 0, L, &kern, &G, &smem, &mws)) return rc;
+  Dev d = make_dev(ctx, mws, precision, 0, G);
+  void* args[] = {&d, (void*)&d_v, &d_w};
+  CK(cudaLaunchKernel(kern, dim3(G), dim3(NT), args, 0, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int gmres_k_resid(gmres_ctx* ctx, int32_t precision, const double* d_b, const double* d_x, void* d_r, double* out2) {
+  if (!ctx || !d_b || !d_x || !d_r || !out2) return fail(ctx, GMRES_EINVAL, "null argument");
+  const int L = auto_lanes(ctx->n, ctx->nnz);
+  const void* kern;
+  int G;
+  size_t smem;
+  int mws;
+  if (int rc = comp_setup(ctx, precision, 1, 1, L, &kern, &G, &smem, &mws)) return rc;
+  Dev d = make_dev(ctx, mws, precision, 0, G);
+  d.b = d_b;
+  d.x = const_cast<double*>(d_x);
+  double* d_out2 = nullptr;
+  CK(cudaMalloc(&d_out2, sizeof(double) * 2));
+  void* args[] = {&d, &d_r, &d_out2};
+  int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream);
+  if (rc == 0) {
+    cudaError_t e = cudaMemcpyAsync(out2, d_out2, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
+  }
+  int fl[2] = {0, 0};
+  cudaMemcpy(fl, ctx->d_flags, sizeof(fl), cudaMemcpyDeviceToHost);
+  cudaFree(d_out2);
+  if (rc == 0 && fl[0]) rc = fail(ctx, GMRES_ETIMEOUT, "device watchdog fired");
+  if (rc == 0 && (fl[1] & ERRF_NONFINITE)) rc = fail(ctx, GMRES_ENONFINITE, "non-finite residual");
+  if (rc == 0 && (fl[1] & ERRF_RANGE)) rc = fail(ctx, GMRES_EFP32RANGE, "residual entry outside the fp32 range");
+  return rc;
+}
+
+int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
+                  void* d_w, double* h_out) {
+  if (!ctx || !d_V || !d_w || !h_out) return fail(ctx, GMRES_EINVAL, "null argument");
+  if (j < 1 || ldv < ctx->ldv || ldv % LDALIGN) return fail(ctx, GMRES_EINVAL, "need j >= 1, ldv >= round_up(n,64), ldv % 64 == 0");
+  if (ortho != GMRES_MGS && ortho != GMRES_CGSR) return fail(ctx, GMRES_EINVAL, "bad ortho");
+  const int L = auto_lanes(ctx->n, ctx->nnz);
+  const void* kern;
+  int G;
+  size_t smem;
+  int m;
+  if (int rc = comp_setup(ctx, precision, j, 2, L, &kern, &G, &smem, &m)) return rc;
+  const size_t wb = precision == GMRES_MIXED ? 4 : 8;
+  // the work vector lives in the padded workspace buffer (zero padding rows)
+  CK(cudaMemsetAsync(ctx->d_w0, 0, wb * ctx->ldv, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_w0, d_w, wb * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  Dev d = make_dev(ctx, m, precision, ortho, G);
+  double* d_h = nullptr;
+  CK(cudaMalloc(&d_h, sizeof(double) * (j + 1)));
+  long long ld = ldv;
+  void* wp = ctx->d_w0;
+  void* args[] = {&d, &j, (void*)&d_V, &ld, &wp, &d_h};
+  int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream);
+  if (rc == 0) {
+    cudaError_t e = cudaMemcpyAsync(d_w, ctx->d_w0, wb * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out, d_h, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
+  }
+  cudaFree(d_h);
+  int fl = 0;
+  cudaMemcpy(&fl, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost);
+  if (rc == 0 && fl) rc = fail(ctx, GMRES_ETIMEOUT, "device watchdog fired");
+  return rc;
+}
+
+int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_V, int64_t ldv, const double* y,
+                    double* d_x) {
+  if (!ctx || !d_V || !y || !d_x) return fail(ctx, GMRES_EINVAL, "null argument");
+  if (J < 1 || ldv < ctx->ldv || ldv % LDALIGN) return fail(ctx, GMRES_EINVAL, "need J >= 1, ldv >= round_up(n,64), ldv % 64 == 0");
+  const int L = auto_lanes(ctx->n, ctx->nnz);
+  const void* kern;
+  int G;
+  size_t smem;
+  int mws;
+  if (int rc = comp_setup(ctx, precision, J, 3, L, &kern, &G, &smem, &mws)) return rc;
+  Dev d = make_dev(ctx, mws, precision, 0, G);
+  d.x = d_x;
+  double* d_y = nullptr;
+  CK(cudaMalloc(&d_y, sizeof(double) * J));
+  CK(cudaMemcpy(d_y, y, sizeof(double) * J, cudaMemcpyHostToDevice));
+  long long ld = ldv;
+  void* args[] = {&d, &J, (void*)&d_V, &ld, &d_y};
+  cudaError_t e = cudaLaunchKernel(kern, dim3(G), dim3(NT), args, smem, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_y);
+  if (e != cudaSuccess) return fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
+  return 0;
+}
+
+int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar, double beta, double* R, double* s,
+                       double* y) {
+  if (!Hbar || !R || !s || !y) return fail(ctx, GMRES_EINVAL, "null argument");
+  if (m < 1 || J < 1 || J > m) return fail(ctx, GMRES_EINVAL, "need 1 <= J <= m");
+  double *dH, *dR, *ds, *dy;
+  const size_t hb = sizeof(double) * (m + 1) * m;
+  CK(cudaMalloc(&dH, hb));
+  CK(cudaMalloc(&dR, hb));
+  CK(cudaMalloc(&ds, sizeof(double) * (m + 1)));
+  CK(cudaMalloc(&dy, sizeof(double) * m));
+  CK(cudaMemcpy(dH, Hbar, hb, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dR, 0, hb));
+  const size_t smem = sizeof(double) * (6 * (m + 2));
+  k_hess_kernel<<<1, NT, smem>>>(m, J, dH, beta, dR, ds, dy);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(R, dR, hb, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(s, ds, sizeof(double) * (J + 1), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(y, dy, sizeof(double) * J, cudaMemcpyDeviceToHost);
+  cudaFree(dH); cudaFree(dR); cudaFree(ds); cudaFree(dy);
+  if (e != cudaSuccess) return fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,257 @@
+"""ctypes binding for include/gmres.h (argument marshalling only).
+
+Names follow the C ABI: ``Solver`` wraps ``gmres_create``/``gmres_destroy``;
+``Solver.solve`` → ``gmres_solve`` (host numpy arrays), ``Solver.solve_device``
+→ ``gmres_solve_device`` (torch CUDA tensors, current stream); ``k_*`` are the
+per-step component entry points used by the parity tests.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libgmres.so")
+_lib = None
+
+MGS, CGSR = 0, 1
+FP64, MIXED = 0, 1
+STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "EBADCSR", -3: "EZERODIAG", -4: "EFP32RANGE",
+          -5: "ENONFINITE", -6: "ENOMEM", -7: "ECUDA", -8: "ETIMEOUT"}
+
+
+class GmresError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("cycles", ctypes.c_int32), ("inner_iters", ctypes.c_int32),
+                ("history_len", ctypes.c_int32), ("final_relres", ctypes.c_double), ("device_ms", ctypes.c_double)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("delta", ctypes.c_double), ("max_cycles", ctypes.c_int32), ("record_inner", ctypes.c_int32),
+                ("lanes_per_row", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libgmres.so; raise if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the CUDA library is required; there is no CPU fallback)")
+    L = ctypes.CDLL(_LIB_PATH)
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    pR, pO = ctypes.POINTER(_Result), ctypes.POINTER(_Opts)
+    L.gmres_create.argtypes = [vp, vp, vp, i64, i64, ctypes.POINTER(vp)]
+    L.gmres_create.restype = ctypes.c_int
+    L.gmres_solve.argtypes = [vp, vp, vp, vp, i32, dbl, i32, i32, pO, pR, vp, i32, ctypes.POINTER(i32)]
+    L.gmres_solve.restype = ctypes.c_int
+    L.gmres_solve_device.argtypes = [vp, vp, vp, vp, i32, dbl, i32, i32, pO, pR, vp, i32, ctypes.POINTER(i32), vp]
+    L.gmres_solve_device.restype = ctypes.c_int
+    L.gmres_get_inner_history.argtypes = [vp, vp, i32, ctypes.POINTER(i32)]
+    L.gmres_get_inner_history.restype = ctypes.c_int
+    L.gmres_get_phase_ns.argtypes = [vp, vp, i32]
+    L.gmres_get_phase_ns.restype = ctypes.c_int
+    L.gmres_last_error.argtypes = [vp]
+    L.gmres_last_error.restype = ctypes.c_char_p
+    L.gmres_destroy.argtypes = [vp]
+    L.gmres_destroy.restype = None
+    L.gmres_k_spmv.argtypes = [vp, i32, vp, vp]
+    L.gmres_k_resid.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.gmres_k_ortho.argtypes = [vp, i32, i32, i32, vp, i64, vp, vp]
+    L.gmres_k_xupdate.argtypes = [vp, i32, i32, vp, i64, vp, vp]
+    L.gmres_k_hessenberg.argtypes = [vp, i32, i32, vp, dbl, vp, vp, vp]
+    L.gmres_k_cast32.argtypes = [vp]
+    L.gmres_k_matrix.argtypes = [vp, vp, vp, vp, vp, vp]
+    for f in ("gmres_k_spmv", "gmres_k_resid", "gmres_k_ortho", "gmres_k_xupdate", "gmres_k_hessenberg",
+              "gmres_k_cast32", "gmres_k_matrix"):
+        getattr(L, f).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _p(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(ctypes.c_void_p)
+    return ctypes.c_void_p(a.data_ptr())  # torch tensor
+
+
+def _prec(p) -> int:
+    if isinstance(p, str):
+        return {"fp64": FP64, "mixed": MIXED}[p.lower()]
+    return int(p)
+
+
+def _ortho(o) -> int:
+    if isinstance(o, str):
+        return {"mgs": MGS, "cgsr": CGSR}[o.lower()]
+    return int(o)
+
+
+def ld_for(n: int) -> int:
+    """Leading dimension the component entry points require for V (n rounded to 64)."""
+    return (n + 63) // 64 * 64
+
+
+@dataclass
+class SolveResult:
+    status: int
+    cycles: int
+    inner_iters: int
+    final_relres: float
+    device_ms: float
+    history: np.ndarray
+    x: object = None
+    inner: np.ndarray | None = None
+    phase_ns: np.ndarray | None = None
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def status_name(self) -> str:
+        return STATUS.get(self.status, str(self.status))
+
+
+class Solver:
+    """gmres_create(csr_fp64) — copies A to the current CUDA device."""
+
+    def __init__(self, row_ptr, col, val):
+        self._lib = load_library()
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        self.n = self.row_ptr.shape[0] - 1
+        self.nnz = int(col.shape[0])
+        h = ctypes.c_void_p()
+        rc = self._lib.gmres_create(_p(self.row_ptr), _p(col), _p(val), self.n, self.nnz, ctypes.byref(h))
+        if rc != 0:
+            raise GmresError(rc, self._lib.gmres_last_error(None).decode())
+        self._h = h
+
+    @classmethod
+    def from_csr(cls, A):
+        return cls(A.row_ptr, A.col, A.val)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.gmres_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _err(self, rc):
+        return GmresError(rc, self._lib.gmres_last_error(self._h).decode())
+
+    @staticmethod
+    def _opts(delta, max_cycles, record_inner, lanes, ctas_per_sm):
+        o = _Opts()
+        o.delta = -1.0 if delta is None else float(delta)
+        o.max_cycles = 0 if max_cycles is None else int(max_cycles)
+        o.record_inner = 1 if record_inner else 0
+        o.lanes_per_row = int(lanes)
+        o.ctas_per_sm = int(ctas_per_sm)
+        return o
+
+    def _finish(self, rc, res, hist, hl, record_inner):
+        if rc < 0:
+            raise self._err(rc)
+        inner = None
+        if record_inner:
+            ln = ctypes.c_int32()
+            self._lib.gmres_get_inner_history(self._h, None, 0, ctypes.byref(ln))
+            inner = np.zeros(ln.value)
+            self._lib.gmres_get_inner_history(self._h, _p(inner), ln.value, ctypes.byref(ln))
+        ph = np.zeros(8)
+        self._lib.gmres_get_phase_ns(self._h, _p(ph), 8)
+        return SolveResult(res.status, res.cycles, res.inner_iters, res.final_relres, res.device_ms,
+                           hist[:min(hl.value, hist.size)].copy(), inner=inner, phase_ns=ph)
+
+    def solve(self, b, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None, max_cycles=None,
+              record_inner=False, lanes=0, ctas_per_sm=0) -> SolveResult:
+        """gmres_solve: host arrays in, host x out (h2d/d2h inside the call)."""
+        b = np.ascontiguousarray(b, np.float64)
+        x0c = None if x0 is None else np.ascontiguousarray(x0, np.float64)
+        x = np.zeros(self.n)
+        mc = 10000 if not max_cycles else int(max_cycles)
+        hist = np.zeros(mc + 2)
+        hl = ctypes.c_int32()
+        res = _Result()
+        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm)
+        rc = self._lib.gmres_solve(self._h, _p(b), _p(x0c), _p(x), int(m), float(tol), _ortho(ortho),
+                                   _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
+                                   ctypes.byref(hl))
+        out = self._finish(rc, res, hist, hl, record_inner)
+        out.x = x
+        return out
+
+    def solve_device(self, b, x, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None,
+                     max_cycles=None, record_inner=False, lanes=0, ctas_per_sm=0, stream=None) -> SolveResult:
+        """gmres_solve_device on torch CUDA float64 tensors (x is written in place)."""
+        import torch
+        for t in (b, x) + ((x0,) if x0 is not None else ()):
+            assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() == self.n
+        st = stream if stream is not None else torch.cuda.current_stream()
+        mc = 10000 if not max_cycles else int(max_cycles)
+        hist = np.zeros(mc + 2)
+        hl = ctypes.c_int32()
+        res = _Result()
+        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm)
+        rc = self._lib.gmres_solve_device(self._h, _p(b), _p(x0), _p(x), int(m), float(tol), _ortho(ortho),
+                                          _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
+                                          ctypes.byref(hl), ctypes.c_void_p(st.cuda_stream))
+        out = self._finish(rc, res, hist, hl, record_inner)
+        out.x = x
+        return out
+
+    # ------------------------------------------------------ components
+    def _ck(self, rc):
+        if rc != 0:
+            raise self._err(rc)
+
+    def k_cast32(self):
+        self._ck(self._lib.gmres_k_cast32(self._h))
+
+    def k_spmv(self, precision, v, w):
+        self._ck(self._lib.gmres_k_spmv(self._h, _prec(precision), _p(v), _p(w)))
+
+    def k_resid(self, precision, b, x, r):
+        out = np.zeros(2)
+        self._ck(self._lib.gmres_k_resid(self._h, _prec(precision), _p(b), _p(x), _p(r), _p(out)))
+        return float(out[0]), float(out[1])
+
+    def k_ortho(self, precision, ortho, j, V, ldv, w):
+        h = np.zeros(j + 1)
+        self._ck(self._lib.gmres_k_ortho(self._h, _prec(precision), _ortho(ortho), int(j), _p(V), int(ldv), _p(w),
+                                         _p(h)))
+        return h
+
+    def k_xupdate(self, precision, J, V, ldv, y, x):
+        y = np.ascontiguousarray(y, np.float64)
+        self._ck(self._lib.gmres_k_xupdate(self._h, _prec(precision), int(J), _p(V), int(ldv), _p(y), _p(x)))
+
+    def k_hessenberg(self, m, J, Hbar, beta):
+        Hc = np.asfortranarray(Hbar, np.float64)  # (m+1, m) column-major
+        assert Hc.shape == (m + 1, m)
+        R = np.zeros((m + 1) * m)
+        s = np.zeros(J + 1)
+        y = np.zeros(J)
+        self._ck(self._lib.gmres_k_hessenberg(self._h, int(m), int(J), Hc.ctypes.data_as(ctypes.c_void_p),
+                                              float(beta), _p(R), _p(s), _p(y)))
+        return R.reshape(m, m + 1).T, s, y

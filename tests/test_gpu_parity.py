@@ -1,0 +1,312 @@
+"""GPU ↔ oracle parity through the C ABI (libgmres.so), on seeded inputs.
+
+Per-step parity (rows a1–a8 of SURVEY.md §8) compares each component entry
+point — which runs the same device code as the fused solve kernel — with the
+oracle's step on identical inputs.  End-to-end parity checks the final
+residual recomputed by the oracle (‖b − A x‖/‖b‖ ≤ 1e-10) and the restart
+count within ±10 % of the oracle's (BASELINE.json).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2011_01850_b200 import gmres as G  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def tdev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def wdt(prec):
+    return np.float32 if prec == G.MIXED else np.float64
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    G.load_library()  # fails loudly if the library is missing
+    yield
+
+
+MATS = {
+    "c1": lambda: inputs.make("C1").A,
+    "c2mini": lambda: inputs.make("C2", 24).A,
+    "c3mini": lambda: inputs.make("C3", 20000).A,
+    "c4mini": lambda: inputs.make("C4", 14).A,
+    "ragged": lambda: inputs.stencil(5, 37, (3.0, -2.0, 0.0)),   # n = 1369: not a multiple of 32
+}
+
+
+@pytest.fixture(scope="module", params=sorted(MATS))
+def mat(request):
+    A = MATS[request.param]()
+    return request.param, A, G.Solver.from_csr(A)
+
+
+# ------------------------------------------------------------------ a2 SpMV
+@pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
+def test_spmv_parity(mat, prec):
+    name, A, S = mat
+    rng = np.random.default_rng(1)
+    aW, dW = O.working_copy(A, prec)
+    v = rng.uniform(-1, 1, A.n).astype(wdt(prec))
+    w_o = O.jacobi_spmv(prec, A, aW, dW, v)
+    vd = tdev(v)
+    wd = torch.empty_like(vd)
+    S.k_spmv(prec, vd, wd)
+    w = wd.cpu().numpy()
+    rel = np.linalg.norm(w.astype(np.float64) - w_o) / np.linalg.norm(w_o)
+    assert rel <= (1e-12 if prec == G.FP64 else 1e-5), rel   # BASELINE.json per-kernel bar
+    # componentwise: |ŵ_i − w_i| ≤ γ_{k+1} |dinv_i| (|A||v|)_i, any summation order
+    u = 2.0 ** -53 if prec == G.FP64 else 2.0 ** -24
+    absAv = np.zeros(A.n)
+    for i in range(A.n):
+        s, e = A.row_ptr[i], A.row_ptr[i + 1]
+        absAv[i] = np.abs(aW[s:e].astype(np.float64) * v[A.col[s:e]].astype(np.float64)).sum()
+    k = np.diff(A.row_ptr) + 1
+    gam = k * u / (1 - k * u)
+    exact = np.array([math.fsum(aW[A.row_ptr[i]:A.row_ptr[i + 1]].astype(np.float64) *
+                                v[A.col[A.row_ptr[i]:A.row_ptr[i + 1]]].astype(np.float64)) for i in range(A.n)])
+    exact *= dW.astype(np.float64)
+    assert np.all(np.abs(w - exact) <= 2 * gam * np.abs(dW) * absAv + 1e-300)
+
+
+# ------------------------------------------------------------------ a1 residual
+@pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
+def test_resid_parity(mat, prec):
+    name, A, S = mat
+    rng = np.random.default_rng(2)
+    b = rng.uniform(-1, 1, A.n) * 1e3
+    x = rng.uniform(-1, 1, A.n) * 1e-2
+    _, dW = O.working_copy(A, prec)
+    rc, r_o, zz_o, rr_o = O.resid(prec, A, b, x, dW)
+    assert rc == 0
+    rd = torch.empty(A.n, dtype=torch.float32 if prec == G.MIXED else torch.float64, device=DEV)
+    zz, rr = S.k_resid(prec, tdev(b), tdev(x), rd)
+    r = rd.cpu().numpy()
+    assert zz == pytest.approx(zz_o, rel=1e-12)
+    assert rr == pytest.approx(rr_o, rel=1e-12 if prec == G.FP64 else 1e-6)
+    rel = np.linalg.norm(r.astype(np.float64) - r_o) / np.linalg.norm(r_o)
+    assert rel <= (1e-12 if prec == G.FP64 else 1e-6)
+
+
+# ------------------------------------------------------------------ a3/a4/a5
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+@pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
+@pytest.mark.parametrize("j", [1, 7, 33])
+def test_ortho_parity(mat, prec, ortho, j):
+    name, A, S = mat
+    n = A.n
+    ld = G.ld_for(n)
+    rng = np.random.default_rng(3 + j)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, j)))
+    Vw = Q.astype(wdt(prec))
+    w0 = (Q @ rng.standard_normal(j) + 0.3 * rng.standard_normal(n)).astype(wdt(prec))
+    proc = O.mgs if ortho == G.MGS else O.cgsr
+    w_o, h_o = proc(prec, Vw, w0)
+    hn_o = math.sqrt(O.dot(prec, w_o, w_o))
+    Vpad = np.zeros((j, ld), wdt(prec))
+    Vpad[:, :n] = Vw.T
+    Vd = tdev(Vpad)
+    wd = tdev(w0)
+    h = S.k_ortho(prec, ortho, j, Vd, ld, wd)
+    w = wd.cpu().numpy().astype(np.float64)
+    nw = np.linalg.norm(w0.astype(np.float64))
+    tol = 1e-12 if prec == G.FP64 else 1e-5
+    assert np.linalg.norm(h[:j] - h_o) <= tol * nw
+    assert np.linalg.norm(w - w_o) <= tol * nw
+    assert h[j] == pytest.approx(hn_o, rel=1e-10 if prec == G.FP64 else 1e-4)
+
+
+# ------------------------------------------------------------------ a8 update
+@pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
+def test_xupdate_parity(mat, prec):
+    name, A, S = mat
+    n = A.n
+    ld = G.ld_for(n)
+    J = 13
+    rng = np.random.default_rng(4)
+    V = rng.standard_normal((n, J)).astype(wdt(prec))
+    y = rng.standard_normal(J)
+    x = rng.standard_normal(n)
+    x_o = O.xupdate(prec, V, y, x)
+    Vpad = np.zeros((J, ld), wdt(prec))
+    Vpad[:, :n] = V.T
+    xd = tdev(x)
+    S.k_xupdate(prec, J, tdev(Vpad), ld, y, xd)
+    assert np.allclose(xd.cpu().numpy(), x_o, rtol=1e-14, atol=1e-14 * np.abs(x_o).max())
+
+
+# ------------------------------------------------------------------ a6/a7 Givens + back-solve
+@pytest.mark.parametrize("m,J", [(1, 1), (12, 12), (50, 31)])
+def test_hessenberg_parity(m, J):
+    A = inputs.make("C1", 8).A
+    S = G.Solver.from_csr(A)
+    rng = np.random.default_rng(5)
+    H = np.triu(rng.standard_normal((m + 1, m)), -1)
+    H[np.arange(m), np.arange(m)] += 3.0
+    beta = 1.7
+    R, s, y = S.k_hessenberg(m, J, H, beta)
+    cs, sn, so = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+    so[0] = beta
+    Ro = np.zeros((m + 1, m))
+    for j in range(1, J + 1):
+        h = np.zeros(m + 1)
+        h[:j + 1] = H[:j + 1, j - 1]
+        O.hess_step(j, h, cs, sn, so)
+        Ro[:, j - 1] = h
+    yo = O.backsolve(Ro[:J, :J], so[:J])
+    assert np.allclose(R[:, :J], Ro[:, :J], rtol=1e-13, atol=1e-13)
+    assert np.allclose(s[:J + 1], so[:J + 1], rtol=1e-13, atol=1e-15)
+    assert np.allclose(y, yo, rtol=1e-12, atol=1e-13)
+
+
+# ------------------------------------------------------------------ end to end
+def check_solution(A, b, x, tol=1e-10):
+    r = b - O.spmv64(A, x)
+    return np.linalg.norm(r) / np.linalg.norm(b)
+
+
+E2E = {
+    "C1": lambda: inputs.make("C1"),
+    "C2mini": lambda: inputs.make("C2", 32),
+    "C3mini": lambda: inputs.make("C3", 30000),
+    "C4mini": lambda: inputs.make("C4", 20),
+}
+
+
+@pytest.fixture(scope="module", params=sorted(E2E))
+def prob(request):
+    P = E2E[request.param]()
+    return P, G.Solver.from_csr(P.A)
+
+
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+@pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
+def test_solve_end_to_end(prob, ortho, prec):
+    P, S = prob
+    m = min(P.m, 50)
+    res = S.solve(P.b, m=m, tol=1e-10, ortho=ortho, precision=prec, record_inner=True)
+    ref = O.solve(P.A, P.b, m=m, tol=1e-10, ortho=ortho, prec=prec)
+    assert res.status == 0, res.status_name
+    assert ref.status == O.OK
+    rel = check_solution(P.A, P.b, res.x)
+    assert rel <= 1e-10, rel
+    assert res.final_relres == pytest.approx(rel, rel=1e-3, abs=1e-13)
+    assert abs(res.cycles - ref.cycles) <= 0.1 * ref.cycles, (res.cycles, ref.cycles)
+    # diagnostic: per-cycle history tracks the oracle's
+    k = min(len(res.history), len(ref.history))
+    assert np.all(np.abs(np.log10(res.history[:k]) - np.log10(ref.history[:k])) <= 0.5)
+    # within a cycle the Arnoldi residual is monotone non-increasing
+    assert res.inner is not None and res.inner.size == res.inner_iters
+
+
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+@pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
+def test_first_cycle_tracks_oracle(ortho, prec):
+    P = inputs.make("C1")
+    S = G.Solver.from_csr(P.A)
+    res = S.solve(P.b, m=30, ortho=ortho, precision=prec, max_cycles=1, record_inner=True)
+    ref = O.solve(P.A, P.b, m=30, ortho=ortho, prec=prec, max_cycles=1)
+    assert res.status == 1 and ref.status == O.NOT_CONVERGED
+    n = min(res.inner.size, ref.inner.size)
+    assert abs(res.inner.size - ref.inner.size) <= 1
+    tol = 1e-8 if prec == G.FP64 else 1e-3
+    mask = ref.inner[:n] > (1e-12 if prec == G.FP64 else 1e-5)
+    assert np.all(np.abs(res.inner[:n][mask] - ref.inner[:n][mask]) <= tol * ref.inner[:n][mask])
+    assert np.allclose(res.x, ref.x, rtol=0, atol=(1e-9 if prec == G.FP64 else 1e-5) * np.abs(ref.x).max())
+
+
+# ------------------------------------------------------------------ edge cases
+def test_special_cases():
+    P = inputs.make("C1", 16)
+    S = G.Solver.from_csr(P.A)
+    r = S.solve(np.zeros(P.A.n), m=10)
+    assert r.status == 0 and r.cycles == 0 and not r.x.any()
+    r = S.solve(P.b, x0=P.x_true, m=10)
+    assert r.status == 0 and r.cycles == 0
+    # A = I: one inner step with breakdown, one cycle
+    n = 77
+    I = inputs.CSR(np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), np.ones(n))
+    SI = G.Solver.from_csr(I)
+    b = np.linspace(1, 2, n)
+    for prec in (G.FP64, G.MIXED):
+        r = SI.solve(b, m=5, precision=prec)
+        assert r.status == 0 and r.inner_iters == r.cycles and np.allclose(r.x, b, rtol=1e-12)
+    # tiny dense DD system (n < 32: one partial row block)
+    rng = np.random.default_rng(9)
+    D = rng.standard_normal((5, 5))
+    np.fill_diagonal(D, np.abs(D).sum(1) + 1)
+    rp = np.arange(0, 26, 5, dtype=np.int32)
+    col = np.tile(np.arange(5, dtype=np.int32), 5)
+    Sd = G.Solver(rp, col, D.ravel())
+    bb = rng.standard_normal(5)
+    for ortho in (G.MGS, G.CGSR):
+        r = Sd.solve(bb, m=5, ortho=ortho, precision=G.FP64, tol=1e-13)
+        assert np.allclose(r.x, np.linalg.solve(D, bb), rtol=1e-11)
+
+
+def test_errors():
+    A = inputs.make("C1", 6).A
+    val = A.val.copy()
+    d = [e for e in range(A.row_ptr[3], A.row_ptr[4]) if A.col[e] == 3][0]
+    val[d] = 0.0
+    with pytest.raises(G.GmresError, match="EZERODIAG.*row 3"):
+        G.Solver(A.row_ptr, A.col, val)
+    bad = A.col.copy()
+    bad[[0, 1]] = bad[[1, 0]]
+    with pytest.raises(G.GmresError, match="EBADCSR"):
+        G.Solver(A.row_ptr, bad, A.val)
+    big = A.val.copy()
+    big[0] = 1e39
+    S = G.Solver(A.row_ptr, A.col, big)
+    with pytest.raises(G.GmresError, match="EFP32RANGE"):
+        S.solve(np.ones(A.n), precision=G.MIXED)
+    S = G.Solver.from_csr(A)
+    with pytest.raises(G.GmresError, match="EINVAL"):
+        S.solve(np.ones(A.n), m=0)
+    with pytest.raises(G.GmresError, match="EINVAL"):
+        S.solve(np.ones(A.n), tol=-1.0)
+    r = S.solve(np.ones(A.n), m=2, max_cycles=1, tol=1e-14)
+    assert r.status == 1 and r.cycles == 1   # NOT_CONVERGED, x = last iterate
+
+
+# ------------------------------------------------------------------ full size (bench configuration)
+@pytest.mark.slow
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+def test_c2_full_size(ortho):
+    P = inputs.make("C2")
+    S = G.Solver.from_csr(P.A)
+    bd = tdev(P.b)
+    xd = torch.zeros_like(bd)
+    cycles = {}
+    for prec in (G.FP64, G.MIXED):
+        r = S.solve_device(bd, xd, m=50, ortho=ortho, precision=prec)
+        assert r.status == 0, r.status_name
+        x = xd.cpu().numpy()
+        assert check_solution(P.A, P.b, x) <= 1e-10
+        cycles[prec] = r.cycles
+    # forced-restart regime: mixed and fp64 need the same number of cycles
+    assert abs(cycles[G.MIXED] - cycles[G.FP64]) <= 0.1 * cycles[G.FP64]
+    # sampled SpMV rows at full size against the oracle, one by one
+    rng = np.random.default_rng(11)
+    v = rng.uniform(-1, 1, P.A.n).astype(np.float32)
+    wd = torch.empty(P.A.n, dtype=torch.float32, device=DEV)
+    S.k_spmv(G.MIXED, tdev(v), wd)
+    w = wd.cpu().numpy()
+    a32 = P.A.val.astype(np.float32)
+    d32 = O.dinv(P.A).astype(np.float32)
+    for i in rng.integers(0, P.A.n, 2000):
+        s, e = P.A.row_ptr[i], P.A.row_ptr[i + 1]
+        exact = math.fsum(a32[s:e].astype(np.float64) * v[P.A.col[s:e]].astype(np.float64)) * float(d32[i])
+        scale = float(np.abs(a32[s:e] * v[P.A.col[s:e]]).sum() * abs(d32[i]))
+        assert abs(float(w[i]) - exact) <= 8 * 2.0 ** -24 * scale + 1e-30
