@@ -57,6 +57,7 @@ typedef struct {
   int32_t history_len;    /* cycles + 1 per-cycle residuals recorded                    */
   double final_relres;    /* ‖b − A x‖₂/‖b‖₂ of the returned x (fp64, on device)        */
   double device_ms;       /* device time of the solve (CUDA events), incl. the A32 cast */
+  double kernel_ms;       /* device time of the fused solve kernel alone (CUDA events)  */
 } gmres_result;
 
 typedef struct {
@@ -66,6 +67,7 @@ typedef struct {
   int32_t record_inner;   /* != 0: keep |s_{j+1}|/β per inner step (gmres_get_inner_history) */
   int32_t lanes_per_row;  /* SpMV sub-warp width 4/8/16/32; 0 = auto from mean row length */
   int32_t ctas_per_sm;    /* 0 = auto (occupancy)                                       */
+  int32_t profile;        /* != 0: grid barrier after each phase for clean phase timers */
 } gmres_opts;
 
 /* Create a solver context on the current CUDA device: validates the CSR on the
@@ -92,9 +94,13 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
 /* Per-inner-step |s_{j+1}|/β of the last solve (opts.record_inner != 0). */
 int gmres_get_inner_history(gmres_ctx* ctx, double* buf, int32_t cap, int32_t* len);
 
+/* Inner iterations J_k of every cycle k of the last solve (for byte models). */
+int gmres_get_cycle_iters(gmres_ctx* ctx, int32_t* buf, int32_t cap, int32_t* len);
+
 /* Device-side phase timers of the last solve (ns, measured by CTA 0 with
  * %globaltimer): [0] residual, [1] SpMV, [2] orthogonalisation, [3] norm +
- * Givens, [4] back-solve + update, [5] A32 cast.  Returns the count written. */
+ * Givens, [4] back-solve + update; with opts.profile: [5] max and [6] mean
+ * over CTAs of the CTA's own SpMV time.  Returns the count written. */
 int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap);
 
 const char* gmres_last_error(const gmres_ctx* ctx);  /* "" if none; ctx may be NULL */
@@ -131,9 +137,17 @@ int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_
 int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar, double beta, double* R,
                        double* s, double* y);
 
-/* a0: build the fp32 copy of A on the device (also done lazily
+/* a0: build the fp32 copy of A on the device (also rebuilt
  * inside every mixed solve, timed).  EFP32RANGE on overflow. */
 int gmres_k_cast32(gmres_ctx* ctx);
+
+/* Developer microbenchmark (not part of the solve): `iters` repetitions of a
+ * building block inside one cooperative launch on the solve grid; what = 0
+ * grid barrier, 1 one-value all-reduce, 2 MGS sweep, 3/4/5 CGS tile passes
+ * over ncols columns of d_V (ld ldv) and d_w (padded to ldv, zero padding).
+ * *ns = elapsed device ns. */
+int gmres_k_micro(gmres_ctx* ctx, int32_t precision, int32_t what, int32_t iters, int32_t ncols, const void* d_V,
+                  int64_t ldv, void* d_w, double* ns);
 
 /* Device pointers of the context's matrix (for tests): any may be NULL. */
 int gmres_k_matrix(gmres_ctx* ctx, const int32_t** row_ptr, const int32_t** col, const double** val64,

@@ -33,7 +33,7 @@ struct gmres_ctx {
   double* d_dinv64 = nullptr;
   float* d_dinv32 = nullptr;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
   // workspace
   int ws_m = -1, ws_prec = -1, ws_G = 0;
   char* d_ws = nullptr;
@@ -49,14 +49,19 @@ struct gmres_ctx {
   int* d_out_int = nullptr;
   double* d_out_dbl = nullptr;
   unsigned long long* d_prof = nullptr;
+  unsigned long long* d_prof_cta = nullptr;
   double* d_hist = nullptr;
+  int* d_cycJ = nullptr;
   int hist_cap = 0;
   double* d_inner = nullptr;
   int inner_cap = 0;
   int* d_row_begin = nullptr;
+  int4* d_chunks = nullptr;
+  int* d_chunk_off = nullptr;
   int part_G = 0;
   // last solve
   std::vector<double> inner_host;
+  std::vector<int32_t> cycJ_host;
   double phase_ns[PH_N] = {0};
   std::string err;
 };
@@ -82,11 +87,14 @@ int fail(gmres_ctx* c, int code, const std::string& msg) {
 
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
-// mean row length → lanes per row (power of two in [4, 32])
+// lanes per row in the CSR stream: one thread per row when a 512-row chunk of
+// average rows fits the stage (stencils), else the power of two that keeps
+// ~GT lanes (one warp group) busy on a chunk of CHUNK_CAP non-zeros.
 int auto_lanes(int64_t n, int64_t nnz) {
-  double mu = n > 0 ? (double)nnz / (double)n : 1.0;
-  int L = 4;
-  while (L < 32 && L < mu) L *= 2;
+  const double mu = n > 0 ? (double)nnz / (double)n : 1.0;
+  const double rows = std::min((double)CHUNK_RMAX, (double)CHUNK_CAP / std::max(mu, 1.0));
+  int L = 1;
+  while (L < 32 && rows * L < 0.75 * GT) L *= 2;
   return L;
 }
 
@@ -117,6 +125,8 @@ void* solve_kernel_ptr() { return (void*)&solve_kernel<W, L>; }
 void* pick_solve(int prec, int L) {
   if (prec == GMRES_MIXED) {
     switch (L) {
+      case 1: return solve_kernel_ptr<float, 1>();
+      case 2: return solve_kernel_ptr<float, 2>();
       case 4: return solve_kernel_ptr<float, 4>();
       case 8: return solve_kernel_ptr<float, 8>();
       case 16: return solve_kernel_ptr<float, 16>();
@@ -124,6 +134,8 @@ void* pick_solve(int prec, int L) {
     }
   }
   switch (L) {
+    case 1: return solve_kernel_ptr<double, 1>();
+    case 2: return solve_kernel_ptr<double, 2>();
     case 4: return solve_kernel_ptr<double, 4>();
     case 8: return solve_kernel_ptr<double, 8>();
     case 16: return solve_kernel_ptr<double, 16>();
@@ -136,6 +148,8 @@ void* pick_kernel_templ(int kind, int L) {
   switch (kind) {
     case 0:
       switch (L) {
+        case 1: return (void*)&k_spmv_kernel<W, 1>;
+        case 2: return (void*)&k_spmv_kernel<W, 2>;
         case 4: return (void*)&k_spmv_kernel<W, 4>;
         case 8: return (void*)&k_spmv_kernel<W, 8>;
         case 16: return (void*)&k_spmv_kernel<W, 16>;
@@ -143,6 +157,8 @@ void* pick_kernel_templ(int kind, int L) {
       }
     case 1:
       switch (L) {
+        case 1: return (void*)&k_resid_kernel<W, 1>;
+        case 2: return (void*)&k_resid_kernel<W, 2>;
         case 4: return (void*)&k_resid_kernel<W, 4>;
         case 8: return (void*)&k_resid_kernel<W, 8>;
         case 16: return (void*)&k_resid_kernel<W, 16>;
@@ -157,9 +173,13 @@ void* pick_kernel(int prec, int kind, int L) {
   return prec == GMRES_MIXED ? pick_kernel_templ<float>(kind, L) : pick_kernel_templ<double>(kind, L);
 }
 
-constexpr int kTileBytes = 96 * 1024;
+// stride of the per-CTA partial sums: m+1 Gram-Schmidt coefficients, and at
+// least the 3 values of the residual reduction
+int kmax_for(int m) { return std::max(m + 1, 4); }
 
-size_t smem_bytes(int m) { return SmemLayout(m + 1, kTileBytes).total; }
+// shared staging region: two CSR chunk stages, or two V tiles of ≥ 32 rows
+int tile_bytes_for(int m) { return std::max(TILE_BYTES, 2 * (m + 2) * ROWALIGN * 8); }
+size_t smem_bytes(int m) { return SmemLayout(kmax_for(m), tile_bytes_for(m)).total; }
 
 int grid_for(gmres_ctx* ctx, const void* kern, size_t smem, int ctas_per_sm, int* G) {
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -171,14 +191,58 @@ int grid_for(gmres_ctx* ctx, const void* kern, size_t smem, int ctas_per_sm, int
   return 0;
 }
 
+// CSR chunks of every CTA's rows for the TMA-staged stream (gmres_kernels.cuh
+// csr_stream): ≤ CHUNK_RMAX rows and ≤ CHUNK_CAP non-zeros, boundaries at
+// multiples of 4 rows; 4-row groups above CHUNK_CAP become "direct" chunks.
+void make_chunks(const std::vector<int32_t>& rp, int64_t n, const std::vector<int>& rb, std::vector<int4>& ent,
+                 std::vector<int>& off) {
+  const int G = (int)rb.size() - 1;
+  ent.clear();
+  off.assign(G + 1, 0);
+  for (int g = 0; g < G; ++g) {
+    off[g] = (int)ent.size();
+    const int64_t r0 = std::min<int64_t>(rb[g], n), r1 = std::min<int64_t>(rb[g + 1], n);
+    int64_t r = r0;
+    while (r < r1) {
+      const int64_t g4 = std::min(r + 4, r1);
+      if ((int64_t)rp[g4] - rp[r] > CHUNK_CAP) {  // direct chunk
+        ent.push_back(make_int4((int)r, rp[r], 1, 0));
+        r = g4;
+        continue;
+      }
+      int64_t e = g4;
+      while (e < r1) {
+        const int64_t e4 = std::min(e + 4, r1);
+        if (e4 - r > CHUNK_RMAX || (int64_t)rp[e4] - rp[r] > CHUNK_CAP) break;
+        e = e4;
+      }
+      ent.push_back(make_int4((int)r, rp[r], 0, 0));
+      r = e;
+    }
+    ent.push_back(make_int4((int)r1, rp[r1], 0, 0));  // sentinel
+  }
+  off[G] = (int)ent.size();
+}
+
 int ensure_partition(gmres_ctx* ctx, int G) {
   if (ctx->part_G == G && ctx->d_row_begin) return 0;
   std::vector<int> rb;
   make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, rb);
-  if (ctx->d_row_begin) cudaFree(ctx->d_row_begin);
+  std::vector<int4> ent;
+  std::vector<int> off;
+  make_chunks(ctx->h_rp, ctx->n, rb, ent, off);
+  cudaFree(ctx->d_row_begin);
+  cudaFree(ctx->d_chunks);
+  cudaFree(ctx->d_chunk_off);
   ctx->d_row_begin = nullptr;
+  ctx->d_chunks = nullptr;
+  ctx->d_chunk_off = nullptr;
   CK(cudaMalloc(&ctx->d_row_begin, sizeof(int) * (G + 1)));
   CK(cudaMemcpy(ctx->d_row_begin, rb.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->d_chunks, sizeof(int4) * ent.size()));
+  CK(cudaMemcpy(ctx->d_chunks, ent.data(), sizeof(int4) * ent.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->d_chunk_off, sizeof(int) * (G + 1)));
+  CK(cudaMemcpy(ctx->d_chunk_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
   ctx->part_G = G;
   return 0;
 }
@@ -191,7 +255,7 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   if (ctx->d_ws) cudaFree(ctx->d_ws);
   ctx->d_ws = nullptr;
   const size_t wb = prec == GMRES_MIXED ? 4 : 8;
-  const size_t kmax = (size_t)m + 1;
+  const size_t kmax = (size_t)kmax_for(m);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t r = off; off += (bytes + 255) & ~size_t(255); return r; };
   const size_t oV = take(wb * ctx->ldv * (m + 1));
@@ -205,7 +269,9 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   const size_t ooi = take(sizeof(int) * 8);
   const size_t ood = take(sizeof(double) * 4);
   const size_t opr = take(sizeof(unsigned long long) * PH_N);
+  const size_t opc = take(sizeof(unsigned long long) * G);
   const size_t oh = take(sizeof(double) * hist_cap);
+  const size_t ocj = take(sizeof(int) * hist_cap);
   const size_t oi = take(sizeof(double) * std::max(inner_cap, 1));
   CK(cudaMalloc(&ctx->d_ws, off));
   CK(cudaMemsetAsync(ctx->d_ws, 0, off, ctx->stream));
@@ -221,7 +287,9 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   ctx->d_out_int = (int*)(ctx->d_ws + ooi);
   ctx->d_out_dbl = (double*)(ctx->d_ws + ood);
   ctx->d_prof = (unsigned long long*)(ctx->d_ws + opr);
+  ctx->d_prof_cta = (unsigned long long*)(ctx->d_ws + opc);
   ctx->d_hist = (double*)(ctx->d_ws + oh);
+  ctx->d_cycJ = (int*)(ctx->d_ws + ocj);
   ctx->d_inner = (double*)(ctx->d_ws + oi);
   ctx->hist_cap = hist_cap;
   ctx->inner_cap = inner_cap;
@@ -231,9 +299,12 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   return 0;
 }
 
-int ensure_a32(gmres_ctx* ctx, cudaStream_t st) {
-  if (ctx->a32_ready) return 0;
-  if (!ctx->d_a32) CK(cudaMalloc(&ctx->d_a32, sizeof(float) * std::max<int64_t>(ctx->nnz, 1)));
+int ensure_a32(gmres_ctx* ctx, cudaStream_t st, bool force = false) {
+  if (ctx->a32_ready && !force) return 0;
+  if (!ctx->d_a32) {
+    CK(cudaMalloc(&ctx->d_a32, sizeof(float) * (ctx->nnz + ARR_PAD)));
+    CK(cudaMemset(ctx->d_a32, 0, sizeof(float) * (ctx->nnz + ARR_PAD)));
+  }
   int* d_err = nullptr;
   CK(cudaMallocAsync(&d_err, sizeof(int), st));
   CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
@@ -254,9 +325,9 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.n = (int)ctx->n;
   d.m = m;
   d.G = G;
-  d.kmax = m + 1;
+  d.kmax = kmax_for(m);
   d.ortho = ortho;
-  d.tile_bytes = kTileBytes;
+  d.tile_bytes = tile_bytes_for(m);
   d.rp = ctx->d_rp;
   d.ci = ctx->d_ci;
   d.a64 = ctx->d_a64;
@@ -273,13 +344,17 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.abort_flag = ctx->d_flags;
   d.err_flag = ctx->d_flags + 1;
   d.row_begin = ctx->d_row_begin;
+  d.chunks = ctx->d_chunks;
+  d.chunk_off = ctx->d_chunk_off;
   d.history = ctx->d_hist;
+  d.cycle_J = ctx->d_cycJ;
   d.hist_cap = ctx->hist_cap;
   d.inner_hist = ctx->d_inner;
   d.inner_cap = ctx->inner_cap;
   d.out_int = ctx->d_out_int;
   d.out_dbl = ctx->d_out_dbl;
   d.prof = ctx->d_prof;
+  d.prof_cta = ctx->d_prof_cta;
   d.timeout_ns = 20ll * 1000 * 1000 * 1000;
   return d;
 }
@@ -341,9 +416,15 @@ int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, 
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
-    CK(cudaMalloc(&ctx->d_rp, sizeof(int32_t) * (n + 1)));
-    CK(cudaMalloc(&ctx->d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
-    CK(cudaMalloc(&ctx->d_a64, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    CK(cudaEventCreate(&ctx->evk0));
+    CK(cudaEventCreate(&ctx->evk1));
+    // slack after the arrays: TMA bulk copies round sizes up to 16 bytes
+    CK(cudaMalloc(&ctx->d_rp, sizeof(int32_t) * (n + 1 + ARR_PAD)));
+    CK(cudaMalloc(&ctx->d_ci, sizeof(int32_t) * (nnz + ARR_PAD)));
+    CK(cudaMalloc(&ctx->d_a64, sizeof(double) * (nnz + ARR_PAD)));
+    CK(cudaMemset(ctx->d_rp, 0, sizeof(int32_t) * (n + 1 + ARR_PAD)));
+    CK(cudaMemset(ctx->d_ci, 0, sizeof(int32_t) * (nnz + ARR_PAD)));
+    CK(cudaMemset(ctx->d_a64, 0, sizeof(double) * (nnz + ARR_PAD)));
     CK(cudaMalloc(&ctx->d_dinv64, sizeof(double) * ctx->nvec));
     CK(cudaMalloc(&ctx->d_dinv32, sizeof(float) * ctx->nvec));
     CK(cudaMemcpy(ctx->d_rp, row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
@@ -382,8 +463,12 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_dinv32);
   cudaFree(ctx->d_ws);
   cudaFree(ctx->d_row_begin);
+  cudaFree(ctx->d_chunks);
+  cudaFree(ctx->d_chunk_off);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->evk0) cudaEventDestroy(ctx->evk0);
+  if (ctx->evk1) cudaEventDestroy(ctx->evk1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -394,7 +479,7 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
   ctx->err.clear();
   if (!d_b || !d_x) return fail(ctx, GMRES_EINVAL, "b/x is NULL");
-  if (m < 1 || m > 1024) return fail(ctx, GMRES_EINVAL, "m must be in [1, 1024]");
+  if (m < 1 || m > MAX_M) return fail(ctx, GMRES_EINVAL, "m must be in [1, 256]");
   if (!(tol > 0.0) || !std::isfinite(tol)) return fail(ctx, GMRES_EINVAL, "tol must be > 0");
   if (ortho != GMRES_MGS && ortho != GMRES_CGSR) return fail(ctx, GMRES_EINVAL, "ortho must be 0 (MGS) or 1 (CGSR)");
   if (int rc = check_prec(ctx, precision)) return rc;
@@ -404,7 +489,8 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   const int max_cycles = (opts && opts->max_cycles > 0) ? opts->max_cycles : 10000;
   const bool rec_inner = opts && opts->record_inner;
   int L = (opts && opts->lanes_per_row) ? opts->lanes_per_row : auto_lanes(ctx->n, ctx->nnz);
-  if (L != 4 && L != 8 && L != 16 && L != 32) return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 4/8/16/32");
+  if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16 && L != 32)
+    return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 1/2/4/8/16/32");
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
 
   const void* kern = pick_solve(precision, L);
@@ -417,12 +503,13 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   if (int rc = ensure_ws(ctx, m, precision, G, hist_cap_dev, inner_cap_dev)) return rc;
 
   CK(cudaEventRecord(ctx->ev0, st));
-  if (precision == GMRES_MIXED) {  // a0 inside the timed solve
-    if (int rc = ensure_a32(ctx, st)) return rc;
+  if (precision == GMRES_MIXED) {  // a0: rebuilt inside every timed solve
+    if (int rc = ensure_a32(ctx, st, true)) return rc;
   }
   if (d_x0 && d_x0 != d_x) CK(cudaMemcpyAsync(d_x, d_x0, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
   if (!d_x0) CK(cudaMemsetAsync(d_x, 0, sizeof(double) * ctx->n, st));
   CK(cudaMemsetAsync(ctx->d_prof, 0, sizeof(unsigned long long) * PH_N, st));
+  CK(cudaMemsetAsync(ctx->d_prof_cta, 0, sizeof(unsigned long long) * G, st));
   CK(cudaMemsetAsync(ctx->d_out_int, 0, sizeof(int) * 8, st));
 
   Dev d = make_dev(ctx, m, precision, ortho, G);
@@ -432,12 +519,15 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   d.delta = delta;
   d.max_cycles = max_cycles;
   d.inner_cap = inner_cap_dev;
+  d.profile = (opts && opts->profile) ? 1 : 0;
 
   gmres_result r{};
   if (int rc = reset_flags(ctx, st)) return rc;
   void* args[] = {&d};
+  CK(cudaEventRecord(ctx->evk0, st));
   if (int rc = launch_coop(ctx, kern, G, smem, args, st)) return rc;
   CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->evk1, st));
   CK(cudaEventRecord(ctx->ev1, st));
   int oi[8];
   double od[4];
@@ -446,8 +536,10 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   CK(cudaMemcpyAsync(od, ctx->d_out_dbl, sizeof(od), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(prof, ctx->d_prof, sizeof(prof), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  float ms = 0.f;
+  float ms = 0.f, kms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  CK(cudaEventElapsedTime(&kms, ctx->evk0, ctx->evk1));
+  r.kernel_ms = kms;
   r.status = oi[0];
   r.cycles = oi[1];
   r.inner_iters = oi[2];
@@ -455,10 +547,22 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   r.final_relres = od[0];
   r.device_ms = ms;
   for (int i = 0; i < PH_N; ++i) ctx->phase_ns[i] = (double)prof[i];
+  if (d.profile) {  // per-CTA own SpMV time: [5] max, [6] mean
+    std::vector<unsigned long long> pc(G);
+    CK(cudaMemcpy(pc.data(), ctx->d_prof_cta, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost));
+    double mx = 0, sm = 0;
+    for (auto v : pc) { mx = std::max(mx, (double)v); sm += (double)v; }
+    ctx->phase_ns[5] = mx;
+    ctx->phase_ns[6] = sm / G;
+    ctx->phase_ns[7] = 0;
+  }
   const int hl = std::min(r.history_len, std::min(history_cap, ctx->hist_cap));
   if (history && hl > 0) CK(cudaMemcpy(history, ctx->d_hist, sizeof(double) * hl, cudaMemcpyDeviceToHost));
   if (history_len) *history_len = r.history_len;
   ctx->inner_host.clear();
+  ctx->cycJ_host.assign(std::max(0, std::min(r.cycles, ctx->hist_cap)), 0);
+  if (!ctx->cycJ_host.empty())
+    CK(cudaMemcpy(ctx->cycJ_host.data(), ctx->d_cycJ, sizeof(int) * ctx->cycJ_host.size(), cudaMemcpyDeviceToHost));
   if (rec_inner && oi[4] > 0) {
     const int il = std::min(oi[4], ctx->inner_cap);
     ctx->inner_host.resize(il);
@@ -499,6 +603,14 @@ int gmres_get_inner_history(gmres_ctx* ctx, double* buf, int32_t cap, int32_t* l
   if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
   const int n = (int)ctx->inner_host.size();
   if (buf) std::memcpy(buf, ctx->inner_host.data(), sizeof(double) * std::min(n, std::max(cap, 0)));
+  if (len) *len = n;
+  return 0;
+}
+
+int gmres_get_cycle_iters(gmres_ctx* ctx, int32_t* buf, int32_t cap, int32_t* len) {
+  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
+  const int n = (int)ctx->cycJ_host.size();
+  if (buf) std::memcpy(buf, ctx->cycJ_host.data(), sizeof(int32_t) * std::min(n, std::max(cap, 0)));
   if (len) *len = n;
   return 0;
 }
@@ -560,7 +672,7 @@ int gmres_k_spmv(gmres_ctx* ctx, int32_t precision, const void* d_v, void* d_w) 
   if (int rc = comp_setup(ctx, precision, 1, 0, L, &kern, &G, &smem, &mws)) return rc;
   Dev d = make_dev(ctx, mws, precision, 0, G);
   void* args[] = {&d, (void*)&d_v, &d_w};
-  CK(cudaLaunchKernel(kern, dim3(G), dim3(NT), args, 0, ctx->stream));
+  CK(cudaLaunchKernel(kern, dim3(G), dim3(NT), args, smem, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
@@ -651,6 +763,37 @@ int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_
   cudaFree(d_y);
   if (e != cudaSuccess) return fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
   return 0;
+}
+
+int gmres_k_micro(gmres_ctx* ctx, int32_t precision, int32_t what, int32_t iters, int32_t ncols, const void* d_V,
+                  int64_t ldv, void* d_w, double* ns) {
+  if (!ctx || !d_V || !d_w || !ns) return fail(ctx, GMRES_EINVAL, "null argument");
+  const int L = auto_lanes(ctx->n, ctx->nnz);
+  const void* kern0;
+  int G;
+  size_t smem;
+  int m;
+  if (int rc = comp_setup(ctx, precision, std::max(ncols, 1), 2, L, &kern0, &G, &smem, &m)) return rc;
+  const void* kern = precision == GMRES_MIXED ? (const void*)&k_micro_kernel<float> : (const void*)&k_micro_kernel<double>;
+  int Gk = 0;
+  if (int rc = grid_for(ctx, kern, smem, 0, &Gk)) return rc;
+  if (Gk < G) return fail(ctx, GMRES_ECUDA, "micro kernel occupancy below the solve grid");
+  Dev d = make_dev(ctx, m, precision, 0, G);
+  unsigned long long* d_ns = nullptr;
+  CK(cudaMalloc(&d_ns, 16));
+  CK(cudaMemset(d_ns, 0, 16));
+  long long ld = ldv;
+  void* args[] = {&d, &what, &iters, &ncols, (void*)&d_V, &ld, &d_w, &d_ns};
+  int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream);
+  unsigned long long h[2] = {0, 0};
+  if (rc == 0) {
+    cudaError_t e = cudaMemcpyAsync(h, d_ns, 16, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
+  }
+  cudaFree(d_ns);
+  *ns = (double)h[0];
+  return rc;
 }
 
 int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar, double beta, double* R, double* s,

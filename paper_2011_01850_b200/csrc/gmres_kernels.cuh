@@ -9,14 +9,20 @@
 // bit-identical reduced inputs (so every CTA takes the same branch); CTA 0
 // keeps R for the back-substitution.
 //
+// Data movement: the CSR stream (row_ptr, col, val) and the V tiles are staged
+// into shared memory by TMA bulk copies (cp.async.bulk + mbarrier, double
+// buffered); threads only gather v_j / x and do arithmetic.
+//
 // W is the working precision of Alg. 1 lines 89–146 (float in mixed mode,
 // double in fp64 mode).  Element-wise W operations use the
 // explicit _rn intrinsics (no FMA contraction) so that their rounding is the
-// single W rounding per operation the oracle performs (R9/R10).
+// single W rounding per operation the oracle performs (R9/R10);
+// with one thread per row the SpMV row sums are even bit-identical to the
+// oracle's (ascending column order).
 #pragma once
 #include <cuda_runtime.h>
-#include <stdint.h>
 #include <float.h>
+#include <stdint.h>
 
 namespace g200 {
 
@@ -24,10 +30,21 @@ constexpr int NT = 512;        // threads per CTA (16 warps)
 constexpr int NW = NT / 32;
 constexpr int ROWALIGN = 32;   // row-partition granularity (128 B of fp32)
 constexpr int LDALIGN = 64;    // leading dimension of V (256 B of fp32)
+constexpr int NGRP = 4;          // CSR-stream warp groups per CTA (independent pipelines)
+constexpr int GT = NT / NGRP;    // threads per group (4 warps)
+constexpr int CHUNK_CAP = 1024;  // max nnz of a TMA-staged CSR chunk
+constexpr int CHUNK_RMAX = GT;   // max rows of a CSR chunk (multiple of 4)
+constexpr int ST_OFF_CI = 544;                             // stage layout (bytes): row_ptr slice
+constexpr int ST_OFF_A = ST_OFF_CI + (CHUNK_CAP + 8) * 4;  // 4672: col slice, then values
+constexpr int STAGE_BYTES = ST_OFF_A + (CHUNK_CAP + 8) * 8;  // 12928
+constexpr int TILE_BYTES = NGRP * 2 * STAGE_BYTES;         // 103424: 2 stages per group
+constexpr int MAX_M = 256;                               // restart length limit (shared-memory bound)
+constexpr int ARR_PAD = 8;   // elements of slack after rp/col/val (TMA rounds up to 16 B)
 
 enum { ST_OK = 0, ST_NOT_CONVERGED = 1, ST_EFP32RANGE = -4, ST_ENONFINITE = -5, ST_ETIMEOUT = -8 };
 enum { ERRF_RANGE = 1, ERRF_NONFINITE = 2 };
-enum { PH_RESID = 0, PH_SPMV = 1, PH_ORTHO = 2, PH_GIVENS = 3, PH_UPDATE = 4, PH_N = 8 };
+enum { PH_RESID = 0, PH_SPMV = 1, PH_ORTHO = 2, PH_GIVENS = 3, PH_UPDATE = 4, PH_N = 16 };
+// profile-mode sub-phases of CGSR in prof[8..13]: pass1, red1, pass2, red2, pass3, red3
 
 struct Dev {
   int n;            // rows
@@ -35,7 +52,7 @@ struct Dev {
   int G;            // CTAs in the grid
   int kmax;         // m + 1 (stride of the partial buffers)
   int ortho;        // 0 MGS, 1 CGSR
-  int tile_bytes;   // shared bytes reserved for V tiles
+  int tile_bytes;   // shared bytes reserved for the staging region
   const int* rp;
   const int* ci;
   const double* a64;
@@ -54,13 +71,18 @@ struct Dev {
   int* abort_flag;
   int* err_flag;
   const int* row_begin; // G+1 row boundaries (multiples of ROWALIGN, last = nvec)
+  const int4* chunks;   // CSR chunks {row_begin, nnz_begin, direct, 0}; per CTA a sentinel
+  const int* chunk_off; // G+1 offsets into chunks (CTA g: [off[g], off[g+1]-1) + sentinel)
   double tol, delta;
   int max_cycles;
   double* history; int hist_cap;
+  int* cycle_J;         // [hist_cap] inner iterations of every cycle
   double* inner_hist; int inner_cap;
   int* out_int;         // [0] status [1] cycles [2] inner iters [3] history len [4] inner len
   double* out_dbl;      // [0] final relres
   unsigned long long* prof;   // [PH_N] ns accumulated by CTA 0
+  unsigned long long* prof_cta;  // [G] per-CTA own SpMV ns (profile mode)
+  int profile;          // != 0: grid barrier after every phase (clean attribution)
   long long timeout_ns;
 };
 
@@ -98,27 +120,79 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 // per-CTA control block in static shared memory
 struct Shm {
-  unsigned long long epoch;   // grid barriers passed by this CTA
-  int red_epoch;              // all-reduces done (selects the partial slot)
+  unsigned long long mbar[NGRP][2];  // TMA stage barriers (per CSR-stream group)
+  unsigned long long epoch;          // grid barriers passed by this CTA
+  unsigned tma_phase[NGRP];          // bit s: parity of the next completion of stage s
+  int red_epoch;               // all-reduces done (selects the partial slot)
   int abort;
   int flag;
-  int status;
-  double bc[4];
-  double red[NW * 2];
+  double red[NW * 4];
 };
+
+// wait for stage s of group grp's TMA pipeline; watchdog on %globaltimer
+// (a timeout raises the global abort flag; callers keep their barrier
+// sequence and the solve ends with ETIMEOUT at the next grid barrier)
+__device__ __forceinline__ void stage_wait(const Dev& d, Shm& sh, int grp, int s) {
+  const unsigned par = (sh.tma_phase[grp] >> s) & 1u;
+  if (mbar_try_wait(&sh.mbar[grp][s], par)) return;
+  const unsigned long long t0 = globaltimer();
+  for (;;) {
+    if (mbar_try_wait(&sh.mbar[grp][s], par)) return;
+    if ((long long)(globaltimer() - t0) > d.timeout_ns) {
+      atomicExch(d.abort_flag, 1);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ void group_sync(int grp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(GT) : "memory");
+}
+
+__device__ __forceinline__ void init_shm(Shm& sh) {
+  if (threadIdx.x == 0) {
+    sh.epoch = 0;
+    sh.red_epoch = 0;
+    sh.abort = 0;
+    sh.flag = 0;
+    for (int g = 0; g < NGRP; ++g) {
+      sh.tma_phase[g] = 0;
+      mbar_init(&sh.mbar[g][0], 1);
+      mbar_init(&sh.mbar[g][1], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
 
 // Grid-wide barrier over the co-resident (cooperative) grid: monotone 64-bit
 // arrival counter, release/acquire through __threadfence + atomics.  A device
@@ -141,6 +215,7 @@ __device__ __forceinline__ bool grid_sync(const Dev& d, Shm& sh) {
       }
     }
     __threadfence();
+    if (!ab && *(volatile int*)d.abort_flag) ab = 1;
     sh.abort = ab;
   }
   __syncthreads();
@@ -166,8 +241,11 @@ __device__ __forceinline__ void block_sum(double (&v)[K], Shm& sh, double* out) 
 }
 
 // Grid all-reduce of K fp64 values (s_part → s_out, both shared).  Every CTA
-// sums the G partials in the same fixed order, so all CTAs hold bit-identical
-// results (replicated control flow).
+// sums the G partials in the same fixed order (warp w owns a contiguous block
+// of CTAs; blocks in order), so all CTAs hold bit-identical results
+// (replicated control flow).  The G·K loads of a CTA are all
+// independent (one L2 round trip).
+constexpr int GCH = 8;  // independent partial loads in flight per lane
 __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const double* s_part, int K, double* s_out,
                                                double* s_tmp) {
   const int slot = sh.red_epoch & 1;
@@ -175,11 +253,48 @@ __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const doub
   for (int k = threadIdx.x; k < K; k += NT) P[(size_t)blockIdx.x * d.kmax + k] = s_part[k];
   if (!grid_sync(d, sh)) return false;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (K * d.G <= NT * 4 && K <= 4) {
+    // small K: thread g < G loads CTA g's K partials (one round trip), then a
+    // fixed shuffle tree per warp and warps in order
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int g = threadIdx.x; g < d.G; g += NT) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < K) v[k] += __ldcg(P + (size_t)g * d.kmax + k);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < K) {
+        const double sv = warp_sum(v[k]);
+        if (lane == 0) s_tmp[warp * d.kmax + k] = sv;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+      double acc = 0.0;
+      for (int w = 0; w < NW; ++w) acc += s_tmp[w * d.kmax + threadIdx.x];
+      s_out[threadIdx.x] = acc;
+    }
+    if (threadIdx.x == 0) sh.red_epoch++;
+    __syncthreads();
+    return true;
+  }
+  const int gpw = (d.G + NW - 1) / NW;
+  const int g0 = warp * gpw;
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int k = k0 + lane;
     if (k < K) {
       double acc = 0.0;
-      for (int g = warp; g < d.G; g += NW) acc += __ldcg(P + (size_t)g * d.kmax + k);
+      for (int u0 = 0; u0 < gpw; u0 += GCH) {
+        double v[GCH];
+#pragma unroll
+        for (int u = 0; u < GCH; ++u) {
+          const int g = g0 + u0 + u;
+          v[u] = (u0 + u < gpw && g < d.G) ? __ldcg(P + (size_t)g * d.kmax + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < GCH; ++u) acc += v[u];
+      }
       s_tmp[warp * d.kmax + k] = acc;
     }
   }
@@ -194,78 +309,160 @@ __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const doub
   return true;
 }
 
-// ------------------------------------------------------------------ a1
-// Alg. 1 lines 86–90 (PAPER.md:188-196, 287): z = b − A64 x in fp64, then
-// r = RN_W(dinv_W · RN_W(z)) (reading R10).  L lanes per row, fp64 row sums.
-template <class W, int L>
-__device__ void resid_rows(const Dev& d, int r0, int r1, W* __restrict__ r_out, double& zz, double& rr, double& bb,
-                           int& err) {
-  const int lane = threadIdx.x & (L - 1);
-  const int rend = min(r1, d.n);
-  const W* dinv = (const W*)d.dinvW;
-  for (int base = r0 + (threadIdx.x >> 5) * (32 / L); base < rend; base += NT / L) {
-    const int row = base + ((threadIdx.x & 31) / L);
-    const bool act = row < rend;
-    double acc = 0.0;
-    if (act) {
-      const int s = __ldg(d.rp + row), e = __ldg(d.rp + row + 1);
-      for (int p = s + lane; p < e; p += L) acc += __ldg(d.a64 + p) * d.x[__ldg(d.ci + p)];
+// ---------------------------------------------------- CSR stream (a1, a2)
+// The CTA's rows are cut (on the host) into chunks of ≤ CHUNK_RMAX rows and
+// ≤ CHUNK_CAP non-zeros whose boundaries are multiples of 4 rows.  The CTA
+// runs NGRP independent warp groups; group g takes chunks g, g+NGRP, ... and
+// owns a 2-stage ring: its leader stages chunk i+2's row_ptr/col/val slices
+// into shared memory with three TMA bulk copies (cp.async.bulk, mbarrier)
+// while the group computes chunk i.  Groups drift out of phase, so one
+// group's gathers overlap another's TMA wait.  L lanes per row (L = 1: one
+// thread per row, the oracle's summation order); gathers from global (L1/L2).
+// Chunks whose 4 rows exceed CHUNK_CAP are "direct": a warp per row from
+// global memory.  pre(row) is called by the epilogue lane before the row's
+// gathers (to prefetch per-row operands); epi(row, acc, pre) after.
+template <class AT> struct AccOps;
+template <> struct AccOps<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+};
+template <> struct AccOps<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+};
+
+template <class AT, int L, class Gather, class Pre, class Epi>
+__device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __restrict__ vals, Gather gat, Pre pre,
+                           Epi epi) {
+  using Ops = AccOps<AT>;
+  using PT = decltype(pre(0));
+  const int grp = threadIdx.x / GT, gt = threadIdx.x % GT;
+  const int c0 = d.chunk_off[blockIdx.x], c1 = d.chunk_off[blockIdx.x + 1] - 1;
+  char* gbase = s_stage + grp * 2 * STAGE_BYTES;
+  auto issue = [&](int c, int s) {  // group leader only
+    const int4 e = d.chunks[c], f = d.chunks[c + 1];
+    if (e.z) return;
+    char* st = gbase + s * STAGE_BYTES;
+    const int ea = e.y & ~3, eb = (f.y + 3) & ~3;
+    const unsigned b_rp = (unsigned)(((f.x - e.x + 1) + 3) & ~3) * 4u;
+    const unsigned b_ci = (unsigned)(eb - ea) * 4u;
+    const unsigned b_a = (unsigned)(eb - ea) * (unsigned)sizeof(AT);
+    fence_proxy_async();
+    mbar_expect_tx(&sh.mbar[grp][s], b_rp + b_ci + b_a);
+    tma_load_1d(st, d.rp + e.x, b_rp, &sh.mbar[grp][s]);
+    if (b_ci) {
+      tma_load_1d(st + ST_OFF_CI, d.ci + ea, b_ci, &sh.mbar[grp][s]);
+      tma_load_1d(st + ST_OFF_A, vals + ea, b_a, &sh.mbar[grp][s]);
     }
+  };
+  if (gt == 0) {
+    if (c0 + grp < c1) issue(c0 + grp, 0);
+    if (c0 + grp + NGRP < c1) issue(c0 + grp + NGRP, 1);
+  }
+  const int wl = threadIdx.x & 31, gw = gt >> 5;  // lane, warp within the group
+  int i = 0;
+  for (int c = c0 + grp; c < c1; c += NGRP, ++i) {
+    const int s = i & 1;
+    const int4 e = d.chunks[c];
+    const int rb = e.x, nrow = d.chunks[c + 1].x - rb;
+    if (!e.z) {
+      stage_wait(d, sh, grp, s);
+      const char* st = gbase + s * STAGE_BYTES;
+      const int* srp = reinterpret_cast<const int*>(st);
+      const int* sci = reinterpret_cast<const int*>(st + ST_OFF_CI);
+      const AT* sa = reinterpret_cast<const AT*>(st + ST_OFF_A);
+      const int ea = e.y & ~3;
+      if (L == 1) {
+        for (int lr = gt; lr < nrow; lr += GT) {
+          const PT pv = pre(rb + lr);
+          const int p0 = srp[lr] - ea, p1 = srp[lr + 1] - ea;
+          AT acc = (AT)0;
+#pragma unroll 4
+          for (int p = p0; p < p1; ++p) acc = Ops::add(acc, Ops::mul(sa[p], gat(sci[p])));
+          epi(rb + lr, acc, pv);
+        }
+      } else {
+        const int sub = wl / L, lane = wl & (L - 1);
+        for (int base = gw * (32 / L); base < nrow; base += GT / L) {
+          const int lr = base + sub;
+          const bool act = lr < nrow;
+          PT pv{};
+          if (act && lane == 0) pv = pre(rb + lr);
+          AT acc = (AT)0;
+          if (act) {
+            const int p0 = srp[lr] - ea, p1 = srp[lr + 1] - ea;
+            for (int p = p0 + lane; p < p1; p += L) acc = Ops::add(acc, Ops::mul(sa[p], gat(sci[p])));
+          }
 #pragma unroll
-    for (int o = L / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (act && lane == 0) {
-      const double bi = d.b[row];
-      bb += bi * bi;
-      const double z = bi - acc;
-      if (!isfinite(z)) err |= ERRF_NONFINITE;
-      zz += z * z;
-      if (sizeof(W) == 4 && fabs(z) > (double)FLT_MAX) err |= ERRF_RANGE;
-      const W ri = mulw(__ldg(dinv + row), RN<W>(z));
-      r_out[row] = ri;
-      rr += (double)ri * (double)ri;
+          for (int o = L / 2; o > 0; o >>= 1) acc = Ops::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+          if (act && lane == 0) epi(rb + lr, acc, pv);
+        }
+      }
+    } else {
+      // direct chunk (very long rows): one warp per row from global memory
+      for (int lr = gw; lr < nrow; lr += GT / 32) {
+        const int row = rb + lr;
+        PT pv{};
+        if (wl == 0) pv = pre(row);
+        const int p0 = __ldg(d.rp + row), p1 = __ldg(d.rp + row + 1);
+        AT acc = (AT)0;
+        for (int p = p0 + wl; p < p1; p += 32) acc = Ops::add(acc, Ops::mul(__ldg(vals + p), gat(__ldg(d.ci + p))));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = Ops::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        if (wl == 0) epi(row, acc, pv);
+      }
+    }
+    group_sync(grp);
+    if (gt == 0) {
+      if (!e.z) sh.tma_phase[grp] ^= (1u << s);
+      if (c + 2 * NGRP < c1) issue(c + 2 * NGRP, s);
     }
   }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ a1
+// Alg. 1 lines 86–90 (PAPER.md:188-196, 287): z = b − A64 x in fp64, then
+// r = RN_W(dinv_W · RN_W(z)) (reading R10).  fp64 row sums.
+template <class W, int L>
+__device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict__ r_out, double& zz, double& rr,
+                            double& bb, int& err) {
+  const W* dinv = (const W*)d.dinvW;
+  const double* __restrict__ x = d.x;
+  struct P2 { double b; W di; };
+  auto gat = [&](int col) -> double { return x[col]; };
+  auto pre = [&](int row) -> P2 { return P2{d.b[row], __ldg(dinv + row)}; };
+  auto epi = [&](int row, double acc, P2 pv) {
+    const double bi = pv.b;
+    bb += bi * bi;
+    const double z = bi - acc;
+    if (!isfinite(z)) err |= ERRF_NONFINITE;
+    zz += z * z;
+    if (sizeof(W) == 4 && fabs(z) > (double)FLT_MAX) err |= ERRF_RANGE;
+    const W ri = mulw(pv.di, RN<W>(z));
+    r_out[row] = ri;
+    rr += (double)ri * (double)ri;
+  };
+  csr_stream<double, L>(d, sh, s_stage, d.a64, gat, pre, epi);
 }
 
 // ------------------------------------------------------------------ a2
 // Alg. 1: w = RN_W(dinv_W ∘ (A_W v_j)), with v_j = RN_W(src · inv)
 // formed on the fly from the unnormalised previous vector (line 105 fused
-// into the gather: identical bits to normalising first).  L lanes per row.
+// into the gather: identical bits to normalising first).  The epilogue also
+// stores the CTA's own rows of v_j into V[:, j−1].
 template <class W, int L>
-__device__ void spmv_rows(const Dev& d, int r0, int r1, const W* __restrict__ src, double inv, W* __restrict__ dst) {
-  const int lane = threadIdx.x & (L - 1);
-  const int rend = min(r1, d.n);
-  const W* aW = (const W*)d.aW;
+__device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
+                           W* __restrict__ dst, W* __restrict__ vcol) {
   const W* dinv = (const W*)d.dinvW;
-  for (int base = r0 + (threadIdx.x >> 5) * (32 / L); base < rend; base += NT / L) {
-    const int row = base + ((threadIdx.x & 31) / L);
-    const bool act = row < rend;
-    W acc = (W)0;
-    if (act) {
-      const int s = __ldg(d.rp + row), e = __ldg(d.rp + row + 1);
-      for (int p = s + lane; p < e; p += L) {
-        const W v = RN<W>((double)src[__ldg(d.ci + p)] * inv);
-        acc = addw(acc, mulw(__ldg(aW + p), v));
-      }
-    }
-#pragma unroll
-    for (int o = L / 2; o > 0; o >>= 1) acc = addw(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-    if (act && lane == 0) dst[row] = mulw(__ldg(dinv + row), acc);
-  }
-}
-
-// own rows of the new basis column: V[:, j] = RN_W(src · inv) (Alg. 1)
-template <class W>
-__device__ void write_vcol(int r0, int r1, const W* __restrict__ src, double inv, W* __restrict__ vcol) {
-  using V4 = typename VecT<W>::T;
-  constexpr int N = VecT<W>::N;
-  for (int q = r0 / N + threadIdx.x; q < r1 / N; q += NT) {
-    V4 a = reinterpret_cast<const V4*>(src)[q];
-    W* pa = reinterpret_cast<W*>(&a);
-#pragma unroll
-    for (int t = 0; t < N; ++t) pa[t] = RN<W>((double)pa[t] * inv);
-    reinterpret_cast<V4*>(vcol)[q] = a;
-  }
+  struct P2 { W di; W self; };
+  auto gat = [&](int col) -> W { return RN<W>((double)src[col] * inv); };
+  auto pre = [&](int row) -> P2 { return P2{__ldg(dinv + row), vcol ? src[row] : (W)0}; };
+  auto epi = [&](int row, W acc, P2 pv) {
+    dst[row] = mulw(pv.di, acc);
+    if (vcol) vcol[row] = RN<W>((double)pv.self * inv);
+  };
+  csr_stream<W, L>(d, sh, s_stage, (const W*)d.aW, gat, pre, epi);
 }
 
 // ------------------------------------------------------------------ a3
@@ -274,123 +471,163 @@ __device__ void write_vcol(int r0, int r1, const W* __restrict__ src, double inv
 //   the partial of h_i = w·v_next (line 154 of step i), or of ‖w‖² when
 //   v_next == nullptr (line 104).  fp64 accumulation (reading R9).
 template <class W>
-__device__ double mgs_sweep(int r0, int r1, W* __restrict__ w, const W* __restrict__ vprev, W hprev,
+__device__ __noinline__ double mgs_sweep(int r0, int r1, W* __restrict__ w, const W* __restrict__ vprev, W hprev,
                             const W* __restrict__ vnext) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
+  constexpr int UB = 4;  // independent 16-byte loads in flight per array per thread
   double acc = 0.0;
-  for (int q = r0 / N + threadIdx.x; q < r1 / N; q += NT) {
-    V4 a = reinterpret_cast<V4*>(w)[q];
-    W* pa = reinterpret_cast<W*>(&a);
-    if (vprev) {
-      V4 b = reinterpret_cast<const V4*>(vprev)[q];
-      const W* pb = reinterpret_cast<const W*>(&b);
+  const int q0 = r0 / N, q1 = r1 / N;
+  for (int qb = q0 + threadIdx.x; qb < q1; qb += UB * NT) {
+    V4 a[UB], b[UB], c[UB];
 #pragma unroll
-      for (int t = 0; t < N; ++t) pa[t] = subw(pa[t], mulw(hprev, pb[t]));
-      reinterpret_cast<V4*>(w)[q] = a;
+    for (int u = 0; u < UB; ++u) {
+      const int q = qb + u * NT;
+      if (q < q1) {
+        a[u] = reinterpret_cast<V4*>(w)[q];
+        if (vprev) b[u] = reinterpret_cast<const V4*>(vprev)[q];
+        if (vnext) c[u] = reinterpret_cast<const V4*>(vnext)[q];
+      }
     }
-    if (vnext) {
-      V4 c = reinterpret_cast<const V4*>(vnext)[q];
-      const W* pc = reinterpret_cast<const W*>(&c);
 #pragma unroll
-      for (int t = 0; t < N; ++t) acc += (double)pa[t] * (double)pc[t];
-    } else {
+    for (int u = 0; u < UB; ++u) {
+      const int q = qb + u * NT;
+      if (q < q1) {
+        W* pa = reinterpret_cast<W*>(&a[u]);
+        if (vprev) {
+          const W* pb = reinterpret_cast<const W*>(&b[u]);
 #pragma unroll
-      for (int t = 0; t < N; ++t) acc += (double)pa[t] * (double)pa[t];
+          for (int t = 0; t < N; ++t) pa[t] = subw(pa[t], mulw(hprev, pb[t]));
+          reinterpret_cast<V4*>(w)[q] = a[u];
+        }
+        if (vnext) {
+          const W* pc = reinterpret_cast<const W*>(&c[u]);
+#pragma unroll
+          for (int t = 0; t < N; ++t) acc += (double)pa[t] * (double)pc[t];
+        } else {
+#pragma unroll
+          for (int t = 0; t < N; ++t) acc += (double)pa[t] * (double)pa[t];
+        }
+      }
     }
   }
   return acc;
 }
 
 // ------------------------------------------------------------------ a4/a8
-// Tiled passes over the CTA's rows with the V tile (T rows × ncols) staged in
-// shared memory by cp.async (double-buffered), so each pass reads V once:
+// Row-tile passes over the CTA's rows: each thread owns N consecutive rows
+// (one 16-byte vector) of a 512·N-row tile and streams the tile's V columns
+// with independent vector loads (all j in flight):
 //   MODE 1: colacc_i += Σ_r V_ri w_r                       (CGS pass, line 161)
-//   MODE 2: w ← RN_W(w − Σ_i V_i c_i), then colacc += Vᵀw   (line 162 + next line 161)
+//   MODE 2: w ← RN_W(w − Σ_i V_i c_i), then colacc += Vᵀw   (line 162 + next line 161;
+//           the second read of the tile's V is served by L2)
 //   MODE 3: w ← RN_W(w − Σ_i V_i c_i), nn += ‖w‖²          (line 162 + line 104)
 //   MODE 4: x_r += Σ_i (double)V_ri · y_i                   (lines 145–147, fp64)
-// V·c is summed in W with i ascending (reading R2/R9); dots in fp64.
-template <class W>
-__device__ __forceinline__ int tile_rows(int ncols, int tile_bytes) {
-  int T = tile_bytes / (2 * (ncols + 1) * (int)sizeof(W));
-  T = (T / ROWALIGN) * ROWALIGN;
-  if (T > 1024) T = 1024;
-  if (T < ROWALIGN) T = ROWALIGN;
-  return T;
-}
-
+// V·c is summed in W with i ascending (reading R2/R9); dots in fp64, reduced
+// per warp (shuffle tree) into s_wcol[warp][i] in tile order: deterministic.
 template <class W, int MODE>
-__device__ void tile_pass(const Dev& d, int r0, int r1, const W* __restrict__ V, long long ldv, int ncols,
-                          W* __restrict__ w, const W* s_coefW, const double* s_y, double* s_colacc, double& nn,
-                          char* s_tiles) {
+__device__ __noinline__ double rowtile_pass_impl(int n, double* __restrict__ xg, int kmax, int r0, int r1,
+                                                 const W* __restrict__ V, long long ldv, int ncols,
+                                                 W* __restrict__ w, const W* s_coefW, const double* s_y,
+                                                 double* s_acc, typename VecT<W>::T* s_wt) {
+  using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
-  const int T = tile_rows<W>(ncols, d.tile_bytes);
-  const int nrows = r1 - r0;
-  if (nrows <= 0) return;
-  const int ntiles = (nrows + T - 1) / T;
-  const int stride = (ncols + 1) * T;  // W elements per buffer (V tile + w tile)
-  W* buf0 = reinterpret_cast<W*>(s_tiles);
+  constexpr int HALF = NT / 2;  // vectors per dot work item
+  double nn = 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool has_w = MODE != 4;
-
-  auto stage = [&](int t, W* sb) {
-    const int t0 = r0 + t * T;
-    const int cnt = min(T, r1 - t0);
-    const int cpc = cnt / N;  // 16-byte chunks per column
-    const int ncol_ld = ncols + (has_w ? 1 : 0);
-    for (int idx = threadIdx.x; idx < ncol_ld * cpc; idx += NT) {
-      const int c = idx / cpc, q = idx - c * cpc;
-      const W* g = (c < ncols) ? (V + (long long)c * ldv + t0 + q * N) : (w + t0 + q * N);
-      cp_async16(sb + c * T + q * N, g);
-    }
-  };
-
-  stage(0, buf0);
-  cp_async_commit();
-  for (int t = 0; t < ntiles; ++t) {
-    W* sb = buf0 + (t & 1) * stride;
-    if (t + 1 < ntiles) {
-      stage(t + 1, buf0 + ((t + 1) & 1) * stride);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int t0 = r0 + t * T;
-    const int cnt = min(T, r1 - t0);
-    W* sw = sb + ncols * T;
-    if (MODE == 2 || MODE == 3) {
-      for (int r = threadIdx.x; r < cnt; r += NT) {
-        W acc = (W)0;
-        for (int i = 0; i < ncols; ++i) acc = addw(acc, mulw(sb[i * T + r], s_coefW[i]));
-        const W wn = subw(sw[r], acc);
-        sw[r] = wn;
-        w[t0 + r] = wn;
-        if (MODE == 3) nn += (double)wn * (double)wn;
-      }
-      if (MODE == 2) __syncthreads();
-    }
-    if (MODE == 1 || MODE == 2) {
-      for (int i = warp; i < ncols; i += NW) {
-        double acc = 0.0;
-        for (int r = lane; r < cnt; r += 32) acc += (double)sb[i * T + r] * (double)sw[r];
-        acc = warp_sum(acc);
-        if (lane == 0) s_colacc[i] += acc;
-      }
-    }
-    if (MODE == 4) {
-      for (int r = threadIdx.x; r < cnt; r += NT) {
-        const int row = t0 + r;
-        if (row < d.n) {
-          double u = 0.0;
-          for (int i = 0; i < ncols; ++i) u += (double)sb[i * T + r] * s_y[i];
-          d.x[row] = d.x[row] + u;
+  const int q0 = r0 / N, q1 = r1 / N;
+  if (MODE == 1 || MODE == 2) {
+    for (int i = threadIdx.x; i < 2 * ncols; i += NT) s_acc[i] = 0.0;
+  }
+  for (int qb = q0; qb < q1; qb += NT) {
+    const int q = qb + threadIdx.x;
+    const bool act = q < q1;
+    V4 wv;
+    W* pw = reinterpret_cast<W*>(&wv);
+#pragma unroll
+    for (int t = 0; t < N; ++t) pw[t] = (W)0;
+    if (MODE != 4 && act) wv = reinterpret_cast<const V4*>(w)[q];
+    if (MODE == 2 || MODE == 3 || MODE == 4) {
+      // step a: thread-per-vector sweep over all ncols columns (all loads in flight)
+      W acc[N];
+      double u[N];
+#pragma unroll
+      for (int t = 0; t < N; ++t) { acc[t] = (W)0; u[t] = 0.0; }
+      if (act) {
+#pragma unroll 8
+        for (int i = 0; i < ncols; ++i) {
+          const V4 v = __ldcg(reinterpret_cast<const V4*>(V + (long long)i * ldv) + q);
+          const W* pv = reinterpret_cast<const W*>(&v);
+          if (MODE == 4) {
+            const double yi = s_y[i];
+#pragma unroll
+            for (int t = 0; t < N; ++t) u[t] = __dadd_rn(u[t], __dmul_rn((double)pv[t], yi));
+          } else {
+            const W ci = s_coefW[i];
+#pragma unroll
+            for (int t = 0; t < N; ++t) acc[t] = addw(acc[t], mulw(pv[t], ci));
+          }
+        }
+        if (MODE == 4) {
+#pragma unroll
+          for (int t = 0; t < N; ++t) {
+            const int row = q * N + t;
+            if (row < n) xg[row] = xg[row] + u[t];
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < N; ++t) pw[t] = subw(pw[t], acc[t]);
+          reinterpret_cast<V4*>(w)[q] = wv;
+          if (MODE == 3) {
+#pragma unroll
+            for (int t = 0; t < N; ++t) nn += (double)pw[t] * (double)pw[t];
+          }
         }
       }
     }
-    __syncthreads();
+    if (MODE == 1 || MODE == 2) {
+      // step b: column dots over the tile; work item = (column, half tile),
+      // item it owned by warp it % NW in every tile (fixed accumulation order)
+      s_wt[threadIdx.x] = wv;
+      __syncthreads();
+      for (int it = warp; it < 2 * ncols; it += NW) {
+        const int col = it >> 1, h0 = (it & 1) * HALF;
+        const V4* vc = reinterpret_cast<const V4*>(V + (long long)col * ldv) + qb + h0;
+        const int lim = min(HALF, q1 - (qb + h0));
+        double p = 0.0;
+#pragma unroll 8
+        for (int k = lane; k < HALF; k += 32) {
+          if (k < lim) {
+            const V4 v = __ldcg(vc + k);
+            const V4 ww = s_wt[h0 + k];
+            const W* pv = reinterpret_cast<const W*>(&v);
+            const W* pq = reinterpret_cast<const W*>(&ww);
+#pragma unroll
+            for (int t = 0; t < N; ++t) p += (double)pv[t] * (double)pq[t];
+          }
+        }
+        p = warp_sum(p);
+        if (lane == 0) s_acc[it] += p;
+      }
+      __syncthreads();
+    }
   }
+  return nn;
+}
+
+template <class W, int MODE>
+__device__ __forceinline__ void rowtile_pass(const Dev& d, int r0, int r1, const W* V, long long ldv, int ncols, W* w,
+                                             const W* s_coefW, const double* s_y, double* s_acc, char* s_tiles,
+                                             double& nn) {
+  nn += rowtile_pass_impl<W, MODE>(d.n, d.x, d.kmax, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_acc,
+                                   reinterpret_cast<typename VecT<W>::T*>(s_tiles));
+}
+
+// (column, half) accumulators → per-CTA column partials, fixed order
+__device__ __forceinline__ void combine_acc(const double* s_acc, int ncols, double* s_part) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncols; i += NT) s_part[i] = s_acc[2 * i] + s_acc[2 * i + 1];
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ a6
@@ -433,7 +670,8 @@ __device__ void backsolve_cta(int J, const double* R, int ldr, const double* s, 
     if (threadIdx.x == 0) s_y[i] = s_rhs[i] / __ldcg(R + (size_t)i * ldr + i);
     __syncthreads();
     const double yi = s_y[i];
-    for (int k = threadIdx.x; k < i; k += NT) s_rhs[k] = __dsub_rn(s_rhs[k], __dmul_rn(__ldcg(R + (size_t)i * ldr + k), yi));
+    for (int k = threadIdx.x; k < i; k += NT)
+      s_rhs[k] = __dsub_rn(s_rhs[k], __dmul_rn(__ldcg(R + (size_t)i * ldr + k), yi));
     __syncthreads();
   }
   for (int k = threadIdx.x; k < J; k += NT) y_out[k] = s_y[k];
@@ -446,7 +684,7 @@ struct SmemLayout {
   size_t off_part, off_out, off_tmp, off_h, off_cs, off_sn, off_s, off_y, off_rhs, off_coef, off_tiles, total;
   __host__ __device__ SmemLayout(int kmax_, int tile_bytes) : kmax(kmax_) {
     size_t o = 0;
-    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 127) & ~size_t(127); return r; };
     off_part = take(sizeof(double) * kmax);
     off_out = take(sizeof(double) * kmax);
     off_tmp = take(sizeof(double) * NW * kmax);
@@ -462,27 +700,92 @@ struct SmemLayout {
   }
 };
 
+#define G200_SMEM_CARVE(W)                                                  \
+  extern __shared__ __align__(128) char dsm[];                              \
+  __shared__ Shm sh;                                                        \
+  const SmemLayout lay(d.kmax, d.tile_bytes);                               \
+  double* s_part = reinterpret_cast<double*>(dsm + lay.off_part);           \
+  double* s_out = reinterpret_cast<double*>(dsm + lay.off_out);             \
+  double* s_tmp = reinterpret_cast<double*>(dsm + lay.off_tmp);             \
+  double* s_h = reinterpret_cast<double*>(dsm + lay.off_h);                 \
+  double* s_cs = reinterpret_cast<double*>(dsm + lay.off_cs);               \
+  double* s_sn = reinterpret_cast<double*>(dsm + lay.off_sn);               \
+  double* s_s = reinterpret_cast<double*>(dsm + lay.off_s);                 \
+  double* s_y = reinterpret_cast<double*>(dsm + lay.off_y);                 \
+  double* s_rhs = reinterpret_cast<double*>(dsm + lay.off_rhs);             \
+  W* s_coefW = reinterpret_cast<W*>(dsm + lay.off_coef);                    \
+  char* s_tiles = dsm + lay.off_tiles;                                      \
+  (void)s_part; (void)s_out; (void)s_tmp; (void)s_h; (void)s_cs; (void)s_sn; \
+  (void)s_s; (void)s_y; (void)s_rhs; (void)s_coefW; (void)s_tiles;          \
+  init_shm(sh);
+
+// Orthogonalisation of w (own rows) against V[:, 0..j) and its norm: MGS
+// or CGSR (two passes).  s_h[0..j) gets
+// h_{1..j, j}; returns ‖w‖² through NN.
+template <class W>
+__device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
+                            double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
+                            char* s_tiles, double& NN) {
+  if (d.ortho == 0) {
+    W hprev = (W)0;
+    for (int i = 1; i <= j; ++i) {
+      double p[1] = {mgs_sweep<W>(r0, r1, w, i > 1 ? V + (long long)(i - 2) * ldv : nullptr, hprev,
+                                  V + (long long)(i - 1) * ldv)};
+      block_sum<1>(p, sh, s_part);
+      if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
+      if (threadIdx.x == 0) s_h[i - 1] = s_out[0];
+      hprev = RN<W>(s_out[0]);
+    }
+    double p[1] = {mgs_sweep<W>(r0, r1, w, V + (long long)(j - 1) * ldv, hprev, nullptr)};
+    block_sum<1>(p, sh, s_part);
+    if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
+    NN = s_out[0];
+    return true;
+  }
+  double nn = 0.0;
+  const bool lead = d.profile && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long tp = lead ? globaltimer() : 0ull;
+  auto sub = [&](int slot) {
+    if (d.profile) {
+      grid_sync(d, sh);
+      if (lead) { const unsigned long long t = globaltimer(); d.prof[8 + slot] += t - tp; tp = t; }
+    }
+  };
+  rowtile_pass<W, 1>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  combine_acc(s_tmp, j, s_part);
+  sub(0);
+  if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return false;
+  sub(1);
+  for (int i = threadIdx.x; i < j; i += NT) {
+    s_h[i] = s_out[i];
+    s_coefW[i] = RN<W>(s_out[i]);
+  }
+  __syncthreads();
+  rowtile_pass<W, 2>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  combine_acc(s_tmp, j, s_part);
+  sub(2);
+  if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return false;
+  sub(3);
+  for (int i = threadIdx.x; i < j; i += NT) {
+    s_h[i] = s_h[i] + s_out[i];
+    s_coefW[i] = RN<W>(s_out[i]);
+  }
+  __syncthreads();
+  nn = 0.0;
+  rowtile_pass<W, 3>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  double p[1] = {nn};
+  block_sum<1>(p, sh, s_part);
+  sub(4);
+  if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
+  sub(5);
+  NN = s_out[0];
+  return true;
+}
+
 // ---------------------------------------------------------- the solve
 template <class W, int L>
 __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ Shm sh;
-  const SmemLayout lay(d.kmax, d.tile_bytes);
-  double* s_part = reinterpret_cast<double*>(dsm + lay.off_part);
-  double* s_out = reinterpret_cast<double*>(dsm + lay.off_out);
-  double* s_tmp = reinterpret_cast<double*>(dsm + lay.off_tmp);
-  double* s_h = reinterpret_cast<double*>(dsm + lay.off_h);
-  double* s_cs = reinterpret_cast<double*>(dsm + lay.off_cs);
-  double* s_sn = reinterpret_cast<double*>(dsm + lay.off_sn);
-  double* s_s = reinterpret_cast<double*>(dsm + lay.off_s);
-  double* s_y = reinterpret_cast<double*>(dsm + lay.off_y);
-  double* s_rhs = reinterpret_cast<double*>(dsm + lay.off_rhs);
-  W* s_coefW = reinterpret_cast<W*>(dsm + lay.off_coef);
-  char* s_tiles = dsm + lay.off_tiles;
-
-  if (threadIdx.x == 0) { sh.epoch = 0; sh.red_epoch = 0; sh.abort = 0; sh.flag = 0; sh.status = 0; }
-  __syncthreads();
-
+  G200_SMEM_CARVE(W)
   const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
   W* const wb0 = reinterpret_cast<W*>(d.w0);
   W* const wb1 = reinterpret_cast<W*>(d.w1);
@@ -499,7 +802,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     // ---------------- residual, stop test (Alg. 1 lines 86–92)
     double v3[3] = {0.0, 0.0, 0.0};
     int err = 0;
-    resid_rows<W, L>(d, r0, r1, wb0, v3[0], v3[1], v3[2], err);
+    resid_phase<W, L>(d, sh, s_tiles, wb0, v3[0], v3[1], v3[2], err);
     if (err) atomicOr(d.err_flag, err);
     block_sum<3>(v3, sh, s_part);
     if (!grid_allreduce(d, sh, s_part, 3, s_out, s_tmp)) { status = ST_ETIMEOUT; break; }
@@ -535,53 +838,19 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     int J = 0;
     bool fail = false;
     for (int j = 1; j <= d.m; ++j) {
-      // ------------ v_j (own rows) and w = M⁻¹ A v_j   (lines 100, 105)
-      write_vcol<W>(r0, r1, src, inv, V + (long long)(j - 1) * ldv);
-      spmv_rows<W, L>(d, r0, r1, src, inv, dst);
-      __syncthreads();
+      // ------------ w = M⁻¹ A v_j, v_j (own rows) → V   (lines 100, 105)
+      const unsigned long long ts0 = d.profile && threadIdx.x == 0 ? globaltimer() : 0ull;
+      spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V + (long long)(j - 1) * ldv);
+      if (d.profile) {
+        if (threadIdx.x == 0) d.prof_cta[blockIdx.x] += globaltimer() - ts0;
+        if (!grid_sync(d, sh)) { fail = true; break; }
+      }
       tick(PH_SPMV);
       // ------------ orthogonalise (line 101) and ‖w‖ (line 104)
       double NN;
-      if (d.ortho == 0) {
-        W hprev = (W)0;
-        for (int i = 1; i <= j; ++i) {
-          double p[1] = {mgs_sweep<W>(r0, r1, dst, i > 1 ? V + (long long)(i - 2) * ldv : nullptr, hprev,
-                                      V + (long long)(i - 1) * ldv)};
-          block_sum<1>(p, sh, s_part);
-          if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) { fail = true; break; }
-          if (threadIdx.x == 0) s_h[i - 1] = s_out[0];
-          hprev = RN<W>(s_out[0]);
-        }
-        if (fail) break;
-        double p[1] = {mgs_sweep<W>(r0, r1, dst, V + (long long)(j - 1) * ldv, hprev, nullptr)};
-        block_sum<1>(p, sh, s_part);
-        if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) { fail = true; break; }
-        NN = s_out[0];
-      } else {
-        double nn = 0.0;
-        for (int i = threadIdx.x; i < j; i += NT) s_part[i] = 0.0;
-        __syncthreads();
-        tile_pass<W, 1>(d, r0, r1, V, ldv, j, dst, s_coefW, s_y, s_part, nn, s_tiles);
-        if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) { fail = true; break; }
-        for (int i = threadIdx.x; i < j; i += NT) {
-          s_h[i] = s_out[i];
-          s_coefW[i] = RN<W>(s_out[i]);
-          s_part[i] = 0.0;
-        }
-        __syncthreads();
-        tile_pass<W, 2>(d, r0, r1, V, ldv, j, dst, s_coefW, s_y, s_part, nn, s_tiles);
-        if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) { fail = true; break; }
-        for (int i = threadIdx.x; i < j; i += NT) {
-          s_h[i] = s_h[i] + s_out[i];
-          s_coefW[i] = RN<W>(s_out[i]);
-        }
-        __syncthreads();
-        nn = 0.0;
-        tile_pass<W, 3>(d, r0, r1, V, ldv, j, dst, s_coefW, s_y, s_part, nn, s_tiles);
-        double p[1] = {nn};
-        block_sum<1>(p, sh, s_part);
-        if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) { fail = true; break; }
-        NN = s_out[0];
+      if (!ortho_phase<W>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) {
+        fail = true;
+        break;
       }
       tick(PH_ORTHO);
       // ------------ h_{j+1,j}, Givens, exit test (lines 104, 108–140, 98)
@@ -606,13 +875,14 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     }
     if (fail) { if (status == ST_OK) status = ST_ETIMEOUT; break; }
     total_inner += J;
+    if (lead && k < d.hist_cap) d.cycle_J[k] = J;
     // ------------ y = R⁻¹ s, x ← x + V_J y  (lines 143–147)
     if (blockIdx.x == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     for (int i = threadIdx.x; i < J; i += NT) s_y[i] = __ldcg(d.y + i);
     __syncthreads();
     double dummy = 0.0;
-    tile_pass<W, 4>(d, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_part, dummy, s_tiles);
+    rowtile_pass<W, 4>(d, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     tick(PH_UPDATE);
     ++k;
@@ -658,79 +928,28 @@ __global__ void dinv_kernel(int n, const int* __restrict__ rp, const int* __rest
 // Each runs the same device functions as solve_kernel for one step.
 template <class W, int L>
 __global__ void __launch_bounds__(NT, 1) k_spmv_kernel(Dev d, const W* v, W* w) {
-  const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
-  spmv_rows<W, L>(d, r0, r1, v, 1.0, w);
+  G200_SMEM_CARVE(W)
+  spmv_phase<W, L>(d, sh, s_tiles, v, 1.0, w, nullptr);
 }
 
 template <class W, int L>
 __global__ void __launch_bounds__(NT, 1) k_resid_kernel(Dev d, W* r, double* out2) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ Shm sh;
-  const SmemLayout lay(d.kmax, d.tile_bytes);
-  double* s_part = reinterpret_cast<double*>(dsm + lay.off_part);
-  double* s_out = reinterpret_cast<double*>(dsm + lay.off_out);
-  double* s_tmp = reinterpret_cast<double*>(dsm + lay.off_tmp);
-  if (threadIdx.x == 0) { sh.epoch = 0; sh.red_epoch = 0; sh.abort = 0; }
-  __syncthreads();
-  const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
-  double v2[2] = {0.0, 0.0}, bb = 0.0;
+  G200_SMEM_CARVE(W)
+  double v3[3] = {0.0, 0.0, 0.0};
   int err = 0;
-  resid_rows<W, L>(d, r0, r1, r, v2[0], v2[1], bb, err);
+  resid_phase<W, L>(d, sh, s_tiles, r, v3[0], v3[1], v3[2], err);
   if (err) atomicOr(d.err_flag, err);
-  block_sum<2>(v2, sh, s_part);
-  if (!grid_allreduce(d, sh, s_part, 2, s_out, s_tmp)) return;
+  block_sum<3>(v3, sh, s_part);
+  if (!grid_allreduce(d, sh, s_part, 3, s_out, s_tmp)) return;
   if (blockIdx.x == 0 && threadIdx.x < 2) out2[threadIdx.x] = s_out[threadIdx.x];
 }
 
 template <class W>
 __global__ void __launch_bounds__(NT, 1) k_ortho_kernel(Dev d, int j, const W* V, long long ldv, W* w, double* hout) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ Shm sh;
-  const SmemLayout lay(d.kmax, d.tile_bytes);
-  double* s_part = reinterpret_cast<double*>(dsm + lay.off_part);
-  double* s_out = reinterpret_cast<double*>(dsm + lay.off_out);
-  double* s_tmp = reinterpret_cast<double*>(dsm + lay.off_tmp);
-  double* s_h = reinterpret_cast<double*>(dsm + lay.off_h);
-  double* s_y = reinterpret_cast<double*>(dsm + lay.off_y);
-  W* s_coefW = reinterpret_cast<W*>(dsm + lay.off_coef);
-  char* s_tiles = dsm + lay.off_tiles;
-  if (threadIdx.x == 0) { sh.epoch = 0; sh.red_epoch = 0; sh.abort = 0; }
-  __syncthreads();
+  G200_SMEM_CARVE(W)
   const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
-  double NN;
-  if (d.ortho == 0) {
-    W hprev = (W)0;
-    for (int i = 1; i <= j; ++i) {
-      double p[1] = {mgs_sweep<W>(r0, r1, w, i > 1 ? V + (long long)(i - 2) * ldv : nullptr, hprev,
-                                  V + (long long)(i - 1) * ldv)};
-      block_sum<1>(p, sh, s_part);
-      if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return;
-      if (threadIdx.x == 0) s_h[i - 1] = s_out[0];
-      hprev = RN<W>(s_out[0]);
-    }
-    double p[1] = {mgs_sweep<W>(r0, r1, w, V + (long long)(j - 1) * ldv, hprev, nullptr)};
-    block_sum<1>(p, sh, s_part);
-    if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return;
-    NN = s_out[0];
-  } else {
-    double nn = 0.0;
-    for (int i = threadIdx.x; i < j; i += NT) s_part[i] = 0.0;
-    __syncthreads();
-    tile_pass<W, 1>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_part, nn, s_tiles);
-    if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return;
-    for (int i = threadIdx.x; i < j; i += NT) { s_h[i] = s_out[i]; s_coefW[i] = RN<W>(s_out[i]); s_part[i] = 0.0; }
-    __syncthreads();
-    tile_pass<W, 2>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_part, nn, s_tiles);
-    if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return;
-    for (int i = threadIdx.x; i < j; i += NT) { s_h[i] = s_h[i] + s_out[i]; s_coefW[i] = RN<W>(s_out[i]); }
-    __syncthreads();
-    nn = 0.0;
-    tile_pass<W, 3>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_part, nn, s_tiles);
-    double p[1] = {nn};
-    block_sum<1>(p, sh, s_part);
-    if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return;
-    NN = s_out[0];
-  }
+  double NN = 0.0;
+  if (!ortho_phase<W>(d, sh, r0, r1, j, V, ldv, w, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) return;
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < j; i += NT) hout[i] = s_h[i];
     if (threadIdx.x == 0) hout[j] = sqrt(NN);
@@ -739,23 +958,59 @@ __global__ void __launch_bounds__(NT, 1) k_ortho_kernel(Dev d, int j, const W* V
 
 template <class W>
 __global__ void __launch_bounds__(NT, 1) k_xupdate_kernel(Dev d, int J, const W* V, long long ldv, const double* y) {
-  extern __shared__ __align__(16) char dsm[];
-  const SmemLayout lay(d.kmax, d.tile_bytes);
-  double* s_y = reinterpret_cast<double*>(dsm + lay.off_y);
-  double* s_part = reinterpret_cast<double*>(dsm + lay.off_part);
-  W* s_coefW = reinterpret_cast<W*>(dsm + lay.off_coef);
-  char* s_tiles = dsm + lay.off_tiles;
+  G200_SMEM_CARVE(W)
   for (int i = threadIdx.x; i < J; i += NT) s_y[i] = y[i];
   __syncthreads();
   const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
   double dummy = 0.0;
-  tile_pass<W, 4>(d, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_part, dummy, s_tiles);
+  rowtile_pass<W, 4>(d, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
+}
+
+// Device microbenchmark of the solve's building blocks (dev tool): `iters`
+// repetitions of what = 0 grid barrier, 1 one-value grid all-reduce, 2 MGS
+// sweep (no reduction), 3 CGS tile pass MODE 1 over ncols columns, 4 tile
+// pass MODE 2, 5 tile pass MODE 3.  out_ns = CTA 0's %globaltimer span.
+template <class W>
+__global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int iters, int ncols, const W* V,
+                                                      long long ldv, W* w, unsigned long long* out_ns) {
+  G200_SMEM_CARVE(W)
+  const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
+  for (int i = threadIdx.x; i < ncols; i += NT) { s_part[i] = 0.0; s_coefW[i] = (W)1e-3; }
+  for (int i = threadIdx.x; i < NW * d.kmax; i += NT) s_tmp[i] = 0.0;
+  if (!grid_sync(d, sh)) return;
+  const unsigned long long t0 = globaltimer();
+  double acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    if (what == 0) {
+      if (!grid_sync(d, sh)) return;
+    } else if (what == 1) {
+      double p[1] = {1.0};
+      block_sum<1>(p, sh, s_part);
+      if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return;
+    } else if (what == 2) {
+      acc += mgs_sweep<W>(r0, r1, w, V, (W)1e-3, V + ldv);
+      __syncthreads();
+    } else if (what == 3) {
+      rowtile_pass<W, 1>(d, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
+      __syncthreads();
+    } else if (what == 4) {
+      rowtile_pass<W, 2>(d, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
+      __syncthreads();
+    } else {
+      rowtile_pass<W, 3>(d, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
+      __syncthreads();
+    }
+  }
+  if (!grid_sync(d, sh)) return;
+  const unsigned long long t1 = globaltimer();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out_ns[0] = t1 - t0;
+  if (acc == 12345.678) out_ns[1] = 1;  // keep the work alive
 }
 
 // a6 + a7 on a given unrotated Hessenberg (tests): one CTA.
 __global__ void __launch_bounds__(NT, 1) k_hess_kernel(int m, int J, const double* Hbar, double beta, double* R,
                                                      double* s, double* y) {
-  extern __shared__ __align__(16) char dsm[];
+  extern __shared__ __align__(128) char dsm[];
   double* s_h = reinterpret_cast<double*>(dsm);
   double* s_cs = s_h + (m + 2);
   double* s_sn = s_cs + (m + 1);

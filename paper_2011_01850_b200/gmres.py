@@ -31,12 +31,13 @@ class GmresError(RuntimeError):
 
 class _Result(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("cycles", ctypes.c_int32), ("inner_iters", ctypes.c_int32),
-                ("history_len", ctypes.c_int32), ("final_relres", ctypes.c_double), ("device_ms", ctypes.c_double)]
+                ("history_len", ctypes.c_int32), ("final_relres", ctypes.c_double), ("device_ms", ctypes.c_double),
+                ("kernel_ms", ctypes.c_double)]
 
 
 class _Opts(ctypes.Structure):
     _fields_ = [("delta", ctypes.c_double), ("max_cycles", ctypes.c_int32), ("record_inner", ctypes.c_int32),
-                ("lanes_per_row", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+                ("lanes_per_row", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32), ("profile", ctypes.c_int32)]
 
 
 def library_path() -> str:
@@ -62,6 +63,8 @@ def load_library():
     L.gmres_solve_device.restype = ctypes.c_int
     L.gmres_get_inner_history.argtypes = [vp, vp, i32, ctypes.POINTER(i32)]
     L.gmres_get_inner_history.restype = ctypes.c_int
+    L.gmres_get_cycle_iters.argtypes = [vp, vp, i32, ctypes.POINTER(i32)]
+    L.gmres_get_cycle_iters.restype = ctypes.c_int
     L.gmres_get_phase_ns.argtypes = [vp, vp, i32]
     L.gmres_get_phase_ns.restype = ctypes.c_int
     L.gmres_last_error.argtypes = [vp]
@@ -74,9 +77,10 @@ def load_library():
     L.gmres_k_xupdate.argtypes = [vp, i32, i32, vp, i64, vp, vp]
     L.gmres_k_hessenberg.argtypes = [vp, i32, i32, vp, dbl, vp, vp, vp]
     L.gmres_k_cast32.argtypes = [vp]
+    L.gmres_k_micro.argtypes = [vp, i32, i32, i32, i32, vp, i64, vp, vp]
     L.gmres_k_matrix.argtypes = [vp, vp, vp, vp, vp, vp]
     for f in ("gmres_k_spmv", "gmres_k_resid", "gmres_k_ortho", "gmres_k_xupdate", "gmres_k_hessenberg",
-              "gmres_k_cast32", "gmres_k_matrix"):
+              "gmres_k_cast32", "gmres_k_matrix", "gmres_k_micro"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -115,6 +119,8 @@ class SolveResult:
     final_relres: float
     device_ms: float
     history: np.ndarray
+    kernel_ms: float = 0.0
+    cycle_iters: np.ndarray | None = None
     x: object = None
     inner: np.ndarray | None = None
     phase_ns: np.ndarray | None = None
@@ -160,13 +166,14 @@ class Solver:
         return GmresError(rc, self._lib.gmres_last_error(self._h).decode())
 
     @staticmethod
-    def _opts(delta, max_cycles, record_inner, lanes, ctas_per_sm):
+    def _opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile=False):
         o = _Opts()
         o.delta = -1.0 if delta is None else float(delta)
         o.max_cycles = 0 if max_cycles is None else int(max_cycles)
         o.record_inner = 1 if record_inner else 0
         o.lanes_per_row = int(lanes)
         o.ctas_per_sm = int(ctas_per_sm)
+        o.profile = 1 if profile else 0
         return o
 
     def _finish(self, rc, res, hist, hl, record_inner):
@@ -178,10 +185,15 @@ class Solver:
             self._lib.gmres_get_inner_history(self._h, None, 0, ctypes.byref(ln))
             inner = np.zeros(ln.value)
             self._lib.gmres_get_inner_history(self._h, _p(inner), ln.value, ctypes.byref(ln))
-        ph = np.zeros(8)
-        self._lib.gmres_get_phase_ns(self._h, _p(ph), 8)
+        ph = np.zeros(16)
+        self._lib.gmres_get_phase_ns(self._h, _p(ph), 16)
+        ln = ctypes.c_int32()
+        self._lib.gmres_get_cycle_iters(self._h, None, 0, ctypes.byref(ln))
+        cj = np.zeros(ln.value, np.int32)
+        self._lib.gmres_get_cycle_iters(self._h, _p(cj), ln.value, ctypes.byref(ln))
         return SolveResult(res.status, res.cycles, res.inner_iters, res.final_relres, res.device_ms,
-                           hist[:min(hl.value, hist.size)].copy(), inner=inner, phase_ns=ph)
+                           hist[:min(hl.value, hist.size)].copy(), kernel_ms=res.kernel_ms, cycle_iters=cj,
+                           inner=inner, phase_ns=ph)
 
     def solve(self, b, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None, max_cycles=None,
               record_inner=False, lanes=0, ctas_per_sm=0) -> SolveResult:
@@ -202,7 +214,8 @@ class Solver:
         return out
 
     def solve_device(self, b, x, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None,
-                     max_cycles=None, record_inner=False, lanes=0, ctas_per_sm=0, stream=None) -> SolveResult:
+                     max_cycles=None, record_inner=False, lanes=0, ctas_per_sm=0, stream=None,
+                     profile=False) -> SolveResult:
         """gmres_solve_device on torch CUDA float64 tensors (x is written in place)."""
         import torch
         for t in (b, x) + ((x0,) if x0 is not None else ()):
@@ -212,7 +225,7 @@ class Solver:
         hist = np.zeros(mc + 2)
         hl = ctypes.c_int32()
         res = _Result()
-        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm)
+        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile)
         rc = self._lib.gmres_solve_device(self._h, _p(b), _p(x0), _p(x), int(m), float(tol), _ortho(ortho),
                                           _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
                                           ctypes.byref(hl), ctypes.c_void_p(st.cuda_stream))
@@ -245,6 +258,12 @@ class Solver:
     def k_xupdate(self, precision, J, V, ldv, y, x):
         y = np.ascontiguousarray(y, np.float64)
         self._ck(self._lib.gmres_k_xupdate(self._h, _prec(precision), int(J), _p(V), int(ldv), _p(y), _p(x)))
+
+    def k_micro(self, precision, what, iters, ncols, V, ldv, w):
+        ns = np.zeros(1)
+        self._ck(self._lib.gmres_k_micro(self._h, _prec(precision), int(what), int(iters), int(ncols), _p(V),
+                                         int(ldv), _p(w), _p(ns)))
+        return float(ns[0])
 
     def k_hessenberg(self, m, J, Hbar, beta):
         Hc = np.asfortranarray(Hbar, np.float64)  # (m+1, m) column-major
