@@ -68,6 +68,7 @@ typedef struct {
   int32_t lanes_per_row;  /* SpMV sub-warp width 4/8/16/32; 0 = auto from mean row length */
   int32_t ctas_per_sm;    /* 0 = auto (occupancy)                                       */
   int32_t profile;        /* != 0: grid barrier after each phase for clean phase timers */
+  int32_t tune;           /* developer A/B switches; 0 = production defaults            */
 } gmres_opts;
 
 /* Create a solver context on the current CUDA device: validates the CSR on the

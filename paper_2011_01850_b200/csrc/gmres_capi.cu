@@ -59,6 +59,7 @@ struct gmres_ctx {
   int4* d_chunks = nullptr;
   int* d_chunk_off = nullptr;
   int part_G = 0;
+  int part_max_rows = 0;  // largest CTA row block of the partition
   // last solve
   std::vector<double> inner_host;
   std::vector<int32_t> cycJ_host;
@@ -179,12 +180,34 @@ int kmax_for(int m) { return std::max(m + 1, 4); }
 
 // shared staging region: two CSR chunk stages, or two V tiles of ≥ 32 rows
 int tile_bytes_for(int m) { return std::max(TILE_BYTES, 2 * (m + 2) * ROWALIGN * 8); }
-size_t smem_bytes(int m) { return SmemLayout(kmax_for(m), tile_bytes_for(m)).total; }
+size_t smem_bytes(int m, int tile_bytes = 0) {
+  return SmemLayout(kmax_for(m), tile_bytes ? tile_bytes : tile_bytes_for(m)).total;
+}
+constexpr size_t kMaxDynSmem = 227 * 1024;
+
+struct OccKey { const void* k; size_t smem; };
+thread_local std::vector<std::pair<OccKey, int>> g_occ;  // (kernel, smem) → blocks per SM
 
 int grid_for(gmres_ctx* ctx, const void* kern, size_t smem, int ctas_per_sm, int* G) {
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  int per_sm = -1;
+  for (auto& e : g_occ)
+    if (e.first.k == kern && e.first.smem == smem) per_sm = e.second;
+  // the attribute is per kernel: set it to the largest smem used so far
+  static thread_local std::vector<std::pair<const void*, size_t>> g_attr;
+  size_t cur = 0;
+  for (auto& a : g_attr)
+    if (a.first == kern) cur = a.second;
+  if (smem > cur) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bool found = false;
+    for (auto& a : g_attr)
+      if (a.first == kern) { a.second = smem; found = true; }
+    if (!found) g_attr.push_back({kern, smem});
+  }
+  if (per_sm < 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    g_occ.push_back({OccKey{kern, smem}, per_sm});
+  }
   if (per_sm < 1) return fail(ctx, GMRES_ECUDA, "solve kernel cannot be resident (occupancy 0)");
   if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
   *G = per_sm * ctx->sms;
@@ -228,6 +251,8 @@ int ensure_partition(gmres_ctx* ctx, int G) {
   if (ctx->part_G == G && ctx->d_row_begin) return 0;
   std::vector<int> rb;
   make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, rb);
+  ctx->part_max_rows = 0;
+  for (int g = 0; g < G; ++g) ctx->part_max_rows = std::max(ctx->part_max_rows, rb[g + 1] - rb[g]);
   std::vector<int4> ent;
   std::vector<int> off;
   make_chunks(ctx->h_rp, ctx->n, rb, ent, off);
@@ -296,6 +321,17 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   ctx->ws_m = m;
   ctx->ws_prec = prec;
   ctx->ws_G = G;
+  return 0;
+}
+
+// A32 = RN32(A64) on the stream with the overflow flag in err (device int).
+int launch_cast(gmres_ctx* ctx, cudaStream_t st, int* d_errflag) {
+  if (!ctx->d_a32) {
+    CK(cudaMalloc(&ctx->d_a32, sizeof(float) * (ctx->nnz + ARR_PAD)));
+    CK(cudaMemset(ctx->d_a32, 0, sizeof(float) * (ctx->nnz + ARR_PAD)));
+  }
+  cast32_kernel<<<ctx->sms * 8, 256, 0, st>>>(ctx->d_a64, ctx->d_a32, ctx->nnz, d_errflag);
+  CK(cudaGetLastError());
   return 0;
 }
 
@@ -494,17 +530,38 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
 
   const void* kern = pick_solve(precision, L);
-  const size_t smem = smem_bytes(m);
+  int tile_bytes = tile_bytes_for(m);
+  size_t smem = smem_bytes(m, tile_bytes);
   int G = 0;
   if (int rc = grid_for(ctx, kern, smem, opts ? opts->ctas_per_sm : 0, &G)) return rc;
   if (int rc = ensure_partition(ctx, G)) return rc;
+  // resident MGS (gmres_kernels.cuh mgs_resident): every CTA's rows of w and of
+  // one basis vector in shared memory, ≤ MGS_MV 16-byte vectors per thread
+  int mgs_resident = 0;
+  {
+    const int wb = precision == GMRES_MIXED ? 4 : 8;
+    const int per_vec = 16 / wb;
+    const int res_bytes = 2 * ctx->part_max_rows * wb;
+    const int tb = std::max(tile_bytes, res_bytes);
+    if (ortho == GMRES_MGS && ctx->part_max_rows / per_vec <= MGS_MV * NT && smem_bytes(m, tb) <= kMaxDynSmem) {
+      int G2 = 0;
+      if (grid_for(ctx, kern, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 == G) {
+        mgs_resident = 1;
+        tile_bytes = tb;
+        smem = smem_bytes(m, tb);
+      }
+    }
+  }
   const int hist_cap_dev = max_cycles + 2;
   const int inner_cap_dev = rec_inner ? (int)std::min<int64_t>((int64_t)max_cycles * m, 1 << 22) : 0;
   if (int rc = ensure_ws(ctx, m, precision, G, hist_cap_dev, inner_cap_dev)) return rc;
 
   CK(cudaEventRecord(ctx->ev0, st));
-  if (precision == GMRES_MIXED) {  // a0: rebuilt inside every timed solve
-    if (int rc = ensure_a32(ctx, st, true)) return rc;
+  if (int rc = reset_flags(ctx, st)) return rc;
+  if (precision == GMRES_MIXED) {  // a0: rebuilt inside every timed solve;
+    // overflow is flagged on the device and reported by the solve kernel
+    if (int rc = launch_cast(ctx, st, ctx->d_flags + 1)) return rc;
+    ctx->a32_ready = false;  // validated only by a completed solve
   }
   if (d_x0 && d_x0 != d_x) CK(cudaMemcpyAsync(d_x, d_x0, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
   if (!d_x0) CK(cudaMemsetAsync(d_x, 0, sizeof(double) * ctx->n, st));
@@ -520,9 +577,11 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   d.max_cycles = max_cycles;
   d.inner_cap = inner_cap_dev;
   d.profile = (opts && opts->profile) ? 1 : 0;
+  d.tile_bytes = tile_bytes;
+  d.mgs_resident = mgs_resident;
+  d.tune = opts ? opts->tune : 0;
 
   gmres_result r{};
-  if (int rc = reset_flags(ctx, st)) return rc;
   void* args[] = {&d};
   CK(cudaEventRecord(ctx->evk0, st));
   if (int rc = launch_coop(ctx, kern, G, smem, args, st)) return rc;
@@ -570,7 +629,8 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   }
   if (res) *res = r;
   if (r.status == ST_ETIMEOUT) return fail(ctx, GMRES_ETIMEOUT, "device watchdog fired in a grid barrier");
-  if (r.status == ST_EFP32RANGE) return fail(ctx, GMRES_EFP32RANGE, "residual entry outside the fp32 range");
+  if (precision == GMRES_MIXED && r.status != ST_EFP32RANGE) ctx->a32_ready = true;
+  if (r.status == ST_EFP32RANGE) return fail(ctx, GMRES_EFP32RANGE, "matrix or residual entry outside the fp32 range");
   if (r.status == ST_ENONFINITE) return fail(ctx, GMRES_ENONFINITE, "non-finite value in the residual or Arnoldi process");
   return r.status;
 }
@@ -672,7 +732,7 @@ int gmres_k_spmv(gmres_ctx* ctx, int32_t precision, const void* d_v, void* d_w) 
   if (int rc = comp_setup(ctx, precision, 1, 0, L, &kern, &G, &smem, &mws)) return rc;
   Dev d = make_dev(ctx, mws, precision, 0, G);
   void* args[] = {&d, (void*)&d_v, &d_w};
-  CK(cudaLaunchKernel(kern, dim3(G), dim3(NT), args, smem, ctx->stream));
+  if (int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream)) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
@@ -758,7 +818,7 @@ int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_
   CK(cudaMemcpy(d_y, y, sizeof(double) * J, cudaMemcpyHostToDevice));
   long long ld = ldv;
   void* args[] = {&d, &J, (void*)&d_V, &ld, &d_y};
-  cudaError_t e = cudaLaunchKernel(kern, dim3(G), dim3(NT), args, smem, ctx->stream);
+  cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(NT), args, smem, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   cudaFree(d_y);
   if (e != cudaSuccess) return fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
@@ -779,6 +839,8 @@ int gmres_k_micro(gmres_ctx* ctx, int32_t precision, int32_t what, int32_t iters
   if (int rc = grid_for(ctx, kern, smem, 0, &Gk)) return rc;
   if (Gk < G) return fail(ctx, GMRES_ECUDA, "micro kernel occupancy below the solve grid");
   Dev d = make_dev(ctx, m, precision, 0, G);
+  d.tune = what >> 8;
+  what &= 0xff;
   unsigned long long* d_ns = nullptr;
   CK(cudaMalloc(&d_ns, 16));
   CK(cudaMemset(d_ns, 0, 16));

@@ -83,6 +83,8 @@ struct Dev {
   unsigned long long* prof;   // [PH_N] ns accumulated by CTA 0
   unsigned long long* prof_cta;  // [G] per-CTA own SpMV ns (profile mode)
   int profile;          // != 0: grid barrier after every phase (clean attribution)
+  int tune;             // developer A/B switches (bit 0: no L2 prefetch in MGS, bit 2: no resident MGS)
+  int mgs_resident;     // != 0: every CTA's w and v row blocks fit the staging region (resident MGS)
   long long timeout_ns;
 };
 
@@ -136,6 +138,10 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// bulk prefetch of [src, src+bytes) into L2 (bytes multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
   unsigned ok;
@@ -197,12 +203,20 @@ __device__ __forceinline__ void init_shm(Shm& sh) {
 // Grid-wide barrier over the co-resident (cooperative) grid: monotone 64-bit
 // arrival counter, release/acquire through __threadfence + atomics.  A device
 // watchdog (globaltimer) aborts every CTA instead of hanging the GPU.
+__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ bool grid_sync(const Dev& d, Shm& sh) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned long long target = (sh.epoch += 1ull) * (unsigned long long)d.G;
-    __threadfence();
-    atomicAdd(d.bar, 1ull);
+    if (d.tune & 2) {  // reference variant: full fences around a returning atomic
+      __threadfence();
+      atomicAdd(d.bar, 1ull);
+    } else {
+      red_release_add_u64(d.bar, 1ull);  // release: orders this CTA's prior writes (after bar.sync)
+    }
     int ab = 0;
     unsigned long long t0 = 0;
     unsigned it = 0;
@@ -214,7 +228,7 @@ __device__ __forceinline__ bool grid_sync(const Dev& d, Shm& sh) {
         else if ((long long)(t - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); ab = 1; break; }
       }
     }
-    __threadfence();
+    if (d.tune & 2) __threadfence();
     if (!ab && *(volatile int*)d.abort_flag) ab = 1;
     sh.abort = ab;
   }
@@ -719,6 +733,103 @@ struct SmemLayout {
   (void)s_s; (void)s_y; (void)s_rhs; (void)s_coefW; (void)s_tiles;          \
   init_shm(sh);
 
+// ------------------------------------------------------------------ a3 (resident)
+// MGS with the CTA's rows of w and of the previous basis vector resident in
+// shared memory and the next basis vector in registers: step i updates
+// w ← RN_W(w − RN_W(h_{i−1})·v_{i−1}) from shared memory, forms the partial of
+// h_i = w·v_i from registers, then issues the loads of v_{i+1} BEFORE waiting
+// on h_i's grid reduction, so their latency hides behind the all-reduce.
+// Same operations and order per element as mgs_sweep.
+constexpr int MGS_MV = 8;  // 16-byte vectors per thread kept in registers
+template <class W>
+__device__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
+                             double* s_part, double* s_out, double* s_tmp, double* s_h, char* s_tiles, double& NN) {
+  using V4 = typename VecT<W>::T;
+  constexpr int N = VecT<W>::N;
+  const int q0 = r0 / N, nq = r1 / N - q0;
+  V4* sw = reinterpret_cast<V4*>(s_tiles);
+  V4* sv = sw + nq;
+  V4 vn[MGS_MV];
+  auto load_col = [&](int col) {
+    const V4* vc = reinterpret_cast<const V4*>(V + (long long)col * ldv) + q0;
+#pragma unroll
+    for (int k = 0; k < MGS_MV; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < nq) vn[k] = __ldcg(vc + t);
+    }
+  };
+  // prologue: w → shared, v_1 → registers
+  {
+    const V4* wg = reinterpret_cast<const V4*>(w) + q0;
+#pragma unroll
+    for (int k = 0; k < MGS_MV; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < nq) sw[t] = wg[t];
+    }
+  }
+  load_col(0);
+  W hprev = (W)0;
+  const bool lead = d.profile && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long tp = lead ? globaltimer() : 0ull;
+  for (int i = 1; i <= j; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < MGS_MV; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < nq) {
+        V4 a = sw[t];
+        W* pa = reinterpret_cast<W*>(&a);
+        if (i > 1) {
+          const V4 b = sv[t];
+          const W* pb = reinterpret_cast<const W*>(&b);
+#pragma unroll
+          for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hprev, pb[u]));
+          sw[t] = a;
+        }
+        const W* pc = reinterpret_cast<const W*>(&vn[k]);
+#pragma unroll
+        for (int u = 0; u < N; ++u) acc += (double)pa[u] * (double)pc[u];
+        sv[t] = vn[k];
+      }
+    }
+    if (i < j) load_col(i);  // v_{i+1}: in flight during the reduction below
+    if (lead) { const unsigned long long t = globaltimer(); d.prof[8] += t - tp; tp = t; }
+    double p[1] = {acc};
+    block_sum<1>(p, sh, s_part);
+    if (lead) { const unsigned long long t = globaltimer(); d.prof[9] += t - tp; tp = t; }
+    if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
+    if (threadIdx.x == 0) s_h[i - 1] = s_out[0];
+    hprev = RN<W>(s_out[0]);
+    if (lead) { const unsigned long long t = globaltimer(); d.prof[10] += t - tp; tp = t; }
+  }
+  // final update w ← w − h_j v_j, ‖w‖², w back to global for the next SpMV
+  double nn = 0.0;
+  {
+    V4* wg = reinterpret_cast<V4*>(w) + q0;
+#pragma unroll
+    for (int k = 0; k < MGS_MV; ++k) {
+      const int t = threadIdx.x + k * NT;
+      if (t < nq) {
+        V4 a = sw[t];
+        const V4 b = sv[t];
+        W* pa = reinterpret_cast<W*>(&a);
+        const W* pb = reinterpret_cast<const W*>(&b);
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+          pa[u] = subw(pa[u], mulw(hprev, pb[u]));
+          nn += (double)pa[u] * (double)pa[u];
+        }
+        wg[t] = a;
+      }
+    }
+  }
+  double p[1] = {nn};
+  block_sum<1>(p, sh, s_part);
+  if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
+  NN = s_out[0];
+  return true;
+}
+
 // Orthogonalisation of w (own rows) against V[:, 0..j) and its norm: MGS
 // or CGSR (two passes).  s_h[0..j) gets
 // h_{1..j, j}; returns ‖w‖² through NN.
@@ -726,11 +837,18 @@ template <class W>
 __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
                             double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
                             char* s_tiles, double& NN) {
+  if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4))
+    return mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_part, s_out, s_tmp, s_h, s_tiles, NN);
   if (d.ortho == 0) {
     W hprev = (W)0;
+    const bool pf = !(d.tune & 1) && r1 > r0;
+    const unsigned pf_bytes = (unsigned)((r1 - r0) * (int)sizeof(W));
     for (int i = 1; i <= j; ++i) {
       double p[1] = {mgs_sweep<W>(r0, r1, w, i > 1 ? V + (long long)(i - 2) * ldv : nullptr, hprev,
                                   V + (long long)(i - 1) * ldv)};
+      // while this step's reduction is in flight, pull the next basis
+      // vector's rows (v_{i+1}) of this CTA into L2
+      if (pf && i < j && threadIdx.x == 0) prefetch_l2(V + (long long)i * ldv + r0, pf_bytes);
       block_sum<1>(p, sh, s_part);
       if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
       if (threadIdx.x == 0) s_h[i - 1] = s_out[0];
@@ -798,6 +916,10 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
   };
 
   int k = 0, total_inner = 0, inner_len = 0, status = ST_OK;
+  if (*(volatile int*)d.err_flag & ERRF_RANGE) {  // A32 cast overflow (cast32_kernel, same stream)
+    if (lead) { d.out_int[0] = ST_EFP32RANGE; d.out_int[1] = 0; d.out_int[2] = 0; d.out_int[4] = 0; }
+    return;
+  }
   for (;;) {
     // ---------------- residual, stop test (Alg. 1 lines 86–92)
     double v3[3] = {0.0, 0.0, 0.0};

@@ -37,7 +37,8 @@ class _Result(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("delta", ctypes.c_double), ("max_cycles", ctypes.c_int32), ("record_inner", ctypes.c_int32),
-                ("lanes_per_row", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32), ("profile", ctypes.c_int32)]
+                ("lanes_per_row", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32), ("profile", ctypes.c_int32),
+                ("tune", ctypes.c_int32)]
 
 
 def library_path() -> str:
@@ -166,7 +167,7 @@ class Solver:
         return GmresError(rc, self._lib.gmres_last_error(self._h).decode())
 
     @staticmethod
-    def _opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile=False):
+    def _opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile=False, tune=0):
         o = _Opts()
         o.delta = -1.0 if delta is None else float(delta)
         o.max_cycles = 0 if max_cycles is None else int(max_cycles)
@@ -174,6 +175,7 @@ class Solver:
         o.lanes_per_row = int(lanes)
         o.ctas_per_sm = int(ctas_per_sm)
         o.profile = 1 if profile else 0
+        o.tune = int(tune)
         return o
 
     def _finish(self, rc, res, hist, hl, record_inner):
@@ -215,7 +217,7 @@ class Solver:
 
     def solve_device(self, b, x, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None,
                      max_cycles=None, record_inner=False, lanes=0, ctas_per_sm=0, stream=None,
-                     profile=False) -> SolveResult:
+                     profile=False, tune=0) -> SolveResult:
         """gmres_solve_device on torch CUDA float64 tensors (x is written in place)."""
         import torch
         for t in (b, x) + ((x0,) if x0 is not None else ()):
@@ -225,7 +227,7 @@ class Solver:
         hist = np.zeros(mc + 2)
         hl = ctypes.c_int32()
         res = _Result()
-        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile)
+        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile, tune)
         rc = self._lib.gmres_solve_device(self._h, _p(b), _p(x0), _p(x), int(m), float(tol), _ortho(ortho),
                                           _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
                                           ctypes.byref(hl), ctypes.c_void_p(st.cuda_stream))

@@ -2,6 +2,8 @@
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, inputs
+TUNE = int(os.environ.get('TUNE', '0'))
+TUNE = int(os.environ.get('TUNE', '0'))
 from paper_2011_01850_b200 import gmres as G
 P = inputs.make(sys.argv[1] if len(sys.argv) > 1 else "C2")
 n = P.A.n; S = G.Solver.from_csr(P.A); ld = G.ld_for(n)
@@ -9,9 +11,9 @@ for prec, wb, dt in ((G.MIXED, 4, torch.float32), (G.FP64, 8, torch.float64)):
     V = torch.rand(51, ld, dtype=dt, device="cuda") * 1e-3
     w = torch.rand(ld, dtype=dt, device="cuda")
     it = 200
-    ns = S.k_micro(prec, 0, it, 1, V, ld, w); print(f"prec={prec} grid barrier      {ns/it/1e3:7.2f} us")
-    ns = S.k_micro(prec, 1, it, 1, V, ld, w); print(f"prec={prec} allreduce(1)      {ns/it/1e3:7.2f} us")
-    ns = S.k_micro(prec, 2, it, 1, V, ld, w); print(f"prec={prec} mgs sweep         {ns/it/1e3:7.2f} us  {3*wb*n/(ns/it):7.0f} GB/s (3 vectors)")
+    ns = S.k_micro(prec, 0 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} grid barrier      {ns/it/1e3:7.2f} us")
+    ns = S.k_micro(prec, 1 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} allreduce(1)      {ns/it/1e3:7.2f} us")
+    ns = S.k_micro(prec, 2 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} mgs sweep         {ns/it/1e3:7.2f} us  {3*wb*n/(ns/it):7.0f} GB/s (3 vectors)")
     for nc in (1, 10, 25, 50):
         for mode in (3, 4, 5):
             ns = S.k_micro(prec, mode, 20, nc, V, ld, w)

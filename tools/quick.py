@@ -20,7 +20,7 @@ for prec in (G.MIXED, G.FP64):
     for ortho in (G.MGS, G.CGSR):
         best = None
         for _ in range(reps):
-            r = S.solve_device(b, x, m=m, ortho=ortho, precision=prec, lanes=lanes, profile=bool(int(os.environ.get("PROFILE", "0"))))
+            r = S.solve_device(b, x, m=m, ortho=ortho, precision=prec, lanes=lanes, profile=bool(int(os.environ.get("PROFILE", "0"))), tune=int(os.environ.get("TUNE", "0")))
             if best is None or r.kernel_ms < best.kernel_ms: best = r
         r = best
         wb = 4 if prec == G.MIXED else 8
@@ -31,4 +31,4 @@ for prec in (G.MIXED, G.FP64):
               f"per-iter {r.kernel_ms/r.inner_iters*1e3:6.1f}us  phases resid/spmv/ortho/givens/upd(ms) "
               + " ".join(f"{v:.1f}" for v in ph) + f" relres={r.final_relres:.2e}"
               + (f" spmv/CTA max {r.phase_ns[5]/1e6:.1f} mean {r.phase_ns[6]/1e6:.1f}ms" if r.phase_ns[5] else "")
-              + (" cgsr sub(ms) " + " ".join(f"{v/1e6:.1f}" for v in r.phase_ns[8:14]) if r.phase_ns[8] else ""))
+              + (" sub(ms) " + " ".join(f"{v/1e6:.1f}" for v in r.phase_ns[8:14]) if r.phase_ns[8] else ""))
