@@ -33,6 +33,8 @@ struct gmres_ctx {
   double* d_dinv64 = nullptr;
   float* d_dinv32 = nullptr;
   cudaStream_t stream = nullptr;
+  double* d_hb = nullptr;  // device staging of b / x for the host-array gmres_solve
+  double* d_hx = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
   // workspace
   int ws_m = -1, ws_prec = -1, ws_G = 0;
@@ -90,7 +92,7 @@ int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 // lanes per row in the CSR stream: one thread per row when a 512-row chunk of
 // average rows fits the stage (stencils), else the power of two that keeps
-// ~GT lanes (one warp group) busy on a chunk of CHUNK_CAP non-zeros.
+// ~GT lanes (one warp) busy on a chunk of CHUNK_CAP non-zeros.
 int auto_lanes(int64_t n, int64_t nnz) {
   const double mu = n > 0 ? (double)nnz / (double)n : 1.0;
   const double rows = std::min((double)CHUNK_RMAX, (double)CHUNK_CAP / std::max(mu, 1.0));
@@ -498,6 +500,8 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_dinv64);
   cudaFree(ctx->d_dinv32);
   cudaFree(ctx->d_ws);
+  cudaFree(ctx->d_hb);
+  cudaFree(ctx->d_hx);
   cudaFree(ctx->d_row_begin);
   cudaFree(ctx->d_chunks);
   cudaFree(ctx->d_chunk_off);
@@ -640,22 +644,18 @@ int gmres_solve(gmres_ctx* ctx, const double* b, const double* x0, double* x_out
                 int32_t history_cap, int32_t* history_len) {
   if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
   if (!b || !x_out) return fail(ctx, GMRES_EINVAL, "b/x_out is NULL");
-  double *d_b = nullptr, *d_x = nullptr;
   const size_t bytes = sizeof(double) * ctx->n;
-  CK(cudaMallocAsync(&d_b, bytes, ctx->stream));
-  CK(cudaMallocAsync(&d_x, bytes, ctx->stream));
-  CK(cudaMemcpyAsync(d_b, b, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  if (x0) CK(cudaMemcpyAsync(d_x, x0, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  int rc = gmres_solve_device(ctx, d_b, x0 ? d_x : nullptr, d_x, m, tol, ortho, precision, opts, res, history,
-                              history_cap, history_len, nullptr);
+  if (!ctx->d_hb) CK(cudaMalloc(&ctx->d_hb, bytes));
+  if (!ctx->d_hx) CK(cudaMalloc(&ctx->d_hx, bytes));
+  CK(cudaMemcpyAsync(ctx->d_hb, b, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (x0) CK(cudaMemcpyAsync(ctx->d_hx, x0, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = gmres_solve_device(ctx, ctx->d_hb, x0 ? ctx->d_hx : nullptr, ctx->d_hx, m, tol, ortho, precision, opts, res,
+                              history, history_cap, history_len, nullptr);
   if (rc >= 0) {
-    cudaError_t e = cudaMemcpyAsync(x_out, d_x, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaError_t e = cudaMemcpyAsync(x_out, ctx->d_hx, bytes, cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) rc = fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
   }
-  cudaFreeAsync(d_b, ctx->stream);
-  cudaFreeAsync(d_x, ctx->stream);
-  cudaStreamSynchronize(ctx->stream);
   return rc;
 }
 

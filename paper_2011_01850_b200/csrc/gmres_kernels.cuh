@@ -30,14 +30,14 @@ constexpr int NT = 512;        // threads per CTA (16 warps)
 constexpr int NW = NT / 32;
 constexpr int ROWALIGN = 32;   // row-partition granularity (128 B of fp32)
 constexpr int LDALIGN = 64;    // leading dimension of V (256 B of fp32)
-constexpr int NGRP = 4;          // CSR-stream warp groups per CTA (independent pipelines)
-constexpr int GT = NT / NGRP;    // threads per group (4 warps)
-constexpr int CHUNK_CAP = 1024;  // max nnz of a TMA-staged CSR chunk
+constexpr int NGRP = NW;         // CSR-stream pipelines per CTA: one per warp
+constexpr int GT = NT / NGRP;    // threads per pipeline (one warp)
+constexpr int CHUNK_CAP = 256;   // max nnz of a TMA-staged CSR chunk
 constexpr int CHUNK_RMAX = GT;   // max rows of a CSR chunk (multiple of 4)
-constexpr int ST_OFF_CI = 544;                             // stage layout (bytes): row_ptr slice
-constexpr int ST_OFF_A = ST_OFF_CI + (CHUNK_CAP + 8) * 4;  // 4672: col slice, then values
-constexpr int STAGE_BYTES = ST_OFF_A + (CHUNK_CAP + 8) * 8;  // 12928
-constexpr int TILE_BYTES = NGRP * 2 * STAGE_BYTES;         // 103424: 2 stages per group
+constexpr int ST_OFF_CI = 160;                             // stage layout (bytes): row_ptr slice
+constexpr int ST_OFF_A = ST_OFF_CI + (CHUNK_CAP + 8) * 4;  // 1216: col slice, then values
+constexpr int STAGE_BYTES = ST_OFF_A + (CHUNK_CAP + 8) * 8;  // 3328
+constexpr int TILE_BYTES = NGRP * 2 * STAGE_BYTES;         // 106496: 2 stages per warp
 constexpr int MAX_M = 256;                               // restart length limit (shared-memory bound)
 constexpr int ARR_PAD = 8;   // elements of slack after rp/col/val (TMA rounds up to 16 B)
 
@@ -180,9 +180,7 @@ __device__ __forceinline__ void stage_wait(const Dev& d, Shm& sh, int grp, int s
   }
 }
 
-__device__ __forceinline__ void group_sync(int grp) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(GT) : "memory");
-}
+__device__ __forceinline__ void group_sync(int) { __syncwarp(); }
 
 __device__ __forceinline__ void init_shm(Shm& sh) {
   if (threadIdx.x == 0) {
@@ -325,12 +323,12 @@ __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const doub
 
 // ---------------------------------------------------- CSR stream (a1, a2)
 // The CTA's rows are cut (on the host) into chunks of ≤ CHUNK_RMAX rows and
-// ≤ CHUNK_CAP non-zeros whose boundaries are multiples of 4 rows.  The CTA
-// runs NGRP independent warp groups; group g takes chunks g, g+NGRP, ... and
-// owns a 2-stage ring: its leader stages chunk i+2's row_ptr/col/val slices
-// into shared memory with three TMA bulk copies (cp.async.bulk, mbarrier)
-// while the group computes chunk i.  Groups drift out of phase, so one
-// group's gathers overlap another's TMA wait.  L lanes per row (L = 1: one
+// ≤ CHUNK_CAP non-zeros whose boundaries are multiples of 4 rows.  Every warp
+// of the CTA is an independent pipeline: warp g takes chunks g, g+NGRP, ...
+// and owns a 2-stage ring; its lane 0 stages chunk i+2's row_ptr/col/val
+// slices into shared memory with three TMA bulk copies (cp.async.bulk,
+// mbarrier) while the warp computes chunk i.  Warps drift out of phase, so
+// one warp's gathers overlap another's TMA wait (no CTA-wide barrier).  L lanes per row (L = 1: one
 // thread per row, the oracle's summation order); gathers from global (L1/L2).
 // Chunks whose 4 rows exceed CHUNK_CAP are "direct": a warp per row from
 // global memory.  pre(row) is called by the epilogue lane before the row's
@@ -361,7 +359,8 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
     const unsigned b_rp = (unsigned)(((f.x - e.x + 1) + 3) & ~3) * 4u;
     const unsigned b_ci = (unsigned)(eb - ea) * 4u;
     const unsigned b_a = (unsigned)(eb - ea) * (unsigned)sizeof(AT);
-    fence_proxy_async();
+    // (no proxy fence: the TMA reads never-written global data and overwrites
+    // a stage the warp finished reading before the __syncwarp)
     mbar_expect_tx(&sh.mbar[grp][s], b_rp + b_ci + b_a);
     tma_load_1d(st, d.rp + e.x, b_rp, &sh.mbar[grp][s]);
     if (b_ci) {
@@ -386,13 +385,30 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
       const int* sci = reinterpret_cast<const int*>(st + ST_OFF_CI);
       const AT* sa = reinterpret_cast<const AT*>(st + ST_OFF_A);
       const int ea = e.y & ~3;
+      // a lane's elements p0+lane, p0+lane+L, ... in batches of GB: all GB
+      // gathers are issued before the (in-order) accumulation
+      constexpr int GB = 8;
+      auto row_dot = [&](int p0, int p1, int lane) -> AT {
+        AT acc = (AT)0;
+        for (int pb = p0 + lane; pb < p1; pb += GB * L) {
+          AT g[GB], a[GB];
+#pragma unroll
+          for (int u = 0; u < GB; ++u) {
+            const int p = pb + u * L;
+            const bool ok = p < p1;
+            g[u] = ok ? gat(sci[p]) : (AT)0;
+            a[u] = ok ? sa[p] : (AT)0;
+          }
+#pragma unroll
+          for (int u = 0; u < GB; ++u)
+            if (pb + u * L < p1) acc = Ops::add(acc, Ops::mul(a[u], g[u]));
+        }
+        return acc;
+      };
       if (L == 1) {
         for (int lr = gt; lr < nrow; lr += GT) {
           const PT pv = pre(rb + lr);
-          const int p0 = srp[lr] - ea, p1 = srp[lr + 1] - ea;
-          AT acc = (AT)0;
-#pragma unroll 4
-          for (int p = p0; p < p1; ++p) acc = Ops::add(acc, Ops::mul(sa[p], gat(sci[p])));
+          const AT acc = row_dot(srp[lr] - ea, srp[lr + 1] - ea, 0);
           epi(rb + lr, acc, pv);
         }
       } else {
@@ -403,10 +419,7 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
           PT pv{};
           if (act && lane == 0) pv = pre(rb + lr);
           AT acc = (AT)0;
-          if (act) {
-            const int p0 = srp[lr] - ea, p1 = srp[lr + 1] - ea;
-            for (int p = p0 + lane; p < p1; p += L) acc = Ops::add(acc, Ops::mul(sa[p], gat(sci[p])));
-          }
+          if (act) acc = row_dot(srp[lr] - ea, srp[lr + 1] - ea, lane);
 #pragma unroll
           for (int o = L / 2; o > 0; o >>= 1) acc = Ops::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
           if (act && lane == 0) epi(rb + lr, acc, pv);
@@ -546,7 +559,7 @@ __device__ __noinline__ double rowtile_pass_impl(int n, double* __restrict__ xg,
                                                  double* s_acc, typename VecT<W>::T* s_wt) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
-  constexpr int HALF = NT / 2;  // vectors per dot work item
+  constexpr int HALF = NT / 2;  // vectors per dot work item (ITEMS == 2)
   double nn = 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q0 = r0 / N, q1 = r1 / N;
@@ -604,25 +617,25 @@ __device__ __noinline__ double rowtile_pass_impl(int n, double* __restrict__ xg,
       // item it owned by warp it % NW in every tile (fixed accumulation order)
       s_wt[threadIdx.x] = wv;
       __syncthreads();
-      for (int it = warp; it < 2 * ncols; it += NW) {
-        const int col = it >> 1, h0 = (it & 1) * HALF;
-        const V4* vc = reinterpret_cast<const V4*>(V + (long long)col * ldv) + qb + h0;
-        const int lim = min(HALF, q1 - (qb + h0));
-        double p = 0.0;
+        for (int it = warp; it < 2 * ncols; it += NW) {
+          const int col = it >> 1, h0 = (it & 1) * HALF;
+          const V4* vc = reinterpret_cast<const V4*>(V + (long long)col * ldv) + qb + h0;
+          const int lim = min(HALF, q1 - (qb + h0));
+          double p = 0.0;
 #pragma unroll 8
-        for (int k = lane; k < HALF; k += 32) {
-          if (k < lim) {
-            const V4 v = __ldcg(vc + k);
-            const V4 ww = s_wt[h0 + k];
-            const W* pv = reinterpret_cast<const W*>(&v);
-            const W* pq = reinterpret_cast<const W*>(&ww);
+          for (int k = lane; k < HALF; k += 32) {
+            if (k < lim) {
+              const V4 v = __ldcg(vc + k);
+              const V4 ww = s_wt[h0 + k];
+              const W* pv = reinterpret_cast<const W*>(&v);
+              const W* pq = reinterpret_cast<const W*>(&ww);
 #pragma unroll
-            for (int t = 0; t < N; ++t) p += (double)pv[t] * (double)pq[t];
+              for (int t = 0; t < N; ++t) p += (double)pv[t] * (double)pq[t];
+            }
           }
+          p = warp_sum(p);
+          if (lane == 0) s_acc[it] += p;
         }
-        p = warp_sum(p);
-        if (lane == 0) s_acc[it] += p;
-      }
       __syncthreads();
     }
   }
@@ -637,8 +650,8 @@ __device__ __forceinline__ void rowtile_pass(const Dev& d, int r0, int r1, const
                                    reinterpret_cast<typename VecT<W>::T*>(s_tiles));
 }
 
-// (column, half) accumulators → per-CTA column partials, fixed order
-__device__ __forceinline__ void combine_acc(const double* s_acc, int ncols, double* s_part) {
+// (column, half-tile) accumulators → per-CTA column partials, fixed order
+__device__ __forceinline__ void combine_acc(const Dev& d, const double* s_acc, int ncols, double* s_part) {
   __syncthreads();
   for (int i = threadIdx.x; i < ncols; i += NT) s_part[i] = s_acc[2 * i] + s_acc[2 * i + 1];
   __syncthreads();
@@ -870,7 +883,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
     }
   };
   rowtile_pass<W, 1>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
-  combine_acc(s_tmp, j, s_part);
+  combine_acc(d, s_tmp, j, s_part);
   sub(0);
   if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return false;
   sub(1);
@@ -880,7 +893,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   }
   __syncthreads();
   rowtile_pass<W, 2>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
-  combine_acc(s_tmp, j, s_part);
+  combine_acc(d, s_tmp, j, s_part);
   sub(2);
   if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return false;
   sub(3);
@@ -1112,6 +1125,16 @@ __global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int ite
     } else if (what == 2) {
       acc += mgs_sweep<W>(r0, r1, w, V, (W)1e-3, V + ldv);
       __syncthreads();
+    } else if (what == 6) {  // CSR stream without gathers (TMA streaming + epilogue)
+      const W* dinv = (const W*)d.dinvW;
+      auto gat = [&](int) -> W { return (W)1; };
+      auto pre = [&](int row) -> W { return __ldg(dinv + row); };
+      auto epi = [&](int row, W a, W di) { w[row] = mulw(di, a); };
+      csr_stream<W, 1>(d, sh, s_tiles, (const W*)d.aW, gat, pre, epi);
+    } else if (what == 7) {  // full SpMV phase (gathers from V column 0), L = 1
+      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, nullptr);
+    } else if (what == 8) {  // ... plus the fused V-column write (as in the solve)
+      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, const_cast<W*>(V) + 2 * ldv);
     } else if (what == 3) {
       rowtile_pass<W, 1>(d, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
       __syncthreads();

@@ -198,11 +198,16 @@ class Solver:
                            inner=inner, phase_ns=ph)
 
     def solve(self, b, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None, max_cycles=None,
-              record_inner=False, lanes=0, ctas_per_sm=0) -> SolveResult:
-        """gmres_solve: host arrays in, host x out (h2d/d2h inside the call)."""
+              record_inner=False, lanes=0, ctas_per_sm=0, out=None) -> SolveResult:
+        """gmres_solve: host arrays in, host x out (h2d/d2h inside the call).  `out` may be a
+        preallocated (e.g. pinned) float64 array of length n."""
         b = np.ascontiguousarray(b, np.float64)
         x0c = None if x0 is None else np.ascontiguousarray(x0, np.float64)
-        x = np.zeros(self.n)
+        if out is not None:
+            assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == self.n
+            x = out
+        else:
+            x = np.zeros(self.n)
         mc = 10000 if not max_cycles else int(max_cycles)
         hist = np.zeros(mc + 2)
         hl = ctypes.c_int32()

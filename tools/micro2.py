@@ -14,6 +14,12 @@ for prec, wb, dt in ((G.MIXED, 4, torch.float32), (G.FP64, 8, torch.float64)):
     ns = S.k_micro(prec, 0 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} grid barrier      {ns/it/1e3:7.2f} us")
     ns = S.k_micro(prec, 1 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} allreduce(1)      {ns/it/1e3:7.2f} us")
     ns = S.k_micro(prec, 2 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} mgs sweep         {ns/it/1e3:7.2f} us  {3*wb*n/(ns/it):7.0f} GB/s (3 vectors)")
+    it = 50
+    nnz = P.A.nnz
+    ns = S.k_micro(prec, 6 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} csr stream (no gather) {ns/it/1e3:7.2f} us  {((wb+4)*nnz+4*n+2*wb*n)/(ns/it):7.0f} GB/s")
+    ns = S.k_micro(prec, 7 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} spmv phase (L=1)     {ns/it/1e3:7.2f} us  {((wb+4)*nnz+4*n+3*wb*n)/(ns/it):7.0f} GB/s")
+    ns = S.k_micro(prec, 8 | (TUNE << 8), it, 1, V, ld, w); print(f"prec={prec} spmv phase + vcol    {ns/it/1e3:7.2f} us  {((wb+4)*nnz+4*n+4*wb*n)/(ns/it):7.0f} GB/s")
+    if os.environ.get("ONLY_SPMV"): continue
     for nc in (1, 10, 25, 50):
         for mode in (3, 4, 5):
             ns = S.k_micro(prec, mode, 20, nc, V, ld, w)
