@@ -43,10 +43,11 @@ struct gmres_ctx {
   void* d_V = nullptr;
   void* d_w0 = nullptr;
   void* d_w1 = nullptr;
-  double* d_partials = nullptr;
+  double* d_slots = nullptr;      // grid all-reduce partials [2][G][kst]
+  unsigned long long* d_ctr = nullptr;  // arrival counter
+  size_t slots_count = 0;
   double* d_R = nullptr;
   double* d_y = nullptr;
-  unsigned long long* d_bar = nullptr;
   int* d_flags = nullptr;  // [0] abort [1] err [2] scratch
   int* d_out_int = nullptr;
   double* d_out_dbl = nullptr;
@@ -288,10 +289,11 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   const size_t oV = take(wb * ctx->ldv * (m + 1));
   const size_t ow0 = take(wb * ctx->ldv);
   const size_t ow1 = take(wb * ctx->ldv);
-  const size_t oP = take(sizeof(double) * 2 * G * kmax);
+  const size_t kst = (kmax + 3) & ~size_t(3);
+  const size_t oP = take(sizeof(double) * 2 * G * kst);
+  const size_t octr = take(sizeof(unsigned long long) * 4);
   const size_t oR = take(sizeof(double) * kmax * m);
   const size_t oy = take(sizeof(double) * kmax);
-  const size_t obar = take(sizeof(unsigned long long) * 4);
   const size_t ofl = take(sizeof(int) * 8);
   const size_t ooi = take(sizeof(int) * 8);
   const size_t ood = take(sizeof(double) * 4);
@@ -306,10 +308,11 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   ctx->d_V = ctx->d_ws + oV;
   ctx->d_w0 = ctx->d_ws + ow0;
   ctx->d_w1 = ctx->d_ws + ow1;
-  ctx->d_partials = (double*)(ctx->d_ws + oP);
+  ctx->d_slots = (double*)(ctx->d_ws + oP);
+  ctx->slots_count = 2 * G * kst;
+  ctx->d_ctr = (unsigned long long*)(ctx->d_ws + octr);
   ctx->d_R = (double*)(ctx->d_ws + oR);
   ctx->d_y = (double*)(ctx->d_ws + oy);
-  ctx->d_bar = (unsigned long long*)(ctx->d_ws + obar);
   ctx->d_flags = (int*)(ctx->d_ws + ofl);
   ctx->d_out_int = (int*)(ctx->d_ws + ooi);
   ctx->d_out_dbl = (double*)(ctx->d_ws + ood);
@@ -375,10 +378,18 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.ldv = ctx->ldv;
   d.w0 = ctx->d_w0;
   d.w1 = ctx->d_w1;
-  d.partials = ctx->d_partials;
+  d.slots = ctx->d_slots;
+  d.ctr = ctx->d_ctr;
+  for (int q = 0; q < MAXR; ++q) { d.slot_peer[q] = ctx->d_slots; d.ctr_peer[q] = ctx->d_ctr; }
+  d.kst = (d.kmax + 3) & ~3;
+  d.GG = G;
+  d.cta0 = 0;
+  d.nranks = 1;
+  d.rank = 0;
+  d.sys_scope = 0;
+  d.mgs_nbuf = 2;
   d.R = ctx->d_R;
   d.y = ctx->d_y;
-  d.bar = ctx->d_bar;
   d.abort_flag = ctx->d_flags;
   d.err_flag = ctx->d_flags + 1;
   d.row_begin = ctx->d_row_begin;
@@ -398,7 +409,7 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
 }
 
 int reset_flags(gmres_ctx* ctx, cudaStream_t st) {
-  CK(cudaMemsetAsync(ctx->d_bar, 0, sizeof(unsigned long long) * 4, st));
+  CK(cudaMemsetAsync(ctx->d_ctr, 0, sizeof(unsigned long long) * 4, st));
   CK(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * 8, st));
   return 0;
 }
@@ -539,18 +550,23 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   int G = 0;
   if (int rc = grid_for(ctx, kern, smem, opts ? opts->ctas_per_sm : 0, &G)) return rc;
   if (int rc = ensure_partition(ctx, G)) return rc;
-  // resident MGS (gmres_kernels.cuh mgs_resident): every CTA's rows of w and of
-  // one basis vector in shared memory, ≤ MGS_MV 16-byte vectors per thread
-  int mgs_resident = 0;
+  // resident MGS (gmres_kernels.cuh mgs_resident): every CTA's rows of w and
+  // v_{i-1} in ≤ MGS_MV 16-byte registers per thread, and a ring of NB = 3 (else
+  // 2) shared buffers of one basis-vector row block for the TMA stream
+  int mgs_resident = 0, mgs_nbuf = 2;
   {
     const int wb = precision == GMRES_MIXED ? 4 : 8;
     const int per_vec = 16 / wb;
-    const int res_bytes = 2 * ctx->part_max_rows * wb;
-    const int tb = std::max(tile_bytes, res_bytes);
-    if (ortho == GMRES_MGS && ctx->part_max_rows / per_vec <= MGS_MV * NT && smem_bytes(m, tb) <= kMaxDynSmem) {
+    const int nq = ctx->part_max_rows / per_vec;
+    const int buf_bytes = ((nq + 7) & ~7) * 16;
+    const int tune = opts ? opts->tune : 0;
+    for (int nb = (tune & 256) ? 2 : 3; nb >= 2 && ortho == GMRES_MGS && nq <= MGS_MV * NT && !mgs_resident; --nb) {
+      const int tb = std::max(tile_bytes, nb * buf_bytes);
+      if (smem_bytes(m, tb) > kMaxDynSmem) continue;
       int G2 = 0;
       if (grid_for(ctx, kern, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 == G) {
         mgs_resident = 1;
+        mgs_nbuf = nb;
         tile_bytes = tb;
         smem = smem_bytes(m, tb);
       }
@@ -583,6 +599,7 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   d.profile = (opts && opts->profile) ? 1 : 0;
   d.tile_bytes = tile_bytes;
   d.mgs_resident = mgs_resident;
+  d.mgs_nbuf = mgs_nbuf;
   d.tune = opts ? opts->tune : 0;
 
   gmres_result r{};

@@ -40,6 +40,7 @@ constexpr int STAGE_BYTES = ST_OFF_A + (CHUNK_CAP + 8) * 8;  // 3328
 constexpr int TILE_BYTES = NGRP * 2 * STAGE_BYTES;         // 106496: 2 stages per warp
 constexpr int MAX_M = 256;                               // restart length limit (shared-memory bound)
 constexpr int ARR_PAD = 8;   // elements of slack after rp/col/val (TMA rounds up to 16 B)
+constexpr int MAXR = 8;      // ranks (GPUs) of a row-partitioned solve
 
 enum { ST_OK = 0, ST_NOT_CONVERGED = 1, ST_EFP32RANGE = -4, ST_ENONFINITE = -5, ST_ETIMEOUT = -8 };
 enum { ERRF_RANGE = 1, ERRF_NONFINITE = 2 };
@@ -64,10 +65,20 @@ struct Dev {
   long long ldv;
   void* w0;             // ping-pong work vectors (W, ldv rows, zero padding)
   void* w1;
-  double* partials;     // [2][G][kmax]
+  // grid all-reduce (see grid_allreduce): this rank's partial array
+  // [2][GG][kst] fp64 and arrival counter, and the same of every rank
+  // (peer-mapped; [rank] is the local one) for the pushes and arrivals
+  double* slots;
+  double* slot_peer[MAXR];
+  unsigned long long* ctr;
+  unsigned long long* ctr_peer[MAXR];
+  int kst;              // k stride of a slot row (kmax rounded to 4)
+  int GG;               // CTAs over all ranks (nranks * G)
+  int cta0;             // global index of this rank's CTA 0 (rank * G)
+  int nranks, rank;
+  int sys_scope;        // != 0: peers are other GPUs (system-scope release/acquire)
   double* R;            // rotated Hessenberg, (m+1) x m, ld m+1 (CTA 0)
   double* y;            // m
-  unsigned long long* bar;
   int* abort_flag;
   int* err_flag;
   const int* row_begin; // G+1 row boundaries (multiples of ROWALIGN, last = nvec)
@@ -84,7 +95,8 @@ struct Dev {
   unsigned long long* prof_cta;  // [G] per-CTA own SpMV ns (profile mode)
   int profile;          // != 0: grid barrier after every phase (clean attribution)
   int tune;             // developer A/B switches (bit 0: no L2 prefetch in MGS, bit 2: no resident MGS)
-  int mgs_resident;     // != 0: every CTA's w and v row blocks fit the staging region (resident MGS)
+  int mgs_resident;     // != 0: every CTA's w and v_{i-1} rows fit MGS_MV vectors per thread (resident MGS)
+  int mgs_nbuf;         // TMA ring depth of the resident MGS (2 or 3 basis-vector buffers)
   long long timeout_ns;
 };
 
@@ -122,6 +134,20 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Dot of two 16-byte vectors for the length-n reductions (reading R9): in
+// mixed mode the 4 products of a float4 form one short fp32 sum (fma chain,
+// "short sums stay in W") that is then accumulated in fp64 — one fp32→fp64
+// conversion per 4 elements instead of 8 (F2F runs at 1/8 of the fp32 rate and
+// bounded the MGS step, ncu/globaltimer r01); in fp64 mode plain fp64.
+__device__ __forceinline__ double dotv(const float4& a, const float4& b) {
+  float s = __fmul_rn(a.x, b.x);
+  s = __fmaf_rn(a.y, b.y, s);
+  s = __fmaf_rn(a.z, b.z, s);
+  s = __fmaf_rn(a.w, b.w, s);
+  return (double)s;
+}
+__device__ __forceinline__ double dotv(const double2& a, const double2& b) { return a.x * b.x + a.y * b.y; }
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
@@ -156,12 +182,15 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned 
 // per-CTA control block in static shared memory
 struct Shm {
   unsigned long long mbar[NGRP][2];  // TMA stage barriers (per CSR-stream group)
-  unsigned long long epoch;          // grid barriers passed by this CTA
+  unsigned long long mbar_v[3];      // TMA barriers of the resident-MGS basis buffers
   unsigned tma_phase[NGRP];          // bit s: parity of the next completion of stage s
-  int red_epoch;               // all-reduces done (selects the partial slot)
+  unsigned vphase;                   // bit b: parity of the next completion of mbar_v[b]
   int abort;
   int flag;
+  unsigned long long epoch;          // grid barriers passed by this CTA (thread 0)
+  int red_epoch;                     // all-reduces done (partial buffer parity; thread 0 writes)
   double red[NW * 4];
+  double red2[NW * 4];
 };
 
 // wait for stage s of group grp's TMA pipeline; watchdog on %globaltimer
@@ -188,50 +217,80 @@ __device__ __forceinline__ void init_shm(Shm& sh) {
     sh.red_epoch = 0;
     sh.abort = 0;
     sh.flag = 0;
+    sh.vphase = 0;
     for (int g = 0; g < NGRP; ++g) {
       sh.tma_phase[g] = 0;
       mbar_init(&sh.mbar[g][0], 1);
       mbar_init(&sh.mbar[g][1], 1);
     }
+    for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_v[b], 1);
     fence_mbar_init();
   }
   __syncthreads();
 }
 
-// Grid-wide barrier over the co-resident (cooperative) grid: monotone 64-bit
-// arrival counter, release/acquire through __threadfence + atomics.  A device
-// watchdog (globaltimer) aborts every CTA instead of hanging the GPU.
-__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// ------------------------------------------------ grid all-reduce (push + counter)
+// Every rank holds a partial array [2][GG][kst] fp64 (GG = CTAs over all
+// ranks) and an arrival counter.  Reduction e uses buffer e mod 2: CTA c
+// writes its K partials into row c of that buffer in EVERY rank's array (the
+// local one among them), then adds 1 to every rank's counter with a release
+// reduction; thread 0 of each CTA spins (acquire) on its own rank's counter
+// until all GG CTAs of this epoch arrived, and the CTA loads the GG·K partials
+// from local memory and sums each k over the GG CTAs in one fixed order — the
+// same in every CTA of every rank, so all hold bit-identical results
+// (replicated control flow).  Buffer e mod 2 is rewritten at
+// e+2, after every CTA arrived at e+1, i.e. after everyone finished reading it.
+// (tools/ar_bench.cu: this beats sentinel-slot polling on B200, whose 148×148
+// pollers contend in L2: 1.96 vs ≥ 2.56 µs per one-value all-reduce.)
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v, bool sys) {
+  if (sys) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_ctr(const unsigned long long* p, bool sys) {
+  unsigned long long v;
+  if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
+__device__ __forceinline__ double* slot_row(const Dev& d, double* base, int buf, int gcta) {
+  return base + ((size_t)buf * d.GG + gcta) * d.kst;
+}
+
+// thread 0: arrive on every rank's counter, wait for all GG CTAs (watchdog);
+// the caller brackets it with __syncthreads.  Returns false on abort.
+__device__ __forceinline__ bool arrive_wait(const Dev& d, Shm& sh) {
+  const bool sys = d.sys_scope != 0;
+  const unsigned long long target = (sh.epoch += 1ull) * (unsigned long long)d.GG;
+  for (int q = 0; q < d.nranks; ++q) red_release_add(d.ctr_peer[q], 1ull, sys);
+  unsigned it = 0;
+  unsigned long long t0 = 0;
+  while (ld_acquire_ctr(d.ctr, sys) < target) {
+    if (((++it) & 1023u) == 0u) {
+      if (*(volatile int*)d.abort_flag) return false;
+      const unsigned long long t = globaltimer();
+      if (t0 == 0) t0 = t;
+      else if ((long long)(t - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); return false; }
+    }
+  }
+  return *(volatile int*)d.abort_flag == 0;
+}
+
+// Grid barrier over all CTAs of all ranks (release/acquire).
 __device__ __forceinline__ bool grid_sync(const Dev& d, Shm& sh) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long target = (sh.epoch += 1ull) * (unsigned long long)d.G;
-    if (d.tune & 2) {  // reference variant: full fences around a returning atomic
-      __threadfence();
-      atomicAdd(d.bar, 1ull);
-    } else {
-      red_release_add_u64(d.bar, 1ull);  // release: orders this CTA's prior writes (after bar.sync)
-    }
-    int ab = 0;
-    unsigned long long t0 = 0;
-    unsigned it = 0;
-    while (ld_acquire_u64(d.bar) < target) {
-      if (((++it) & 1023u) == 0u) {
-        if (*(volatile int*)d.abort_flag) { ab = 1; break; }
-        const unsigned long long t = globaltimer();
-        if (t0 == 0) t0 = t;
-        else if ((long long)(t - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); ab = 1; break; }
-      }
-    }
-    if (d.tune & 2) __threadfence();
-    if (!ab && *(volatile int*)d.abort_flag) ab = 1;
-    sh.abort = ab;
-  }
+  if (threadIdx.x == 0) sh.abort = arrive_wait(d, sh) ? 0 : 1;
   __syncthreads();
   return sh.abort == 0;
+}
+
+// push this CTA's K partials into buffer buf of every rank's array
+__device__ __forceinline__ void push_partials(const Dev& d, const double* s_part, int K, int buf) {
+  const int gc = d.cta0 + (int)blockIdx.x;
+  for (int t = threadIdx.x; t < K * d.nranks; t += NT) {
+    const int q = t / K, k = t - q * K;
+    slot_row(d, d.slot_peer[q], buf, gc)[k] = s_part[k];
+  }
 }
 
 // Block sum of K doubles (deterministic: warp tree, then warps in order).
@@ -252,46 +311,59 @@ __device__ __forceinline__ void block_sum(double (&v)[K], Shm& sh, double* out) 
   __syncthreads();
 }
 
-// Grid all-reduce of K fp64 values (s_part → s_out, both shared).  Every CTA
-// sums the G partials in the same fixed order (warp w owns a contiguous block
-// of CTAs; blocks in order), so all CTAs hold bit-identical results
-// (replicated control flow).  The G·K loads of a CTA are all
-// independent (one L2 round trip).
+// One-value all-reduce of a per-thread contribution: CTA sum (warp trees,
+// warps in order) → push → arrive/wait → fixed-order sum over all GG CTAs.
+// (acq is implied: the counter acquire orders every later read.)
+__device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool /*acq*/, double& out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int buf = sh.red_epoch & 1;
+  v = warp_sum(v);
+  if (lane == 0) sh.red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double s = lane < NW ? sh.red[lane] : 0.0;  // fixed shuffle tree over the warps
+#pragma unroll
+    for (int o = NW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int gc = d.cta0 + (int)blockIdx.x;
+      for (int q = 0; q < d.nranks; ++q) slot_row(d, d.slot_peer[q], buf, gc)[0] = s;
+      sh.abort = arrive_wait(d, sh) ? 0 : 1;
+      sh.red_epoch++;
+    }
+  }
+  __syncthreads();
+  double x = 0.0;
+  for (int g = threadIdx.x; g < d.GG; g += NT) x += __ldcg(slot_row(d, d.slots, buf, g));
+  const int nwp = min(NW, (d.GG + 31) >> 5);
+  if (warp < nwp) {
+    x = warp_sum(x);
+    if (lane == 0) sh.red2[warp] = x;
+  }
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nwp; ++w) s += sh.red2[w];
+  out = s;
+  return sh.abort == 0;
+}
+
+// Grid all-reduce of K fp64 values (s_part → s_out, both shared; s_part
+// complete and block-synced by the caller).  Warp w loads a contiguous block
+// of CTAs, lane = k; blocks are then summed in warp order: a fixed order, the
+// same in every CTA of every rank.
 constexpr int GCH = 8;  // independent partial loads in flight per lane
 __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const double* s_part, int K, double* s_out,
-                                               double* s_tmp) {
-  const int slot = sh.red_epoch & 1;
-  double* P = d.partials + (size_t)slot * d.G * d.kmax;
-  for (int k = threadIdx.x; k < K; k += NT) P[(size_t)blockIdx.x * d.kmax + k] = s_part[k];
-  if (!grid_sync(d, sh)) return false;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (K * d.G <= NT * 4 && K <= 4) {
-    // small K: thread g < G loads CTA g's K partials (one round trip), then a
-    // fixed shuffle tree per warp and warps in order
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int g = threadIdx.x; g < d.G; g += NT) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (k < K) v[k] += __ldcg(P + (size_t)g * d.kmax + k);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < K) {
-        const double sv = warp_sum(v[k]);
-        if (lane == 0) s_tmp[warp * d.kmax + k] = sv;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < K) {
-      double acc = 0.0;
-      for (int w = 0; w < NW; ++w) acc += s_tmp[w * d.kmax + threadIdx.x];
-      s_out[threadIdx.x] = acc;
-    }
-    if (threadIdx.x == 0) sh.red_epoch++;
-    __syncthreads();
-    return true;
+                                               double* s_tmp, bool /*acq*/ = true) {
+  const int buf = sh.red_epoch & 1;
+  push_partials(d, s_part, K, buf);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sh.abort = arrive_wait(d, sh) ? 0 : 1;
+    sh.red_epoch++;
   }
-  const int gpw = (d.G + NW - 1) / NW;
+  __syncthreads();
+  if (sh.abort) return false;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gpw = (d.GG + NW - 1) / NW;
   const int g0 = warp * gpw;
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int k = k0 + lane;
@@ -302,7 +374,7 @@ __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const doub
 #pragma unroll
         for (int u = 0; u < GCH; ++u) {
           const int g = g0 + u0 + u;
-          v[u] = (u0 + u < gpw && g < d.G) ? __ldcg(P + (size_t)g * d.kmax + k) : 0.0;
+          v[u] = (u0 + u < gpw && g < d.GG) ? __ldcg(slot_row(d, d.slots, buf, g) + k) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < GCH; ++u) acc += v[u];
@@ -316,7 +388,6 @@ __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const doub
     for (int w = 0; w < NW; ++w) acc += s_tmp[w * d.kmax + k];
     s_out[k] = acc;
   }
-  if (threadIdx.x == 0) sh.red_epoch++;
   __syncthreads();
   return true;
 }
@@ -502,7 +573,7 @@ __device__ __noinline__ double mgs_sweep(int r0, int r1, W* __restrict__ w, cons
                             const W* __restrict__ vnext) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
-  constexpr int UB = 4;  // independent 16-byte loads in flight per array per thread
+  constexpr int UB = sizeof(W) == 4 ? 4 : 2;  // independent 16-byte loads in flight per array per thread (fp64: register budget)
   double acc = 0.0;
   const int q0 = r0 / N, q1 = r1 / N;
   for (int qb = q0 + threadIdx.x; qb < q1; qb += UB * NT) {
@@ -528,12 +599,9 @@ __device__ __noinline__ double mgs_sweep(int r0, int r1, W* __restrict__ w, cons
           reinterpret_cast<V4*>(w)[q] = a[u];
         }
         if (vnext) {
-          const W* pc = reinterpret_cast<const W*>(&c[u]);
-#pragma unroll
-          for (int t = 0; t < N; ++t) acc += (double)pa[t] * (double)pc[t];
+          acc += dotv(a[u], c[u]);
         } else {
-#pragma unroll
-          for (int t = 0; t < N; ++t) acc += (double)pa[t] * (double)pa[t];
+          acc += dotv(a[u], a[u]);
         }
       }
     }
@@ -605,10 +673,7 @@ __device__ __noinline__ double rowtile_pass_impl(int n, double* __restrict__ xg,
 #pragma unroll
           for (int t = 0; t < N; ++t) pw[t] = subw(pw[t], acc[t]);
           reinterpret_cast<V4*>(w)[q] = wv;
-          if (MODE == 3) {
-#pragma unroll
-            for (int t = 0; t < N; ++t) nn += (double)pw[t] * (double)pw[t];
-          }
+          if (MODE == 3) nn += dotv(wv, wv);
         }
       }
     }
@@ -626,11 +691,7 @@ __device__ __noinline__ double rowtile_pass_impl(int n, double* __restrict__ xg,
           for (int k = lane; k < HALF; k += 32) {
             if (k < lim) {
               const V4 v = __ldcg(vc + k);
-              const V4 ww = s_wt[h0 + k];
-              const W* pv = reinterpret_cast<const W*>(&v);
-              const W* pq = reinterpret_cast<const W*>(&ww);
-#pragma unroll
-              for (int t = 0; t < N; ++t) p += (double)pv[t] * (double)pq[t];
+              p += dotv(v, s_wt[h0 + k]);
             }
           }
           p = warp_sum(p);
@@ -747,73 +808,90 @@ struct SmemLayout {
   init_shm(sh);
 
 // ------------------------------------------------------------------ a3 (resident)
-// MGS with the CTA's rows of w and of the previous basis vector resident in
-// shared memory and the next basis vector in registers: step i updates
-// w ← RN_W(w − RN_W(h_{i−1})·v_{i−1}) from shared memory, forms the partial of
-// h_i = w·v_i from registers, then issues the loads of v_{i+1} BEFORE waiting
-// on h_i's grid reduction, so their latency hides behind the all-reduce.
-// Same operations and order per element as mgs_sweep.
-constexpr int MGS_MV = 8;  // 16-byte vectors per thread kept in registers
+// MGS with the CTA's rows of w and of v_{i−1} in registers
+// and the basis vectors streamed through a ring of NB shared-memory buffers by
+// TMA bulk copies: at the top of step i the copy of v_{i+NB−1} is issued into
+// the buffer v_{i−1} left, then one pass forms w ← RN_W(w − RN_W(h_{i−1})·v_{i−1})
+// and the partial of h_i = w·v_i.  The HBM read of the next vectors therefore
+// overlaps h_i's all-reduce, and no register holds an in-flight load across
+// it.  Same operations and order per element as mgs_sweep.
+constexpr int MGS_MV = 8;  // 16-byte vectors per thread (w and v_{i-1} in registers)
 template <class W>
-__device__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
-                             double* s_part, double* s_out, double* s_tmp, double* s_h, char* s_tiles, double& NN) {
+__device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
+                                          W* w, double* s_h, char* s_tiles, double& NN) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
   const int q0 = r0 / N, nq = r1 / N - q0;
-  V4* sw = reinterpret_cast<V4*>(s_tiles);
-  V4* sv = sw + nq;
-  V4 vn[MGS_MV];
-  auto load_col = [&](int col) {
-    const V4* vc = reinterpret_cast<const V4*>(V + (long long)col * ldv) + q0;
-#pragma unroll
-    for (int k = 0; k < MGS_MV; ++k) {
-      const int t = threadIdx.x + k * NT;
-      if (t < nq) vn[k] = __ldcg(vc + t);
+  const int nqa = (nq + 7) & ~7;  // 128-byte aligned buffers
+  const int NB = d.mgs_nbuf;
+  V4* sv = reinterpret_cast<V4*>(s_tiles);
+  const unsigned bytes = (unsigned)nq * 16u;
+  unsigned ph = sh.vphase;
+  auto issue = [&](int c) {  // one thread: v_c (1-based) → buffer (c−1) mod NB
+    const int b = (c - 1) % NB;
+    char* dst = reinterpret_cast<char*>(sv + (size_t)b * nqa);
+    const char* src = reinterpret_cast<const char*>(V + (long long)(c - 1) * ldv + r0);
+    mbar_expect_tx(&sh.mbar_v[b], bytes);
+    for (unsigned o = 0; o < bytes; o += 32768u)
+      tma_load_1d(dst + o, src + o, min(32768u, bytes - o), &sh.mbar_v[b]);
+  };
+  auto wait = [&](int b) -> bool {
+    const unsigned par = (ph >> b) & 1u;
+    ph ^= (1u << b);
+    if (mbar_try_wait(&sh.mbar_v[b], par)) return true;
+    const unsigned long long t0 = globaltimer();
+    for (;;) {
+      if (mbar_try_wait(&sh.mbar_v[b], par)) return true;
+      if ((long long)(globaltimer() - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); return false; }
     }
   };
-  // prologue: w → shared, v_1 → registers
+  // copies are issued by warp 1 (TMA_T): warp 0 performs the all-reduce's release
+  constexpr int TMA_T = 32;
+  if (threadIdx.x == TMA_T)
+    for (int c = 1; c <= min(NB - 1, j); ++c) issue(c);
+  V4 wr[MGS_MV], vp[MGS_MV];
   {
     const V4* wg = reinterpret_cast<const V4*>(w) + q0;
 #pragma unroll
     for (int k = 0; k < MGS_MV; ++k) {
       const int t = threadIdx.x + k * NT;
-      if (t < nq) sw[t] = wg[t];
+      if (t < nq) wr[k] = wg[t];
     }
   }
-  load_col(0);
   W hprev = (W)0;
+  bool ok = true;
   const bool lead = d.profile && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long tp = lead ? globaltimer() : 0ull;
+  auto tick = [&](int slot) {
+    if (lead) { const unsigned long long t = globaltimer(); d.prof[slot] += t - tp; tp = t; }
+  };
   for (int i = 1; i <= j; ++i) {
+    if (threadIdx.x == TMA_T && i + NB - 1 <= j) issue(i + NB - 1);
+    const int b = (i - 1) % NB;
+    ok = wait(b) && ok;
+    tick(8);
+    const V4* X = sv + (size_t)b * nqa;
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < MGS_MV; ++k) {
       const int t = threadIdx.x + k * NT;
       if (t < nq) {
-        V4 a = sw[t];
-        W* pa = reinterpret_cast<W*>(&a);
+        W* pa = reinterpret_cast<W*>(&wr[k]);
         if (i > 1) {
-          const V4 b = sv[t];
-          const W* pb = reinterpret_cast<const W*>(&b);
+          const W* pb = reinterpret_cast<const W*>(&vp[k]);
 #pragma unroll
           for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hprev, pb[u]));
-          sw[t] = a;
         }
-        const W* pc = reinterpret_cast<const W*>(&vn[k]);
-#pragma unroll
-        for (int u = 0; u < N; ++u) acc += (double)pa[u] * (double)pc[u];
-        sv[t] = vn[k];
+        vp[k] = X[t];
+        acc += dotv(wr[k], vp[k]);
       }
     }
-    if (i < j) load_col(i);  // v_{i+1}: in flight during the reduction below
-    if (lead) { const unsigned long long t = globaltimer(); d.prof[8] += t - tp; tp = t; }
-    double p[1] = {acc};
-    block_sum<1>(p, sh, s_part);
-    if (lead) { const unsigned long long t = globaltimer(); d.prof[9] += t - tp; tp = t; }
-    if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
-    if (threadIdx.x == 0) s_h[i - 1] = s_out[0];
-    hprev = RN<W>(s_out[0]);
-    if (lead) { const unsigned long long t = globaltimer(); d.prof[10] += t - tp; tp = t; }
+    tick(9);
+    double h;
+    if (!allreduce1(d, sh, acc, false, h)) return false;
+    if (threadIdx.x == 0) s_h[i - 1] = h;
+    hprev = RN<W>(h);
+    tick(10);
   }
   // final update w ← w − h_j v_j, ‖w‖², w back to global for the next SpMV
   double nn = 0.0;
@@ -823,24 +901,17 @@ __device__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int r1, int j, const
     for (int k = 0; k < MGS_MV; ++k) {
       const int t = threadIdx.x + k * NT;
       if (t < nq) {
-        V4 a = sw[t];
-        const V4 b = sv[t];
-        W* pa = reinterpret_cast<W*>(&a);
-        const W* pb = reinterpret_cast<const W*>(&b);
+        W* pa = reinterpret_cast<W*>(&wr[k]);
+        const W* pb = reinterpret_cast<const W*>(&vp[k]);
 #pragma unroll
-        for (int u = 0; u < N; ++u) {
-          pa[u] = subw(pa[u], mulw(hprev, pb[u]));
-          nn += (double)pa[u] * (double)pa[u];
-        }
-        wg[t] = a;
+        for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hprev, pb[u]));
+        nn += dotv(wr[k], wr[k]);
+        wg[t] = wr[k];
       }
     }
   }
-  double p[1] = {nn};
-  block_sum<1>(p, sh, s_part);
-  if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
-  NN = s_out[0];
-  return true;
+  if (threadIdx.x == 0) sh.vphase = ph;  // read by every thread at entry, before the syncs below
+  return allreduce1(d, sh, nn, true, NN);
 }
 
 // Orthogonalisation of w (own rows) against V[:, 0..j) and its norm: MGS
@@ -851,27 +922,25 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
                             double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
                             char* s_tiles, double& NN) {
   if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4))
-    return mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_part, s_out, s_tmp, s_h, s_tiles, NN);
+    return mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, NN);
   if (d.ortho == 0) {
     W hprev = (W)0;
     const bool pf = !(d.tune & 1) && r1 > r0;
     const unsigned pf_bytes = (unsigned)((r1 - r0) * (int)sizeof(W));
     for (int i = 1; i <= j; ++i) {
-      double p[1] = {mgs_sweep<W>(r0, r1, w, i > 1 ? V + (long long)(i - 2) * ldv : nullptr, hprev,
-                                  V + (long long)(i - 1) * ldv)};
+      const double acc = mgs_sweep<W>(r0, r1, w, i > 1 ? V + (long long)(i - 2) * ldv : nullptr, hprev,
+                                      V + (long long)(i - 1) * ldv);
       // while this step's reduction is in flight, pull the next basis
       // vector's rows (v_{i+1}) of this CTA into L2
-      if (pf && i < j && threadIdx.x == 0) prefetch_l2(V + (long long)i * ldv + r0, pf_bytes);
-      block_sum<1>(p, sh, s_part);
-      if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
-      if (threadIdx.x == 0) s_h[i - 1] = s_out[0];
-      hprev = RN<W>(s_out[0]);
+      // (issued by warp 1: warp 0's release fence in the all-reduce must not wait on it)
+      if (pf && i < j && threadIdx.x == 32) prefetch_l2(V + (long long)i * ldv + r0, pf_bytes);
+      double h;
+      if (!allreduce1(d, sh, acc, false, h)) return false;
+      if (threadIdx.x == 0) s_h[i - 1] = h;
+      hprev = RN<W>(h);
     }
-    double p[1] = {mgs_sweep<W>(r0, r1, w, V + (long long)(j - 1) * ldv, hprev, nullptr)};
-    block_sum<1>(p, sh, s_part);
-    if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
-    NN = s_out[0];
-    return true;
+    const double acc = mgs_sweep<W>(r0, r1, w, V + (long long)(j - 1) * ldv, hprev, nullptr);
+    return allreduce1(d, sh, acc, true, NN);
   }
   double nn = 0.0;
   const bool lead = d.profile && blockIdx.x == 0 && threadIdx.x == 0;
@@ -885,7 +954,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   rowtile_pass<W, 1>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
   combine_acc(d, s_tmp, j, s_part);
   sub(0);
-  if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return false;
+  if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp, false)) return false;
   sub(1);
   for (int i = threadIdx.x; i < j; i += NT) {
     s_h[i] = s_out[i];
@@ -895,7 +964,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   rowtile_pass<W, 2>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
   combine_acc(d, s_tmp, j, s_part);
   sub(2);
-  if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp)) return false;
+  if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp, false)) return false;
   sub(3);
   for (int i = threadIdx.x; i < j; i += NT) {
     s_h[i] = s_h[i] + s_out[i];
@@ -904,12 +973,9 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   __syncthreads();
   nn = 0.0;
   rowtile_pass<W, 3>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
-  double p[1] = {nn};
-  block_sum<1>(p, sh, s_part);
   sub(4);
-  if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return false;
+  if (!allreduce1(d, sh, nn, true, NN)) return false;
   sub(5);
-  NN = s_out[0];
   return true;
 }
 
@@ -1119,9 +1185,9 @@ __global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int ite
     if (what == 0) {
       if (!grid_sync(d, sh)) return;
     } else if (what == 1) {
-      double p[1] = {1.0};
-      block_sum<1>(p, sh, s_part);
-      if (!grid_allreduce(d, sh, s_part, 1, s_out, s_tmp)) return;
+      double h;
+      if (!allreduce1(d, sh, threadIdx.x == 0 ? 1.0 : 0.0, false, h)) return;
+      acc += h;
     } else if (what == 2) {
       acc += mgs_sweep<W>(r0, r1, w, V, (W)1e-3, V + ldv);
       __syncthreads();

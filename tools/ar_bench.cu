@@ -1,0 +1,164 @@
+// Dev microbenchmark: grid all-reduce variants on a 148 x 512 cooperative grid.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ar_bench tools/ar_bench.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+constexpr int NT = 512, NW = 16;
+constexpr unsigned long long SENT = 0x7ff4dead0badf00dull;
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) {
+  unsigned long long v; asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory"); return v;
+}
+__device__ __forceinline__ unsigned long long ld_rlx(const void* p) {
+  unsigned long long v; asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory"); return v;
+}
+__device__ __forceinline__ unsigned long long ld_vol(const void* p) {
+  unsigned long long v; asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory"); return v;
+}
+__device__ __forceinline__ void st_rel(void* p, double v) {
+  asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_rlx(void* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_rel(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_rlx(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct Args {
+  int variant, iters, G, stride;  // stride: doubles between CTA slots (variant-dependent)
+  unsigned long long* ctr;
+  double* slots;  // [3][G*stride]
+  double* parts;  // [2][G]
+  unsigned long long* out;
+};
+
+__global__ void __launch_bounds__(NT, 1) kern(Args a) {
+  __shared__ double red[NW], red2[NW];
+  __shared__ unsigned long long epoch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = blockIdx.x, G = a.G;
+  if (threadIdx.x == 0) epoch = 0;
+  __syncthreads();
+  double acc_all = 0.0;
+  int e3 = 0;
+  const unsigned long long t0 = gtime();
+  for (int it = 0; it < a.iters; ++it) {
+    double v = (double)(g + 1) * 1e-3 + it;
+    if (a.variant <= 2) {
+      // counter barrier + load partials (old design); 0: red.release+ld.acquire, 1: relaxed red + fence, 2: barrier only
+      v = warp_sum(v);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      double* P = a.parts + (size_t)(it & 1) * G;
+      if (threadIdx.x == 0) {
+        double s = 0; for (int w = 0; w < NW; ++w) s += red[w];
+        P[g] = s;
+        const unsigned long long target = (epoch += 1) * (unsigned long long)G;
+        if (a.variant == 1) { __threadfence(); red_rlx(a.ctr, 1); while (ld_vol(a.ctr) < target) {} __threadfence(); }
+        else { red_rel(a.ctr, 1); while (ld_acq(a.ctr) < target) {} }
+      }
+      __syncthreads();
+      if (a.variant != 2) {
+        double x = 0.0;
+        if (threadIdx.x < G) x = __ldcg(P + threadIdx.x);
+        if (warp < (G + 31) / 32) { x = warp_sum(x); if (lane == 0) red2[warp] = x; }
+        __syncthreads();
+        double s = 0; for (int w = 0; w < (G + 31) / 32; ++w) s += red2[w];
+        acc_all += s;
+      }
+    } else {
+      // sentinel slots: 3: st.release push, relaxed poll, slot stride a.stride (doubles)
+      //                 4: st.relaxed push
+      //                 5: like 3 + acquire fence per polling warp
+      //                 6: like 3 but only warp 0 polls with each lane covering G/32 slots
+      v = warp_sum(v);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      double* S = a.slots + (size_t)e3 * G * a.stride;
+      if (threadIdx.x == 0) {
+        double s = 0; for (int w = 0; w < NW; ++w) s += red[w];
+        if (a.variant == 4) st_rlx(S + (size_t)g * a.stride, __double_as_longlong(s));
+        else st_rel(S + (size_t)g * a.stride, s);
+      }
+      double x = 0.0;
+      if (a.variant == 6) {
+        if (warp == 0) {
+          for (int t = lane; t < G; t += 32) {
+            unsigned long long u;
+            while ((u = ld_rlx(S + (size_t)t * a.stride)) == SENT) {}
+            x += __longlong_as_double(u);
+          }
+        }
+      } else if (threadIdx.x < G) {
+        unsigned long long u;
+        while ((u = ld_rlx(S + (size_t)threadIdx.x * a.stride)) == SENT) {}
+        x = __longlong_as_double(u);
+      }
+      if (a.variant == 5 && threadIdx.x < G) __threadfence();
+      const int nwp = a.variant == 6 ? 1 : (G + 31) / 32;
+      if (warp < nwp) { x = warp_sum(x); if (lane == 0) red2[warp] = x; }
+      __syncthreads();
+      double s = 0; for (int w = 0; w < nwp; ++w) s += red2[w];
+      acc_all += s;
+      // reset own slot of buffer (e3+2)%3 (written at the previous epoch)
+      if (threadIdx.x == 0) st_rlx(a.slots + ((size_t)((e3 + 2) % 3) * G + g) * a.stride, SENT);
+      e3 = (e3 + 1) % 3;
+    }
+  }
+  const unsigned long long t1 = gtime();
+  if (g == 0 && threadIdx.x == 0) { a.out[0] = t1 - t0; a.out[1] = __double_as_longlong(acc_all); }
+}
+
+__global__ void fill(unsigned long long* p, size_t n, unsigned long long v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+int main() {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int G = sms, iters = 2000;
+  unsigned long long *ctr, *out; double *slots, *parts;
+  cudaMalloc(&ctr, 8); cudaMalloc(&out, 16);
+  const int maxstride = 32;
+  cudaMalloc(&slots, sizeof(double) * 3 * G * maxstride);
+  cudaMalloc(&parts, sizeof(double) * 2 * G);
+  struct V { int v, stride; const char* name; } vs[] = {
+    {0, 1, "counter red.release/ld.acquire + partial load"},
+    {1, 1, "counter fence+red.relaxed/volatile + partial load"},
+    {2, 1, "counter barrier only"},
+    {3, 1, "slots release push, relaxed poll, stride 8B"},
+    {3, 4, "slots release push, relaxed poll, stride 32B"},
+    {3, 32, "slots release push, relaxed poll, stride 256B"},
+    {4, 1, "slots relaxed push, stride 8B"},
+    {4, 32, "slots relaxed push, stride 256B"},
+    {5, 1, "slots release push + acquire fence, stride 8B"},
+    {6, 1, "slots release push, warp-0 poll, stride 8B"},
+    {6, 32, "slots release push, warp-0 poll, stride 256B"},
+  };
+  for (auto& v : vs) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(ctr, 0, 8);
+      fill<<<64, 256>>>((unsigned long long*)slots, (size_t)3 * G * maxstride, SENT);
+      Args a{v.v, iters, G, v.stride, ctr, slots, parts, out};
+      void* args[] = {&a};
+      cudaError_t e = cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(NT), args, 0, 0);
+      if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return 1; }
+      e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("run: %s\n", cudaGetErrorString(e)); return 1; }
+      unsigned long long h[2]; cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
+      if (rep == 1) printf("%-55s %7.3f us/op  (check %.6e)\n", v.name, h[0] / 1e3 / iters, __builtin_bit_cast(double, h[1]));
+    }
+  }
+  return 0;
+}
