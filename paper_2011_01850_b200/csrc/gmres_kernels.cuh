@@ -34,10 +34,16 @@ constexpr int NGRP = NW;         // CSR-stream pipelines per CTA: one per warp
 constexpr int GT = NT / NGRP;    // threads per pipeline (one warp)
 constexpr int CHUNK_CAP = 256;   // max nnz of a TMA-staged CSR chunk
 constexpr int CHUNK_RMAX = GT;   // max rows of a CSR chunk (multiple of 4)
-constexpr int ST_OFF_CI = 160;                             // stage layout (bytes): row_ptr slice
-constexpr int ST_OFF_A = ST_OFF_CI + (CHUNK_CAP + 8) * 4;  // 1216: col slice, then values
-constexpr int STAGE_BYTES = ST_OFF_A + (CHUNK_CAP + 8) * 8;  // 3328
-constexpr int TILE_BYTES = NGRP * 2 * STAGE_BYTES;         // 106496: 2 stages per warp
+constexpr int ST_OFF_RV = 160;                              // stage layout (bytes): row_ptr slice,
+constexpr int ST_OFF_CI = ST_OFF_RV + CHUNK_RMAX * 8;       // 416: per-row operand slice (dinv),
+constexpr int ST_OFF_A = ST_OFF_CI + (CHUNK_CAP + 8) * 4;   // 1472: col slice, then values
+// per-warp TMA ring: NSTG(AT) stages of stage_bytes(AT) (fp32 values: 4 × 2528 B,
+// fp64 values: 3 × 3584 B), i.e. 3 resp. 2 chunks in flight per warp while one
+// is consumed (≈ 64–96 KB per SM: enough bytes in flight for HBM rate)
+template <class AT> __host__ __device__ constexpr int NSTG() { return sizeof(AT) == 4 ? 4 : 3; }
+template <class AT> __host__ __device__ constexpr int stage_bytes() { return ST_OFF_A + (CHUNK_CAP + 8) * (int)sizeof(AT); }
+constexpr int MAXSTG = 4;
+constexpr int TILE_BYTES = NGRP * 3 * (ST_OFF_A + (CHUNK_CAP + 8) * 8);  // 172032 (≥ the fp32 ring, 161792)
 constexpr int MAX_M = 256;                               // restart length limit (shared-memory bound)
 constexpr int ARR_PAD = 8;   // elements of slack after rp/col/val (TMA rounds up to 16 B)
 constexpr int MAXR = 8;      // ranks (GPUs) of a row-partitioned solve
@@ -181,7 +187,7 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned 
 
 // per-CTA control block in static shared memory
 struct Shm {
-  unsigned long long mbar[NGRP][2];  // TMA stage barriers (per CSR-stream group)
+  unsigned long long mbar[NGRP][MAXSTG];  // TMA stage barriers (per CSR-stream group)
   unsigned long long mbar_v[3];      // TMA barriers of the resident-MGS basis buffers
   unsigned tma_phase[NGRP];          // bit s: parity of the next completion of stage s
   unsigned vphase;                   // bit b: parity of the next completion of mbar_v[b]
@@ -220,8 +226,7 @@ __device__ __forceinline__ void init_shm(Shm& sh) {
     sh.vphase = 0;
     for (int g = 0; g < NGRP; ++g) {
       sh.tma_phase[g] = 0;
-      mbar_init(&sh.mbar[g][0], 1);
-      mbar_init(&sh.mbar[g][1], 1);
+      for (int t = 0; t < MAXSTG; ++t) mbar_init(&sh.mbar[g][t], 1);
     }
     for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_v[b], 1);
     fence_mbar_init();
@@ -314,13 +319,19 @@ __device__ __forceinline__ void block_sum(double (&v)[K], Shm& sh, double* out) 
 // One-value all-reduce of a per-thread contribution: CTA sum (warp trees,
 // warps in order) → push → arrive/wait → fixed-order sum over all GG CTAs.
 // (acq is implied: the counter acquire orders every later read.)
-__device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool /*acq*/, double& out) {
+struct NoMid { __device__ __forceinline__ void operator()() const {} };
+// mid() runs in every thread right after the CTA barrier that follows the
+// local contributions (e.g. to reuse a buffer the contributions were read from)
+template <class Mid = NoMid>
+__device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool /*acq*/, double& out,
+                                           Mid mid = Mid()) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int buf = sh.red_epoch & 1;
   v = warp_sum(v);
   if (lane == 0) sh.red[warp] = v;
   __syncthreads();
-  if (warp == 0) {
+  mid();
+  if (warp == 1) {  // (warp 1 releases: warp 0 may hold in-flight bulk copies, see mgs_resident)
     double s = lane < NW ? sh.red[lane] : 0.0;  // fixed shuffle tree over the warps
 #pragma unroll
     for (int o = NW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -414,73 +425,188 @@ template <> struct AccOps<double> {
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 };
 
-template <class AT, int L, class Gather, class Pre, class Epi>
-__device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __restrict__ vals, Gather gat, Pre pre,
-                           Epi epi) {
+// Chunk metadata of one warp's pipeline, 32 chunks per batch held one per
+// lane (two batches: current and next) and read with warp shuffles, so the
+// chunk table never sits on a chunk's critical path (ncu r01: the two
+// dependent loads of d.chunks per chunk were a top long-scoreboard stall).
+struct ChunkMeta { int rb, nb, direct, re, ne; };
+struct MetaWin {
+  int base;                 // pipeline index of lane 0's chunk in cur
+  int cur[5], nxt[5];
+  __device__ __forceinline__ void load(const Dev& d, int c0, int c1, int grp, int kb, int (&m)[5]) {
+    const int c = c0 + grp + (kb + (int)(threadIdx.x & 31)) * NGRP;
+    if (c < c1) {
+      const int4 e = d.chunks[c], f = d.chunks[c + 1];
+      m[0] = e.x; m[1] = e.y; m[2] = e.z; m[3] = f.x; m[4] = f.y;
+    } else {
+      m[0] = m[1] = m[2] = m[3] = m[4] = 0;
+    }
+  }
+  __device__ __forceinline__ void init(const Dev& d, int c0, int c1, int grp) {
+    base = 0;
+    load(d, c0, c1, grp, 0, cur);
+    load(d, c0, c1, grp, 32, nxt);
+  }
+  // k (warp-uniform) ≥ base; advances the window when k leaves cur
+  __device__ __forceinline__ void advance(const Dev& d, int c0, int c1, int grp, int k) {
+    while (k >= base + 32) {
+#pragma unroll
+      for (int t = 0; t < 5; ++t) cur[t] = nxt[t];
+      base += 32;
+      load(d, c0, c1, grp, base + 32, nxt);
+    }
+  }
+  // metadata of pipeline chunk k, base ≤ k < base + 64 (warp-uniform)
+  __device__ __forceinline__ ChunkMeta get(int k) const {
+    const int idx = k - base;
+    int v[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      const int a = __shfl_sync(0xffffffffu, cur[t], idx & 31);
+      const int b = __shfl_sync(0xffffffffu, nxt[t], idx & 31);
+      v[t] = idx < 32 ? a : b;
+    }
+    return ChunkMeta{v[0], v[1], v[2], v[3], v[4]};
+  }
+};
+
+// CSR stream.  epi(row, acc, pv, diag) gets the row sum, pre()'s value and
+// the gathered value at the diagonal column (0 if the row has none).
+template <class AT, int L, class RT, class Gather, class Pre, class Epi>
+__device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __restrict__ vals,
+                           const RT* __restrict__ rowv, Gather gat, Pre pre, Epi epi) {
   using Ops = AccOps<AT>;
-  using PT = decltype(pre(0));
+  using PT = decltype(pre(0, (RT)0));
   const int grp = threadIdx.x / GT, gt = threadIdx.x % GT;
   const int c0 = d.chunk_off[blockIdx.x], c1 = d.chunk_off[blockIdx.x + 1] - 1;
-  char* gbase = s_stage + grp * 2 * STAGE_BYTES;
-  auto issue = [&](int c, int s) {  // group leader only
-    const int4 e = d.chunks[c], f = d.chunks[c + 1];
-    if (e.z) return;
-    char* st = gbase + s * STAGE_BYTES;
-    const int ea = e.y & ~3, eb = (f.y + 3) & ~3;
-    const unsigned b_rp = (unsigned)(((f.x - e.x + 1) + 3) & ~3) * 4u;
+  const int nk = c1 - c0 > grp ? (c1 - c0 - grp + NGRP - 1) / NGRP : 0;  // chunks of this pipeline
+  constexpr int NS = NSTG<AT>(), SB = stage_bytes<AT>();
+  constexpr int GB = 8;
+  char* gbase = s_stage + grp * NS * SB;
+  MetaWin mw;
+  mw.init(d, c0, c1, grp);
+  auto issue = [&](const ChunkMeta& m, int s) {  // group leader only
+    if (m.direct) return;
+    char* st = gbase + s * SB;
+    const int ea = m.nb & ~3, eb = (m.ne + 3) & ~3;
+    const unsigned b_rp = (unsigned)(((m.re - m.rb + 1) + 3) & ~3) * 4u;
     const unsigned b_ci = (unsigned)(eb - ea) * 4u;
     const unsigned b_a = (unsigned)(eb - ea) * (unsigned)sizeof(AT);
-    // (no proxy fence: the TMA reads never-written global data and overwrites
-    // a stage the warp finished reading before the __syncwarp)
-    mbar_expect_tx(&sh.mbar[grp][s], b_rp + b_ci + b_a);
-    tma_load_1d(st, d.rp + e.x, b_rp, &sh.mbar[grp][s]);
+    const unsigned b_rv = (unsigned)((m.re - m.rb) * (int)sizeof(RT) + 15) & ~15u;  // rowv is padded to 32 rows
+    // (no proxy fence: the TMA reads data no generic store of this launch
+    // wrote, and overwrites a stage the warp finished reading before the __syncwarp)
+    mbar_expect_tx(&sh.mbar[grp][s], b_rp + b_rv + b_ci + b_a);
+    tma_load_1d(st, d.rp + m.rb, b_rp, &sh.mbar[grp][s]);
+    tma_load_1d(st + ST_OFF_RV, rowv + m.rb, b_rv, &sh.mbar[grp][s]);
     if (b_ci) {
       tma_load_1d(st + ST_OFF_CI, d.ci + ea, b_ci, &sh.mbar[grp][s]);
       tma_load_1d(st + ST_OFF_A, vals + ea, b_a, &sh.mbar[grp][s]);
     }
   };
-  if (gt == 0) {
-    if (c0 + grp < c1) issue(c0 + grp, 0);
-    if (c0 + grp + NGRP < c1) issue(c0 + grp + NGRP, 1);
+  for (int t = 0; t < NS && t < nk; ++t) {
+    const ChunkMeta m = mw.get(t);
+    if (gt == 0) issue(m, t);
   }
   const int wl = threadIdx.x & 31, gw = gt >> 5;  // lane, warp within the group
-  int i = 0;
-  for (int c = c0 + grp; c < c1; c += NGRP, ++i) {
-    const int s = i & 1;
-    const int4 e = d.chunks[c];
-    const int rb = e.x, nrow = d.chunks[c + 1].x - rb;
-    if (!e.z) {
-      stage_wait(d, sh, grp, s);
-      const char* st = gbase + s * STAGE_BYTES;
-      const int* srp = reinterpret_cast<const int*>(st);
-      const int* sci = reinterpret_cast<const int*>(st + ST_OFF_CI);
-      const AT* sa = reinterpret_cast<const AT*>(st + ST_OFF_A);
-      const int ea = e.y & ~3;
-      // a lane's elements p0+lane, p0+lane+L, ... in batches of GB: all GB
-      // gathers are issued before the (in-order) accumulation
-      constexpr int GB = 8;
-      auto row_dot = [&](int p0, int p1, int lane) -> AT {
-        AT acc = (AT)0;
-        for (int pb = p0 + lane; pb < p1; pb += GB * L) {
-          AT g[GB], a[GB];
+  struct Stg { const int* rp; const int* ci; const AT* a; const RT* rv; int ea; };
+  auto stage = [&](int s, const ChunkMeta& m) {
+    const char* st = gbase + s * SB;
+    return Stg{reinterpret_cast<const int*>(st), reinterpret_cast<const int*>(st + ST_OFF_CI),
+               reinterpret_cast<const AT*>(st + ST_OFF_A), reinterpret_cast<const RT*>(st + ST_OFF_RV), m.nb & ~3};
+  };
+  // a lane's elements p0+lane, p0+lane+L, ... in batches of GB: all GB
+  // gathers are issued before the (in-order) accumulation
+  auto row_dot = [&](const Stg& S, int row, int p0, int p1, int lane, AT& diag) -> AT {
+    AT acc = (AT)0;
+    for (int pb = p0 + lane; pb < p1; pb += GB * L) {
+      AT g[GB], a[GB];
+      int cc[GB];
 #pragma unroll
-          for (int u = 0; u < GB; ++u) {
-            const int p = pb + u * L;
-            const bool ok = p < p1;
-            g[u] = ok ? gat(sci[p]) : (AT)0;
-            a[u] = ok ? sa[p] : (AT)0;
+      for (int u = 0; u < GB; ++u) {
+        const int p = pb + u * L;
+        const bool ok = p < p1;
+        cc[u] = ok ? S.ci[p] : -1;
+        g[u] = ok ? gat(cc[u]) : (AT)0;
+        a[u] = ok ? S.a[p] : (AT)0;
+      }
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        if (pb + u * L < p1) acc = Ops::add(acc, Ops::mul(a[u], g[u]));
+        if (cc[u] == row) diag = g[u];
+      }
+    }
+    return acc;
+  };
+  for (int k = 0; k < nk; ++k) {
+    mw.advance(d, c0, c1, grp, k);
+    const int s = k % NS;
+    const ChunkMeta m = mw.get(k);
+    const int rb = m.rb, nrow = m.re - m.rb;
+    // one thread per row and an even ring: consume two staged chunks at once,
+    // so that both chunks' gathers are in flight together (the stream is
+    // bound by the per-chunk gather latency at one chunk per warp)
+    if (L == 1 && NS % 2 == 0 && !(d.tune & 1024) && k + 1 < nk) {
+      const ChunkMeta m2 = mw.get(k + 1);
+      if (!m.direct && !m2.direct) {
+        const int s2 = (k + 1) % NS;
+        const int rb2 = m2.rb, nrow2 = m2.re - m2.rb;
+        stage_wait(d, sh, grp, s);
+        stage_wait(d, sh, grp, s2);
+        const Stg S1 = stage(s, m), S2 = stage(s2, m2);
+        for (int lr = gt; lr < max(nrow, nrow2); lr += GT) {
+          const bool act1 = lr < nrow, act2 = lr < nrow2;
+          PT pv1{}, pv2{};
+          if (act1) pv1 = pre(rb + lr, S1.rv[lr]);
+          if (act2) pv2 = pre(rb2 + lr, S2.rv[lr]);
+          int p1 = act1 ? S1.rp[lr] - S1.ea : 0, q1 = act1 ? S1.rp[lr + 1] - S1.ea : 0;
+          int p2 = act2 ? S2.rp[lr] - S2.ea : 0, q2 = act2 ? S2.rp[lr + 1] - S2.ea : 0;
+          AT acc1 = (AT)0, acc2 = (AT)0, dg1 = (AT)0, dg2 = (AT)0;
+          while (p1 < q1 || p2 < q2) {
+            AT g1[GB], a1[GB], g2[GB], a2[GB];
+            int k1[GB], k2[GB];
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+              const bool o1 = p1 + u < q1, o2 = p2 + u < q2;
+              k1[u] = o1 ? S1.ci[p1 + u] : -1;
+              k2[u] = o2 ? S2.ci[p2 + u] : -1;
+              g1[u] = o1 ? gat(k1[u]) : (AT)0;
+              a1[u] = o1 ? S1.a[p1 + u] : (AT)0;
+              g2[u] = o2 ? gat(k2[u]) : (AT)0;
+              a2[u] = o2 ? S2.a[p2 + u] : (AT)0;
+            }
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+              if (p1 + u < q1) acc1 = Ops::add(acc1, Ops::mul(a1[u], g1[u]));
+              if (p2 + u < q2) acc2 = Ops::add(acc2, Ops::mul(a2[u], g2[u]));
+              if (k1[u] == rb + lr) dg1 = g1[u];
+              if (k2[u] == rb2 + lr) dg2 = g2[u];
+            }
+            p1 += GB;
+            p2 += GB;
           }
-#pragma unroll
-          for (int u = 0; u < GB; ++u)
-            if (pb + u * L < p1) acc = Ops::add(acc, Ops::mul(a[u], g[u]));
+          if (act1) epi(rb + lr, acc1, pv1, dg1);
+          if (act2) epi(rb2 + lr, acc2, pv2, dg2);
         }
-        return acc;
-      };
+        __syncwarp();
+        const ChunkMeta n1 = mw.get(min(k + NS, nk - 1)), n2 = mw.get(min(k + NS + 1, nk - 1));
+        if (gt == 0) {
+          sh.tma_phase[grp] ^= (1u << s) | (1u << s2);
+          if (k + NS < nk) issue(n1, s);
+          if (k + NS + 1 < nk) issue(n2, s2);
+        }
+        ++k;
+        continue;
+      }
+    }
+    if (!m.direct) {
+      stage_wait(d, sh, grp, s);
+      const Stg S = stage(s, m);
       if (L == 1) {
         for (int lr = gt; lr < nrow; lr += GT) {
-          const PT pv = pre(rb + lr);
-          const AT acc = row_dot(srp[lr] - ea, srp[lr + 1] - ea, 0);
-          epi(rb + lr, acc, pv);
+          const PT pv = pre(rb + lr, S.rv[lr]);
+          AT dg = (AT)0;
+          const AT acc = row_dot(S, rb + lr, S.rp[lr] - S.ea, S.rp[lr + 1] - S.ea, 0, dg);
+          epi(rb + lr, acc, pv, dg);
         }
       } else {
         const int sub = wl / L, lane = wl & (L - 1);
@@ -488,12 +614,15 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
           const int lr = base + sub;
           const bool act = lr < nrow;
           PT pv{};
-          if (act && lane == 0) pv = pre(rb + lr);
-          AT acc = (AT)0;
-          if (act) acc = row_dot(srp[lr] - ea, srp[lr + 1] - ea, lane);
+          if (act && lane == 0) pv = pre(rb + lr, S.rv[lr]);
+          AT acc = (AT)0, dg = (AT)0;
+          if (act) acc = row_dot(S, rb + lr, S.rp[lr] - S.ea, S.rp[lr + 1] - S.ea, lane, dg);
 #pragma unroll
-          for (int o = L / 2; o > 0; o >>= 1) acc = Ops::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-          if (act && lane == 0) epi(rb + lr, acc, pv);
+          for (int o = L / 2; o > 0; o >>= 1) {
+            acc = Ops::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+            dg += __shfl_xor_sync(0xffffffffu, dg, o);  // one lane holds the diagonal
+          }
+          if (act && lane == 0) epi(rb + lr, acc, pv, dg);
         }
       }
     } else {
@@ -501,19 +630,28 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
       for (int lr = gw; lr < nrow; lr += GT / 32) {
         const int row = rb + lr;
         PT pv{};
-        if (wl == 0) pv = pre(row);
+        if (wl == 0) pv = pre(row, __ldg(rowv + row));
         const int p0 = __ldg(d.rp + row), p1 = __ldg(d.rp + row + 1);
-        AT acc = (AT)0;
-        for (int p = p0 + wl; p < p1; p += 32) acc = Ops::add(acc, Ops::mul(__ldg(vals + p), gat(__ldg(d.ci + p))));
+        AT acc = (AT)0, dg = (AT)0;
+        for (int p = p0 + wl; p < p1; p += 32) {
+          const int col = __ldg(d.ci + p);
+          const AT g = gat(col);
+          acc = Ops::add(acc, Ops::mul(__ldg(vals + p), g));
+          if (col == row) dg = g;
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc = Ops::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-        if (wl == 0) epi(row, acc, pv);
+        for (int o = 16; o > 0; o >>= 1) {
+          acc = Ops::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+          dg += __shfl_xor_sync(0xffffffffu, dg, o);
+        }
+        if (wl == 0) epi(row, acc, pv, dg);
       }
     }
-    group_sync(grp);
+    __syncwarp();
+    const ChunkMeta n = mw.get(min(k + NS, nk - 1));
     if (gt == 0) {
-      if (!e.z) sh.tma_phase[grp] ^= (1u << s);
-      if (c + 2 * NGRP < c1) issue(c + 2 * NGRP, s);
+      if (!m.direct) sh.tma_phase[grp] ^= (1u << s);
+      if (k + NS < nk) issue(n, s);
     }
   }
   __syncthreads();
@@ -529,8 +667,8 @@ __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict_
   const double* __restrict__ x = d.x;
   struct P2 { double b; W di; };
   auto gat = [&](int col) -> double { return x[col]; };
-  auto pre = [&](int row) -> P2 { return P2{d.b[row], __ldg(dinv + row)}; };
-  auto epi = [&](int row, double acc, P2 pv) {
+  auto pre = [&](int row, W di) -> P2 { return P2{d.b[row], di}; };
+  auto epi = [&](int row, double acc, P2 pv, double) {
     const double bi = pv.b;
     bb += bi * bi;
     const double z = bi - acc;
@@ -541,7 +679,7 @@ __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict_
     r_out[row] = ri;
     rr += (double)ri * (double)ri;
   };
-  csr_stream<double, L>(d, sh, s_stage, d.a64, gat, pre, epi);
+  csr_stream<double, L>(d, sh, s_stage, d.a64, dinv, gat, pre, epi);
 }
 
 // ------------------------------------------------------------------ a2
@@ -553,14 +691,13 @@ template <class W, int L>
 __device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
                            W* __restrict__ dst, W* __restrict__ vcol) {
   const W* dinv = (const W*)d.dinvW;
-  struct P2 { W di; W self; };
   auto gat = [&](int col) -> W { return RN<W>((double)src[col] * inv); };
-  auto pre = [&](int row) -> P2 { return P2{__ldg(dinv + row), vcol ? src[row] : (W)0}; };
-  auto epi = [&](int row, W acc, P2 pv) {
-    dst[row] = mulw(pv.di, acc);
-    if (vcol) vcol[row] = RN<W>((double)pv.self * inv);
+  auto pre = [&](int, W di) -> W { return di; };
+  auto epi = [&](int row, W acc, W di, W vj) {
+    dst[row] = mulw(di, acc);
+    if (vcol) vcol[row] = vj;  // v_j at the diagonal = RN_W(src_row · inv), gathered above
   };
-  csr_stream<W, L>(d, sh, s_stage, (const W*)d.aW, gat, pre, epi);
+  csr_stream<W, L>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, epi);
 }
 
 // ------------------------------------------------------------------ a3
@@ -808,17 +945,18 @@ struct SmemLayout {
   init_shm(sh);
 
 // ------------------------------------------------------------------ a3 (resident)
-// MGS with the CTA's rows of w and of v_{i−1} in registers
-// and the basis vectors streamed through a ring of NB shared-memory buffers by
-// TMA bulk copies: at the top of step i the copy of v_{i+NB−1} is issued into
-// the buffer v_{i−1} left, then one pass forms w ← RN_W(w − RN_W(h_{i−1})·v_{i−1})
-// and the partial of h_i = w·v_i.  The HBM read of the next vectors therefore
-// overlaps h_i's all-reduce, and no register holds an in-flight load across
-// it.  Same operations and order per element as mgs_sweep.
-constexpr int MGS_MV = 8;  // 16-byte vectors per thread (w and v_{i-1} in registers)
+// MGS with the CTA's rows of w in registers and the basis
+// vectors streamed through a ring of NB shared-memory buffers by TMA bulk
+// copies: step i forms w ← RN_W(w − RN_W(h_{i−1})·v_{i−1}) and the partial of
+// h_i = w·v_i in one pass (v_{i−1}, v_i read from the ring); right after the
+// CTA barrier of h_i's all-reduce the buffer of v_{i−1} is free and the copy
+// of v_{i+NB−1} is issued into it, so the HBM reads of the next vectors overlap
+// the all-reduce and no register holds an in-flight load across it.  Same
+// operations and order per element as mgs_sweep.
+constexpr int MGS_MV = 8;  // 16-byte vectors of w per thread (registers)
 template <class W>
 __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
-                                          W* w, double* s_h, char* s_tiles, double& NN) {
+                                             W* w, double* s_h, char* s_tiles, double& NN) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
   const int q0 = r0 / N, nq = r1 / N - q0;
@@ -827,6 +965,8 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   V4* sv = reinterpret_cast<V4*>(s_tiles);
   const unsigned bytes = (unsigned)nq * 16u;
   unsigned ph = sh.vphase;
+  // copies are issued by warp 0 (TMA_T): warp 1 performs the all-reduce's release
+  constexpr int TMA_T = 0;
   auto issue = [&](int c) {  // one thread: v_c (1-based) → buffer (c−1) mod NB
     const int b = (c - 1) % NB;
     char* dst = reinterpret_cast<char*>(sv + (size_t)b * nqa);
@@ -845,11 +985,9 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
       if ((long long)(globaltimer() - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); return false; }
     }
   };
-  // copies are issued by warp 1 (TMA_T): warp 0 performs the all-reduce's release
-  constexpr int TMA_T = 32;
   if (threadIdx.x == TMA_T)
     for (int c = 1; c <= min(NB - 1, j); ++c) issue(c);
-  V4 wr[MGS_MV], vp[MGS_MV];
+  V4 wr[MGS_MV];
   {
     const V4* wg = reinterpret_cast<const V4*>(w) + q0;
 #pragma unroll
@@ -859,36 +997,38 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     }
   }
   W hprev = (W)0;
-  bool ok = true;
   const bool lead = d.profile && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long tp = lead ? globaltimer() : 0ull;
   auto tick = [&](int slot) {
     if (lead) { const unsigned long long t = globaltimer(); d.prof[slot] += t - tp; tp = t; }
   };
   for (int i = 1; i <= j; ++i) {
-    if (threadIdx.x == TMA_T && i + NB - 1 <= j) issue(i + NB - 1);
     const int b = (i - 1) % NB;
-    ok = wait(b) && ok;
+    wait(b);
     tick(8);
-    const V4* X = sv + (size_t)b * nqa;
+    const V4* X = sv + (size_t)b * nqa;                       // v_i
+    const V4* Y = sv + (size_t)((i - 2 + NB) % NB) * nqa;     // v_{i−1} (i > 1)
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < MGS_MV; ++k) {
       const int t = threadIdx.x + k * NT;
       if (t < nq) {
-        W* pa = reinterpret_cast<W*>(&wr[k]);
         if (i > 1) {
-          const W* pb = reinterpret_cast<const W*>(&vp[k]);
+          const V4 y = Y[t];
+          W* pa = reinterpret_cast<W*>(&wr[k]);
+          const W* pb = reinterpret_cast<const W*>(&y);
 #pragma unroll
           for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hprev, pb[u]));
         }
-        vp[k] = X[t];
-        acc += dotv(wr[k], vp[k]);
+        acc += dotv(wr[k], X[t]);
       }
     }
     tick(9);
     double h;
-    if (!allreduce1(d, sh, acc, false, h)) return false;
+    auto mid = [&]() {
+      if (threadIdx.x == TMA_T && i + NB - 1 <= j) issue(i + NB - 1);  // into v_{i−1}'s buffer
+    };
+    if (!allreduce1(d, sh, acc, false, h, mid)) return false;
     if (threadIdx.x == 0) s_h[i - 1] = h;
     hprev = RN<W>(h);
     tick(10);
@@ -896,13 +1036,15 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   // final update w ← w − h_j v_j, ‖w‖², w back to global for the next SpMV
   double nn = 0.0;
   {
+    const V4* X = sv + (size_t)((j - 1) % NB) * nqa;
     V4* wg = reinterpret_cast<V4*>(w) + q0;
 #pragma unroll
     for (int k = 0; k < MGS_MV; ++k) {
       const int t = threadIdx.x + k * NT;
       if (t < nq) {
+        const V4 x = X[t];
         W* pa = reinterpret_cast<W*>(&wr[k]);
-        const W* pb = reinterpret_cast<const W*>(&vp[k]);
+        const W* pb = reinterpret_cast<const W*>(&x);
 #pragma unroll
         for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hprev, pb[u]));
         nn += dotv(wr[k], wr[k]);
@@ -1194,9 +1336,9 @@ __global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int ite
     } else if (what == 6) {  // CSR stream without gathers (TMA streaming + epilogue)
       const W* dinv = (const W*)d.dinvW;
       auto gat = [&](int) -> W { return (W)1; };
-      auto pre = [&](int row) -> W { return __ldg(dinv + row); };
-      auto epi = [&](int row, W a, W di) { w[row] = mulw(di, a); };
-      csr_stream<W, 1>(d, sh, s_tiles, (const W*)d.aW, gat, pre, epi);
+      auto pre = [&](int, W di) -> W { return di; };
+      auto epi = [&](int row, W a, W di, W) { w[row] = mulw(di, a); };
+      csr_stream<W, 1>(d, sh, s_tiles, (const W*)d.aW, dinv, gat, pre, epi);
     } else if (what == 7) {  // full SpMV phase (gathers from V column 0), L = 1
       spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, nullptr);
     } else if (what == 8) {  // ... plus the fused V-column write (as in the solve)
