@@ -122,14 +122,18 @@ int gmres_k_resid(gmres_ctx* ctx, int32_t precision, const double* d_b, const do
                   double* out2);
 
 /* a3/a4 + a5 (Alg. 1): orthogonalise d_w (n, W) in place against
- * the j columns of d_V (column-major, leading dimension ldv ≥ n, ldv % 64 == 0)
- * with MGS or CGSR; h_out (host) receives h_{1..j} and h_out[j] = ‖w‖₂. */
+ * the j columns of d_V (column-major, leading dimension ldv ≥ round_up(n, 256),
+ * ldv % 64 == 0, rows ≥ n zero) with MGS or CGSR; h_out (host) receives
+ * h_{1..j} and h_out[j] = ‖w‖₂.  CGSR copies V into the row-blocked layout a
+ * CGSR solve keeps its basis in and runs on that copy. */
 int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
                   void* d_w, double* h_out);
 
-/* a8 (Alg. 1): d_x += Σ_{i<J} (double)V_i · y_i; y host[J]. */
+/* a8 (Alg. 1): d_x += Σ_{i<J} (double)V_i · y_i; y host[J];
+ * d_V as for gmres_k_ortho.  blocked != 0: run on a row-blocked copy of V
+ * (the layout of a CGSR solve), else on d_V itself (the MGS solves' layout). */
 int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_V, int64_t ldv, const double* y,
-                    double* d_x);
+                    double* d_x, int32_t blocked);
 
 /* a6 + a7 (Alg. 1) on the device: apply the Givens steps to the
  * J columns of the unrotated (m+1)×m Hessenberg Hbar (host, column-major,

@@ -22,8 +22,8 @@ struct gmres_ctx {
   int device = 0;
   int sms = 0;
   int64_t n = 0, nnz = 0;
-  int64_t nvec = 0;  // n rounded up to ROWALIGN
-  int64_t ldv = 0;   // n rounded up to LDALIGN
+  int64_t nvec = 0;  // n rounded up to VEC_ALIGN (padded length of every n-vector)
+  int64_t ldv = 0;   // leading dimension of column-major V (= nvec)
   std::vector<int32_t> h_rp;  // host row_ptr (row partitioning)
   int32_t* d_rp = nullptr;
   int32_t* d_ci = nullptr;
@@ -61,7 +61,7 @@ struct gmres_ctx {
   int* d_row_begin = nullptr;
   int4* d_chunks = nullptr;
   int* d_chunk_off = nullptr;
-  int part_G = 0;
+  int part_G = 0, part_align = 0;
   int part_max_rows = 0;  // largest CTA row block of the partition
   // last solve
   std::vector<double> inner_host;
@@ -102,25 +102,47 @@ int auto_lanes(int64_t n, int64_t nnz) {
   return L;
 }
 
-// Row partition over G CTAs: boundaries on multiples of ROWALIGN, balancing
-// rows + nnz (the merge-path cost), last boundary = nvec.
-void make_partition(const std::vector<int32_t>& rp, int64_t n, int64_t nvec, int G, std::vector<int>& out) {
+// Row partition over G CTAs: boundaries on multiples of `align` rows (32, or
+// the V block height of the row-blocked layout), balancing rows + nnz (the
+// merge-path cost), last boundary = nvec.
+void make_partition(const std::vector<int32_t>& rp, int64_t n, int64_t nvec, int G, int align, std::vector<int>& out) {
   out.assign(G + 1, 0);
   const double total = (double)nvec + (double)rp[n];
   auto cost = [&](int64_t r) { return (double)r + (double)rp[std::min(r, n)]; };
-  const int64_t nblk = nvec / ROWALIGN;
+  const int64_t nblk = nvec / align;
   int64_t lo = 0;
   for (int g = 1; g < G; ++g) {
     const double target = total * g / G;
     int64_t a = lo, b = nblk;  // find smallest block boundary with cost ≥ target
     while (a < b) {
       int64_t mid = (a + b) / 2;
-      if (cost(mid * ROWALIGN) < target) a = mid + 1; else b = mid;
+      if (cost(mid * align) < target) a = mid + 1; else b = mid;
     }
     lo = a;
-    out[g] = (int)(a * ROWALIGN);
+    out[g] = (int)(a * align);
   }
   out[G] = (int)nvec;
+}
+
+// V layout of a solve (gmres_kernels.cuh Dev): CGSR → row-blocked with the
+// largest power-of-two block height in [32, 256] whose (m+1)-column block fits
+// half the staging region; MGS (and CGSR at very large m) → column-major.
+struct VLayout { int tb = 0, tp = 0, lg = 0; long long bs = 0; };
+VLayout vlayout_for(int ortho, int m, int wb, int tile_bytes) {
+  VLayout L;
+  if (ortho != GMRES_CGSR) return L;
+  const int pade = 16 / wb;
+  for (int tb = 256; tb >= 32; tb /= 2) {
+    if ((long long)(m + 1) * (tb + pade) * wb <= tile_bytes / 2) {
+      L.tb = tb;
+      L.tp = tb + pade;
+      L.lg = 0;
+      while ((1 << L.lg) < tb) ++L.lg;
+      L.bs = (long long)(m + 1) * L.tp;
+      return L;
+    }
+  }
+  return L;
 }
 
 template <class W, int L>
@@ -250,10 +272,10 @@ void make_chunks(const std::vector<int32_t>& rp, int64_t n, const std::vector<in
   off[G] = (int)ent.size();
 }
 
-int ensure_partition(gmres_ctx* ctx, int G) {
-  if (ctx->part_G == G && ctx->d_row_begin) return 0;
+int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
+  if (ctx->part_G == G && ctx->part_align == align && ctx->d_row_begin) return 0;
   std::vector<int> rb;
-  make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, rb);
+  make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, align, rb);
   ctx->part_max_rows = 0;
   for (int g = 0; g < G; ++g) ctx->part_max_rows = std::max(ctx->part_max_rows, rb[g + 1] - rb[g]);
   std::vector<int4> ent;
@@ -272,6 +294,7 @@ int ensure_partition(gmres_ctx* ctx, int G) {
   CK(cudaMalloc(&ctx->d_chunk_off, sizeof(int) * (G + 1)));
   CK(cudaMemcpy(ctx->d_chunk_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
   ctx->part_G = G;
+  ctx->part_align = align;
   return 0;
 }
 
@@ -286,7 +309,11 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   const size_t kmax = (size_t)kmax_for(m);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t r = off; off += (bytes + 255) & ~size_t(255); return r; };
-  const size_t oV = take(wb * ctx->ldv * (m + 1));
+  // V: column-major ldv × (m+1), or row-blocked (nvec/32 blocks at most,
+  // each (m+1) columns of 32 + 16/wb elements) — the larger of the two
+  const size_t v_cm = (size_t)ctx->ldv * (m + 1);
+  const size_t v_bl = (size_t)(ctx->nvec / 32) * (m + 1) * (32 + 16 / wb);
+  const size_t oV = take(wb * std::max(v_cm, v_bl));
   const size_t ow0 = take(wb * ctx->ldv);
   const size_t ow1 = take(wb * ctx->ldv);
   const size_t kst = (kmax + 3) & ~size_t(3);
@@ -457,8 +484,8 @@ int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, 
   if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return bail(GMRES_ECUDA); }
   ctx->n = n;
   ctx->nnz = nnz;
-  ctx->nvec = round_up(n, ROWALIGN);
-  ctx->ldv = round_up(n, LDALIGN);
+  ctx->nvec = round_up(n, VEC_ALIGN);
+  ctx->ldv = ctx->nvec;
   ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
   int rc;
   auto setup = [&]() -> int {
@@ -549,7 +576,9 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   size_t smem = smem_bytes(m, tile_bytes);
   int G = 0;
   if (int rc = grid_for(ctx, kern, smem, opts ? opts->ctas_per_sm : 0, &G)) return rc;
-  if (int rc = ensure_partition(ctx, G)) return rc;
+  const VLayout vl = (opts && (opts->tune & 4096)) ? VLayout{} :
+                     vlayout_for(ortho, m, precision == GMRES_MIXED ? 4 : 8, tile_bytes);
+  if (int rc = ensure_partition(ctx, G, vl.tb ? vl.tb : ROWALIGN)) return rc;
   // resident MGS (gmres_kernels.cuh mgs_resident): every CTA's rows of w and
   // v_{i-1} in ≤ MGS_MV 16-byte registers per thread, and a ring of NB = 3 (else
   // 2) shared buffers of one basis-vector row block for the TMA stream
@@ -600,6 +629,10 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   d.tile_bytes = tile_bytes;
   d.mgs_resident = mgs_resident;
   d.mgs_nbuf = mgs_nbuf;
+  d.vtb = vl.tb;
+  d.vtp = vl.tp;
+  d.vtb_log = vl.lg;
+  d.vbs = vl.bs;
   d.tune = opts ? opts->tune : 0;
 
   gmres_result r{};
@@ -719,7 +752,7 @@ int gmres_k_matrix(gmres_ctx* ctx, const int32_t** row_ptr, const int32_t** col,
 namespace {
 // common prologue of the component entry points: kernels, grid, partition, workspace
 int comp_setup(gmres_ctx* ctx, int prec, int m_req, int kind, int L, const void** kern, int* G, size_t* smem,
-               int* m_ws) {
+               int* m_ws, int align = ROWALIGN) {
   if (int rc = check_prec(ctx, prec)) return rc;
   if (prec == GMRES_MIXED)
     if (int rc = ensure_a32(ctx, ctx->stream)) return rc;
@@ -732,10 +765,29 @@ int comp_setup(gmres_ctx* ctx, int prec, int m_req, int kind, int L, const void*
   int Gk = 0;
   if (int rc = grid_for(ctx, *kern, *smem, 0, &Gk)) return rc;
   if (Gk < *G) *G = Gk;
-  if (int rc = ensure_partition(ctx, *G)) return rc;
+  if (int rc = ensure_partition(ctx, *G, align)) return rc;
   if (int rc = ensure_ws(ctx, m, prec, std::max(*G, ctx->ws_G), std::max(ctx->hist_cap, 4), ctx->inner_cap))
     return rc;
   return reset_flags(ctx, ctx->stream);
+}
+// pack the caller's column-major V into the workspace V in row-blocked layout
+int pack_blocked(gmres_ctx* ctx, int prec, const void* d_V, int64_t ldv, int ncols, const VLayout& vl) {
+  const long long nvalid = std::min<long long>(ldv, ctx->n);
+  if (prec == GMRES_MIXED)
+    pack_vblocked_kernel<float><<<ctx->sms * 4, 256, 0, ctx->stream>>>((const float*)d_V, ldv, ncols, ctx->nvec, nvalid,
+                                                                     (float*)ctx->d_V, vl.tb, vl.tp, vl.bs);
+  else
+    pack_vblocked_kernel<double><<<ctx->sms * 4, 256, 0, ctx->stream>>>((const double*)d_V, ldv, ncols, ctx->nvec,
+                                                                      nvalid, (double*)ctx->d_V, vl.tb, vl.tp, vl.bs);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+void set_vlayout(Dev& d, const VLayout& vl) {
+  d.vtb = vl.tb;
+  d.vtp = vl.tp;
+  d.vtb_log = vl.lg;
+  d.vbs = vl.bs;
 }
 }  // namespace
 
@@ -786,7 +838,7 @@ int gmres_k_resid(gmres_ctx* ctx, int32_t precision, const double* d_b, const do
 int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
                   void* d_w, double* h_out) {
   if (!ctx || !d_V || !d_w || !h_out) return fail(ctx, GMRES_EINVAL, "null argument");
-  if (j < 1 || ldv < ctx->ldv || ldv % LDALIGN) return fail(ctx, GMRES_EINVAL, "need j >= 1, ldv >= round_up(n,64), ldv % 64 == 0");
+  if (j < 1 || ldv < ctx->ldv || ldv % LDALIGN) return fail(ctx, GMRES_EINVAL, "need j >= 1, ldv >= round_up(n,256), ldv % 64 == 0");
   if (ortho != GMRES_MGS && ortho != GMRES_CGSR) return fail(ctx, GMRES_EINVAL, "bad ortho");
   const int L = auto_lanes(ctx->n, ctx->nnz);
   const void* kern;
@@ -795,10 +847,18 @@ int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, c
   int m;
   if (int rc = comp_setup(ctx, precision, j, 2, L, &kern, &G, &smem, &m)) return rc;
   const size_t wb = precision == GMRES_MIXED ? 4 : 8;
+  // CGSR runs on the row-blocked V of a CGSR solve: pack the caller's V
+  const VLayout vl = vlayout_for(ortho, m, (int)wb, tile_bytes_for(m));
+  if (vl.tb) {
+    if (int rc = ensure_partition(ctx, G, vl.tb)) return rc;
+    if (int rc = pack_blocked(ctx, precision, d_V, ldv, j, vl)) return rc;
+  }
   // the work vector lives in the padded workspace buffer (zero padding rows)
   CK(cudaMemsetAsync(ctx->d_w0, 0, wb * ctx->ldv, ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_w0, d_w, wb * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
   Dev d = make_dev(ctx, m, precision, ortho, G);
+  set_vlayout(d, vl);
+  if (vl.tb) d_V = ctx->d_V;
   double* d_h = nullptr;
   CK(cudaMalloc(&d_h, sizeof(double) * (j + 1)));
   long long ld = ldv;
@@ -819,16 +879,24 @@ int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, c
 }
 
 int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_V, int64_t ldv, const double* y,
-                    double* d_x) {
+                    double* d_x, int32_t blocked) {
   if (!ctx || !d_V || !y || !d_x) return fail(ctx, GMRES_EINVAL, "null argument");
-  if (J < 1 || ldv < ctx->ldv || ldv % LDALIGN) return fail(ctx, GMRES_EINVAL, "need J >= 1, ldv >= round_up(n,64), ldv % 64 == 0");
+  if (J < 1 || ldv < ctx->ldv || ldv % LDALIGN) return fail(ctx, GMRES_EINVAL, "need J >= 1, ldv >= round_up(n,256), ldv % 64 == 0");
   const int L = auto_lanes(ctx->n, ctx->nnz);
   const void* kern;
   int G;
   size_t smem;
   int mws;
   if (int rc = comp_setup(ctx, precision, J, 3, L, &kern, &G, &smem, &mws)) return rc;
+  const VLayout vl = blocked ? vlayout_for(GMRES_CGSR, mws, precision == GMRES_MIXED ? 4 : 8, tile_bytes_for(mws))
+                             : VLayout{};
+  if (vl.tb) {
+    if (int rc = ensure_partition(ctx, G, vl.tb)) return rc;
+    if (int rc = pack_blocked(ctx, precision, d_V, ldv, J, vl)) return rc;
+    d_V = ctx->d_V;
+  }
   Dev d = make_dev(ctx, mws, precision, 0, G);
+  set_vlayout(d, vl);
   d.x = d_x;
   double* d_y = nullptr;
   CK(cudaMalloc(&d_y, sizeof(double) * J));

@@ -29,7 +29,8 @@ namespace g200 {
 constexpr int NT = 512;        // threads per CTA (16 warps)
 constexpr int NW = NT / 32;
 constexpr int ROWALIGN = 32;   // row-partition granularity (128 B of fp32)
-constexpr int LDALIGN = 64;    // leading dimension of V (256 B of fp32)
+constexpr int LDALIGN = 64;    // leading dimension of a caller's column-major V (component entry points)
+constexpr int VEC_ALIGN = 256; // padded length of every n-vector (≥ the largest V block height)
 constexpr int NGRP = NW;         // CSR-stream pipelines per CTA: one per warp
 constexpr int GT = NT / NGRP;    // threads per pipeline (one warp)
 constexpr int CHUNK_CAP = 256;   // max nnz of a TMA-staged CSR chunk
@@ -67,8 +68,16 @@ struct Dev {
   const void* dinvW;    // W copy of 1/a_ii
   const double* b;
   double* x;
-  void* V;              // column-major, ldv rows, m+1 columns (W)
-  long long ldv;
+  void* V;              // Krylov basis, m+1 columns (W), layout below
+  long long ldv;        // column-major: leading dimension (rows, ≥ n, multiple of 64)
+  // row-blocked layout (CGSR solves, vtb > 0): block b holds rows
+  // [b·vtb, (b+1)·vtb) of all m+1 columns, column c at V + b·vbs + c·vtp with
+  // vtp = vtb + 16/w_B (padding: lanes reading one row group of different
+  // columns hit distinct banks) and vbs = (m+1)·vtp, so a row tile of whole
+  // blocks is one contiguous TMA copy per block (tools/tma_bench.cu: bulk copies
+  // of ≤ 1 KB stream at ~4 TB/s, ≥ 4 KB at ~7 TB/s).  vtb == 0: column-major.
+  int vtb, vtp, vtb_log;
+  long long vbs;
   void* w0;             // ping-pong work vectors (W, ldv rows, zero padding)
   void* w1;
   // grid all-reduce (see grid_allreduce): this rank's partial array
@@ -110,6 +119,13 @@ struct Dev {
 template <class W> struct VecT;
 template <> struct VecT<float> { using T = float4; static constexpr int N = 4; };
 template <> struct VecT<double> { using T = double2; static constexpr int N = 2; };
+
+// address of V(row, col) in the layout of d (see Dev)
+template <class W>
+__device__ __forceinline__ W* v_at(const Dev& d, W* V, long long row, int col) {
+  if (d.vtb == 0) return V + (long long)col * d.ldv + row;
+  return V + (row >> d.vtb_log) * d.vbs + (long long)col * d.vtp + (row & (d.vtb - 1));
+}
 
 __device__ __forceinline__ float rnw(double v, float*) { return __double2float_rn(v); }
 __device__ __forceinline__ double rnw(double v, double*) { return v; }
@@ -162,6 +178,7 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -189,8 +206,10 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned 
 struct Shm {
   unsigned long long mbar[NGRP][MAXSTG];  // TMA stage barriers (per CSR-stream group)
   unsigned long long mbar_v[3];      // TMA barriers of the resident-MGS basis buffers
+  unsigned long long mbar_t[3];      // TMA barriers of the row-tile passes' V tiles
   unsigned tma_phase[NGRP];          // bit s: parity of the next completion of stage s
   unsigned vphase;                   // bit b: parity of the next completion of mbar_v[b]
+  unsigned tphase;                   // bit b: parity of the next completion of mbar_t[b]
   int abort;
   int flag;
   unsigned long long epoch;          // grid barriers passed by this CTA (thread 0)
@@ -229,6 +248,8 @@ __device__ __forceinline__ void init_shm(Shm& sh) {
       for (int t = 0; t < MAXSTG; ++t) mbar_init(&sh.mbar[g][t], 1);
     }
     for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_v[b], 1);
+    for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_t[b], 1);
+    sh.tphase = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -654,6 +675,9 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
       if (k + NS < nk) issue(n, s);
     }
   }
+  // the epilogue's stores (w, the V column) are read next by TMA bulk copies
+  // (async proxy) of this CTA: order them for that proxy before the barrier
+  fence_proxy_async_global();
   __syncthreads();
 }
 
@@ -689,13 +713,13 @@ __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict_
 // stores the CTA's own rows of v_j into V[:, j−1].
 template <class W, int L>
 __device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
-                           W* __restrict__ dst, W* __restrict__ vcol) {
+                           W* __restrict__ dst, W* __restrict__ V, int vc) {
   const W* dinv = (const W*)d.dinvW;
   auto gat = [&](int col) -> W { return RN<W>((double)src[col] * inv); };
   auto pre = [&](int, W di) -> W { return di; };
   auto epi = [&](int row, W acc, W di, W vj) {
     dst[row] = mulw(di, acc);
-    if (vcol) vcol[row] = vj;  // v_j at the diagonal = RN_W(src_row · inv), gathered above
+    if (V) *v_at(d, V, row, vc) = vj;  // v_j at the diagonal = RN_W(src_row · inv), gathered above
   };
   csr_stream<W, L>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, epi);
 }
@@ -747,111 +771,182 @@ __device__ __noinline__ double mgs_sweep(int r0, int r1, W* __restrict__ w, cons
 }
 
 // ------------------------------------------------------------------ a4/a8
-// Row-tile passes over the CTA's rows: each thread owns N consecutive rows
-// (one 16-byte vector) of a 512·N-row tile and streams the tile's V columns
-// with independent vector loads (all j in flight):
-//   MODE 1: colacc_i += Σ_r V_ri w_r                       (CGS pass, line 161)
-//   MODE 2: w ← RN_W(w − Σ_i V_i c_i), then colacc += Vᵀw   (line 162 + next line 161;
-//           the second read of the tile's V is served by L2)
+// Row-tile passes over the CTA's rows with the V tile (and, for MODE 1–3, the
+// w tile) staged in shared memory by TMA bulk copies, one per column segment,
+// double buffered on mbar_t: a tile is T rows × ncols columns, T chosen so a
+// buffer fills half the staging region; each pass reads V once from HBM.
+//   MODE 1: acc_i += Σ_r V_ri w_r                          (CGS pass, line 161)
+//   MODE 2: w ← RN_W(w − Σ_i V_i c_i), then acc_i += Vᵀw   (line 162 + the next line 161)
 //   MODE 3: w ← RN_W(w − Σ_i V_i c_i), nn += ‖w‖²          (line 162 + line 104)
 //   MODE 4: x_r += Σ_i (double)V_ri · y_i                   (lines 145–147, fp64)
-// V·c is summed in W with i ascending (reading R2/R9); dots in fp64, reduced
-// per warp (shuffle tree) into s_wcol[warp][i] in tile order: deterministic.
+// V·c is summed in W per row with i ascending (reading R2/R9).  Dots: warp w
+// owns a fixed share of every tile's rows and lane l the columns l, l+32, …;
+// each lane accumulates dotv partials in fp64 registers over all tiles, and
+// the per-warp column partials (s_acc[warp][i]) are summed over the warps in
+// order by combine_acc: deterministic, no per-tile shuffles.  Column segments
+// sit TP = T + 16/w_B elements apart so that the lanes' 16-byte reads of one
+// row group hit distinct banks.
+constexpr int MAXSLOT = (MAX_M + 1 + 31) / 32;  // columns per lane
 template <class W, int MODE>
-__device__ __noinline__ double rowtile_pass_impl(int n, double* __restrict__ xg, int kmax, int r0, int r1,
-                                                 const W* __restrict__ V, long long ldv, int ncols,
-                                                 W* __restrict__ w, const W* s_coefW, const double* s_y,
-                                                 double* s_acc, typename VecT<W>::T* s_wt) {
+__device__ __forceinline__ void rowtile_pass(const Dev& d, Shm& sh, int r0, int r1, const W* V, long long ldv,
+                                             int ncols, W* w, const W* s_coefW, const double* s_y, double* s_acc,
+                                             char* s_tiles, double& nn) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
-  constexpr int HALF = NT / 2;  // vectors per dot work item (ITEMS == 2)
-  double nn = 0.0;
+  constexpr int NTB = 2;  // ring depth (3 was slower on C2: more, smaller bulk copies)
+  constexpr int NWS = MODE == 4 ? 0 : 1;  // w tile staged (MODE 1-3)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q0 = r0 / N, q1 = r1 / N;
-  if (MODE == 1 || MODE == 2) {
-    for (int i = threadIdx.x; i < 2 * ncols; i += NT) s_acc[i] = 0.0;
+  const int nrows = r1 - r0;  // multiple of ROWALIGN
+  double dacc[MAXSLOT];
+#pragma unroll
+  for (int t = 0; t < MAXSLOT; ++t) dacc[t] = 0.0;
+  const int half = (d.tile_bytes / NTB) & ~127;
+  constexpr int PADE = 16 / (int)sizeof(W);
+  // tile geometry: element (tile row t, column i) at (t >> lg)·bsz + i·cs + (t & msk)
+  int T, cs, lg, msk, bsz, woff;
+  if (d.vtb) {  // row-blocked V: whole blocks per tile, one copy per block
+    const int nbt = max(1, half / ((ncols * d.vtp + d.vtb) * (int)sizeof(W)));
+    T = min(nbt * d.vtb, nrows);
+    cs = d.vtp; lg = d.vtb_log; msk = d.vtb - 1; bsz = ncols * d.vtp;
+    woff = nbt * bsz;
+  } else {      // column-major V: one copy per column segment
+    T = (half / ((ncols + 1) * (int)sizeof(W)) - PADE) & ~(ROWALIGN - 1);
+    T = max(ROWALIGN, min(T, nrows));
+    cs = T + PADE; lg = 30; msk = (1 << 30) - 1; bsz = 0;
+    woff = ncols * cs;
   }
-  for (int qb = q0; qb < q1; qb += NT) {
-    const int q = qb + threadIdx.x;
-    const bool act = q < q1;
-    V4 wv;
-    W* pw = reinterpret_cast<W*>(&wv);
-#pragma unroll
-    for (int t = 0; t < N; ++t) pw[t] = (W)0;
-    if (MODE != 4 && act) wv = reinterpret_cast<const V4*>(w)[q];
-    if (MODE == 2 || MODE == 3 || MODE == 4) {
-      // step a: thread-per-vector sweep over all ncols columns (all loads in flight)
-      W acc[N];
-      double u[N];
-#pragma unroll
-      for (int t = 0; t < N; ++t) { acc[t] = (W)0; u[t] = 0.0; }
-      if (act) {
-#pragma unroll 8
-        for (int i = 0; i < ncols; ++i) {
-          const V4 v = __ldcg(reinterpret_cast<const V4*>(V + (long long)i * ldv) + q);
-          const W* pv = reinterpret_cast<const W*>(&v);
-          if (MODE == 4) {
-            const double yi = s_y[i];
-#pragma unroll
-            for (int t = 0; t < N; ++t) u[t] = __dadd_rn(u[t], __dmul_rn((double)pv[t], yi));
-          } else {
-            const W ci = s_coefW[i];
-#pragma unroll
-            for (int t = 0; t < N; ++t) acc[t] = addw(acc[t], mulw(pv[t], ci));
-          }
-        }
+  auto el = [&](int t, int i) { return (size_t)(t >> lg) * bsz + (size_t)i * cs + (t & msk); };
+  const int ntile = nrows > 0 ? (nrows + T - 1) / T : 0;
+  unsigned ph = sh.tphase;
+  auto buf = [&](int b) { return reinterpret_cast<W*>(s_tiles + (size_t)b * half); };
+  // w rows of the tile are staged too (MODE 1-3); every generic store of w of
+  // this CTA is followed by fence.proxy.async (csr_stream, this pass)
+  auto issue = [&](int k) {  // warp 0
+    const int rows = min(T, nrows - k * T);
+    const long long row0 = r0 + (long long)k * T;
+    const unsigned bytes = (unsigned)rows * (unsigned)sizeof(W);
+    W* dst = buf(k % NTB);
+    unsigned long long* bar = &sh.mbar_t[k % NTB];
+    if (d.vtb) {
+      const int nb = rows >> lg;  // CTA row ranges are block aligned
+      const unsigned bb = (unsigned)(ncols * d.vtp) * (unsigned)sizeof(W);
+      if (lane == 0) mbar_expect_tx(bar, bb * (unsigned)nb + (NWS ? bytes : 0u));
+      __syncwarp();
+      for (int b = lane; b < nb; b += 32) tma_load_1d(dst + (size_t)b * bsz, V + ((row0 >> lg) + b) * d.vbs, bb, bar);
+      if (NWS && lane == 31) tma_load_1d(dst + woff, w + row0, bytes, bar);
+    } else {
+      if (lane == 0) mbar_expect_tx(bar, bytes * (unsigned)(ncols + NWS));
+      __syncwarp();
+      for (int i = lane; i < ncols + NWS; i += 32)
+        tma_load_1d(i < ncols ? dst + (size_t)i * cs : dst + woff, (i < ncols ? V + (long long)i * ldv : w) + row0, bytes,
+                    bar);
+    }
+  };
+  if (warp == 0)
+    for (int k = 0; k < NTB - 1 && k < ntile; ++k) issue(k);
+  for (int k = 0; k < ntile; ++k) {
+    const int b = k % NTB;
+    // the buffer of tile k−1 is free (barrier at the end of its iteration)
+    if (warp == 0 && k + NTB - 1 < ntile) issue(k + NTB - 1);
+    {
+      const unsigned par = (ph >> b) & 1u;
+      ph ^= (1u << b);
+      if (!mbar_try_wait(&sh.mbar_t[b], par)) {
+        const unsigned long long t0 = globaltimer();
+        while (!mbar_try_wait(&sh.mbar_t[b], par))
+          if ((long long)(globaltimer() - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); break; }
+      }
+    }
+    const int rows = min(T, nrows - k * T);
+    const int row0 = r0 + k * T;
+    const W* VT = buf(b);
+    W* s_w = buf(b) + woff;
+    // step a: one thread per 16-byte row group (N rows: N independent chains,
+    // one shared load per column)
+    if (MODE != 1) {
+      for (int g = threadIdx.x; g < rows / N; g += NT) {
+        const int t = g * N;
         if (MODE == 4) {
+          double u[N];
 #pragma unroll
-          for (int t = 0; t < N; ++t) {
-            const int row = q * N + t;
-            if (row < n) xg[row] = xg[row] + u[t];
+          for (int r = 0; r < N; ++r) u[r] = 0.0;
+#pragma unroll 4
+          for (int i = 0; i < ncols; ++i) {
+            const double yi = s_y[i];
+            const V4 v = *reinterpret_cast<const V4*>(VT + el(t, i));
+            const W* pv = reinterpret_cast<const W*>(&v);
+#pragma unroll
+            for (int r = 0; r < N; ++r) u[r] = __dadd_rn(u[r], __dmul_rn((double)pv[r], yi));
           }
-        } else {
 #pragma unroll
-          for (int t = 0; t < N; ++t) pw[t] = subw(pw[t], acc[t]);
-          reinterpret_cast<V4*>(w)[q] = wv;
+          for (int r = 0; r < N; ++r)
+            if (row0 + t + r < d.n) d.x[row0 + t + r] = d.x[row0 + t + r] + u[r];
+        } else {
+          W acc[N];
+#pragma unroll
+          for (int r = 0; r < N; ++r) acc[r] = (W)0;
+#pragma unroll 4
+          for (int i = 0; i < ncols; ++i) {
+            const W ci = s_coefW[i];
+            const V4 v = *reinterpret_cast<const V4*>(VT + el(t, i));
+            const W* pv = reinterpret_cast<const W*>(&v);
+#pragma unroll
+            for (int r = 0; r < N; ++r) acc[r] = addw(acc[r], mulw(pv[r], ci));
+          }
+          V4 wv = *reinterpret_cast<const V4*>(s_w + t);
+          W* pw = reinterpret_cast<W*>(&wv);
+#pragma unroll
+          for (int r = 0; r < N; ++r) pw[r] = subw(pw[r], acc[r]);
+          *reinterpret_cast<V4*>(w + row0 + t) = wv;
+          if (MODE == 2) *reinterpret_cast<V4*>(s_w + t) = wv;
           if (MODE == 3) nn += dotv(wv, wv);
         }
       }
     }
     if (MODE == 1 || MODE == 2) {
-      // step b: column dots over the tile; work item = (column, half tile),
-      // item it owned by warp it % NW in every tile (fixed accumulation order)
-      s_wt[threadIdx.x] = wv;
-      __syncthreads();
-        for (int it = warp; it < 2 * ncols; it += NW) {
-          const int col = it >> 1, h0 = (it & 1) * HALF;
-          const V4* vc = reinterpret_cast<const V4*>(V + (long long)col * ldv) + qb + h0;
-          const int lim = min(HALF, q1 - (qb + h0));
-          double p = 0.0;
-#pragma unroll 8
-          for (int k = lane; k < HALF; k += 32) {
-            if (k < lim) {
-              const V4 v = __ldcg(vc + k);
-              p += dotv(v, s_wt[h0 + k]);
-            }
+      if (MODE == 2) __syncthreads();  // s_w complete
+      const int nq = rows / N;
+      const int qa = (warp * nq) / NW, qb = ((warp + 1) * nq) / NW;
+      const V4* wq = reinterpret_cast<const V4*>(s_w);
+#pragma unroll
+      for (int sl = 0; sl < MAXSLOT; ++sl) {
+        const int i = lane + 32 * sl;
+        if (32 * sl < ncols && i < ncols) {
+          // four independent accumulators (fixed structure: deterministic)
+          double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+          int q = qa;
+          for (; q + 3 < qb; q += 4) {
+            p0 += dotv(*reinterpret_cast<const V4*>(VT + el(q * N, i)), wq[q]);
+            p1 += dotv(*reinterpret_cast<const V4*>(VT + el((q + 1) * N, i)), wq[q + 1]);
+            p2 += dotv(*reinterpret_cast<const V4*>(VT + el((q + 2) * N, i)), wq[q + 2]);
+            p3 += dotv(*reinterpret_cast<const V4*>(VT + el((q + 3) * N, i)), wq[q + 3]);
           }
-          p = warp_sum(p);
-          if (lane == 0) s_acc[it] += p;
+          for (; q < qb; ++q) p0 += dotv(*reinterpret_cast<const V4*>(VT + el(q * N, i)), wq[q]);
+          dacc[sl] += (p0 + p1) + (p2 + p3);
         }
-      __syncthreads();
+      }
+    }
+    __syncthreads();  // buffer b free
+  }
+  if (MODE == 1 || MODE == 2) {
+#pragma unroll
+    for (int sl = 0; sl < MAXSLOT; ++sl) {
+      const int i = lane + 32 * sl;
+      if (i < ncols) s_acc[warp * d.kmax + i] = dacc[sl];
     }
   }
-  return nn;
-}
-
-template <class W, int MODE>
-__device__ __forceinline__ void rowtile_pass(const Dev& d, int r0, int r1, const W* V, long long ldv, int ncols, W* w,
-                                             const W* s_coefW, const double* s_y, double* s_acc, char* s_tiles,
-                                             double& nn) {
-  nn += rowtile_pass_impl<W, MODE>(d.n, d.x, d.kmax, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_acc,
-                                   reinterpret_cast<typename VecT<W>::T*>(s_tiles));
-}
-
-// (column, half-tile) accumulators → per-CTA column partials, fixed order
-__device__ __forceinline__ void combine_acc(const Dev& d, const double* s_acc, int ncols, double* s_part) {
+  if (threadIdx.x == 0) sh.tphase = ph;  // every thread read it at entry, before the barriers above
+  if (MODE == 2 || MODE == 3) fence_proxy_async_global();  // w is staged by TMA in the next pass
   __syncthreads();
-  for (int i = threadIdx.x; i < ncols; i += NT) s_part[i] = s_acc[2 * i] + s_acc[2 * i + 1];
+}
+
+// per-CTA column partials for the all-reduce: warps in order
+__device__ __forceinline__ void combine_acc(const Dev& d, const double* s_acc, int ncols, double* s_part) {
+  for (int i = threadIdx.x; i < ncols; i += NT) {
+    double v = 0.0;
+    for (int w = 0; w < NW; ++w) v += s_acc[w * d.kmax + i];
+    s_part[i] = v;
+  }
   __syncthreads();
 }
 
@@ -1093,7 +1188,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
       if (lead) { const unsigned long long t = globaltimer(); d.prof[8 + slot] += t - tp; tp = t; }
     }
   };
-  rowtile_pass<W, 1>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  rowtile_pass<W, 1>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
   combine_acc(d, s_tmp, j, s_part);
   sub(0);
   if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp, false)) return false;
@@ -1103,7 +1198,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
     s_coefW[i] = RN<W>(s_out[i]);
   }
   __syncthreads();
-  rowtile_pass<W, 2>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  rowtile_pass<W, 2>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
   combine_acc(d, s_tmp, j, s_part);
   sub(2);
   if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp, false)) return false;
@@ -1114,7 +1209,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   }
   __syncthreads();
   nn = 0.0;
-  rowtile_pass<W, 3>(d, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  rowtile_pass<W, 3>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
   sub(4);
   if (!allreduce1(d, sh, nn, true, NN)) return false;
   sub(5);
@@ -1183,7 +1278,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     for (int j = 1; j <= d.m; ++j) {
       // ------------ w = M⁻¹ A v_j, v_j (own rows) → V   (lines 100, 105)
       const unsigned long long ts0 = d.profile && threadIdx.x == 0 ? globaltimer() : 0ull;
-      spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V + (long long)(j - 1) * ldv);
+      spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V, j - 1);
       if (d.profile) {
         if (threadIdx.x == 0) d.prof_cta[blockIdx.x] += globaltimer() - ts0;
         if (!grid_sync(d, sh)) { fail = true; break; }
@@ -1225,7 +1320,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     for (int i = threadIdx.x; i < J; i += NT) s_y[i] = __ldcg(d.y + i);
     __syncthreads();
     double dummy = 0.0;
-    rowtile_pass<W, 4>(d, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
+    rowtile_pass<W, 4>(d, sh, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     tick(PH_UPDATE);
     ++k;
@@ -1245,6 +1340,19 @@ __global__ void cast32_kernel(const double* __restrict__ a, float* __restrict__ 
     const double v = a[e];
     if (isfinite(v) && fabs(v) > (double)FLT_MAX) atomicOr(err, ERRF_RANGE);
     o[e] = __double2float_rn(v);
+  }
+}
+
+// column-major V (ncols columns, leading dimension ldv, rows ≥ nvalid read
+// as 0) → row-blocked layout (Dev::vtb); component entry points only
+template <class W>
+__global__ void pack_vblocked_kernel(const W* __restrict__ src, long long ldv, int ncols, long long nrows,
+                                     long long nvalid, W* __restrict__ dst, int tb, int tp, long long bs) {
+  const long long tot = nrows * ncols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / nrows);
+    const long long r = e - (long long)c * nrows;
+    dst[(r / tb) * bs + (long long)c * tp + (r % tb)] = r < nvalid ? src[(long long)c * ldv + r] : (W)0;
   }
 }
 
@@ -1272,7 +1380,7 @@ __global__ void dinv_kernel(int n, const int* __restrict__ rp, const int* __rest
 template <class W, int L>
 __global__ void __launch_bounds__(NT, 1) k_spmv_kernel(Dev d, const W* v, W* w) {
   G200_SMEM_CARVE(W)
-  spmv_phase<W, L>(d, sh, s_tiles, v, 1.0, w, nullptr);
+  spmv_phase<W, L>(d, sh, s_tiles, v, 1.0, w, (W*)nullptr, 0);
 }
 
 template <class W, int L>
@@ -1306,7 +1414,7 @@ __global__ void __launch_bounds__(NT, 1) k_xupdate_kernel(Dev d, int J, const W*
   __syncthreads();
   const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
   double dummy = 0.0;
-  rowtile_pass<W, 4>(d, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
+  rowtile_pass<W, 4>(d, sh, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
 }
 
 // Device microbenchmark of the solve's building blocks (dev tool): `iters`
@@ -1340,17 +1448,17 @@ __global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int ite
       auto epi = [&](int row, W a, W di, W) { w[row] = mulw(di, a); };
       csr_stream<W, 1>(d, sh, s_tiles, (const W*)d.aW, dinv, gat, pre, epi);
     } else if (what == 7) {  // full SpMV phase (gathers from V column 0), L = 1
-      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, nullptr);
+      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, (W*)nullptr, 0);
     } else if (what == 8) {  // ... plus the fused V-column write (as in the solve)
-      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, const_cast<W*>(V) + 2 * ldv);
+      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, const_cast<W*>(V), 2);
     } else if (what == 3) {
-      rowtile_pass<W, 1>(d, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
+      rowtile_pass<W, 1>(d, sh, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
       __syncthreads();
     } else if (what == 4) {
-      rowtile_pass<W, 2>(d, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
+      rowtile_pass<W, 2>(d, sh, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
       __syncthreads();
     } else {
-      rowtile_pass<W, 3>(d, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
+      rowtile_pass<W, 3>(d, sh, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
       __syncthreads();
     }
   }

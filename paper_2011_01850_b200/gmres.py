@@ -75,7 +75,7 @@ def load_library():
     L.gmres_k_spmv.argtypes = [vp, i32, vp, vp]
     L.gmres_k_resid.argtypes = [vp, i32, vp, vp, vp, vp]
     L.gmres_k_ortho.argtypes = [vp, i32, i32, i32, vp, i64, vp, vp]
-    L.gmres_k_xupdate.argtypes = [vp, i32, i32, vp, i64, vp, vp]
+    L.gmres_k_xupdate.argtypes = [vp, i32, i32, vp, i64, vp, vp, i32]
     L.gmres_k_hessenberg.argtypes = [vp, i32, i32, vp, dbl, vp, vp, vp]
     L.gmres_k_cast32.argtypes = [vp]
     L.gmres_k_micro.argtypes = [vp, i32, i32, i32, i32, vp, i64, vp, vp]
@@ -108,8 +108,8 @@ def _ortho(o) -> int:
 
 
 def ld_for(n: int) -> int:
-    """Leading dimension the component entry points require for V (n rounded to 64)."""
-    return (n + 63) // 64 * 64
+    """Leading dimension the component entry points require for V (n rounded to 256)."""
+    return (n + 255) // 256 * 256
 
 
 @dataclass
@@ -262,9 +262,10 @@ class Solver:
                                          _p(h)))
         return h
 
-    def k_xupdate(self, precision, J, V, ldv, y, x):
+    def k_xupdate(self, precision, J, V, ldv, y, x, blocked=False):
         y = np.ascontiguousarray(y, np.float64)
-        self._ck(self._lib.gmres_k_xupdate(self._h, _prec(precision), int(J), _p(V), int(ldv), _p(y), _p(x)))
+        self._ck(self._lib.gmres_k_xupdate(self._h, _prec(precision), int(J), _p(V), int(ldv), _p(y), _p(x),
+                                           int(bool(blocked))))
 
     def k_micro(self, precision, what, iters, ncols, V, ldv, w):
         ns = np.zeros(1)

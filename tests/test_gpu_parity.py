@@ -128,8 +128,9 @@ def test_ortho_parity(mat, prec, ortho, j):
 
 
 # ------------------------------------------------------------------ a8 update
+@pytest.mark.parametrize("blocked", [False, True])
 @pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
-def test_xupdate_parity(mat, prec):
+def test_xupdate_parity(mat, prec, blocked):
     name, A, S = mat
     n = A.n
     ld = G.ld_for(n)
@@ -142,7 +143,7 @@ def test_xupdate_parity(mat, prec):
     Vpad = np.zeros((J, ld), wdt(prec))
     Vpad[:, :n] = V.T
     xd = tdev(x)
-    S.k_xupdate(prec, J, tdev(Vpad), ld, y, xd)
+    S.k_xupdate(prec, J, tdev(Vpad), ld, y, xd, blocked=blocked)
     assert np.allclose(xd.cpu().numpy(), x_o, rtol=1e-14, atol=1e-14 * np.abs(x_o).max())
 
 
