@@ -104,6 +104,56 @@ int gmres_get_cycle_iters(gmres_ctx* ctx, int32_t* buf, int32_t cap, int32_t* le
  * over CTAs of the CTA's own SpMV time.  Returns the count written. */
 int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap);
 
+/* ------------------------------------------------------------------------
+ * Row-partitioned solve over P ranks (the paper's future work,
+ * PAPER.md:491-495).  Rank q owns the contiguous global rows
+ * [row_begin_q, row_begin_q + n_q) of A, b and x; CSR rows are local, column
+ * indices GLOBAL.  Every rank runs the same restarted solve: the Gram–Schmidt
+ * dots and norms are all-reduced over all ranks' CTAs inside the persistent
+ * kernel (each CTA pushes its partials to every rank and arrives on every
+ * rank's counter), and the rows of the Krylov vector / residual / x a peer
+ * gathers in its SpMV are pushed into the peer's copy by the owning CTA
+ * (peer stores) before that all-reduce publishes them.  All ranks take
+ * bit-identical control decisions (same sums in the same order).
+ * ---------------------------------------------------------------------- */
+
+/* Host-only planning helpers (no device is touched; usable on any host):
+ * gmres_dist_partition: boundaries bounds[0..nranks] (bounds[0] = 0,
+ *   bounds[nranks] = n) of a split of the n rows of a global CSR (row_ptr) at
+ *   multiples of `align`, balancing rows + nonzeros.
+ * gmres_dist_ghosts: the sorted unique global columns of a rank's local rows
+ *   (row_ptr/col, n_local rows starting at global row row_begin) outside
+ *   those rows; *count = their number, at most cap written.
+ * gmres_dist_sends: the local rows of rank [row_begin, row_begin + n_local)
+ *   that appear in a peer's ghost list (i.e. what this rank pushes to it). */
+int gmres_dist_partition(const int32_t* row_ptr, int64_t n, int32_t nranks, int64_t align, int64_t* bounds);
+int gmres_dist_ghosts(const int32_t* row_ptr, const int32_t* col, int64_t n_local, int64_t row_begin, int32_t* ghosts,
+                      int64_t cap, int64_t* count);
+int gmres_dist_sends(int64_t row_begin, int64_t n_local, const int32_t* peer_ghosts, int64_t n_peer_ghosts,
+                     int32_t* rows, int64_t cap, int64_t* count);
+
+/* One rank's share of the matrix (host arrays, copied): n_local rows from
+ * global row row_begin (a multiple of 256; n_local a multiple of 256 unless
+ * the block ends at n_global), 2 ≤ nranks ≤ 8.  Errors as gmres_create. */
+int gmres_create_dist(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n_global,
+                      int64_t row_begin, int64_t n_local, int32_t nranks, int32_t rank, gmres_ctx** out);
+/* One process per GPU: export this rank's blob (ghost list + CUDA IPC
+ * handles of its exchange buffers; *len = size, blob may be NULL to query),
+ * all-gather the blobs (e.g. torch.distributed), then import all of them
+ * (offsets[q] = start of rank q's blob, offsets[nranks] = total).  Afterwards
+ * gmres_solve_device is collective: every rank calls it with the same m,
+ * tol, ortho, precision and options and its own local b, x0, x. */
+int gmres_dist_export(gmres_ctx* ctx, void* blob, int64_t cap, int64_t* len);
+int gmres_dist_import(gmres_ctx* ctx, const void* blobs, const int64_t* offsets);
+/* Several ranks in one process on ONE device ("virtual ranks", 2 ≤ P ≤ 4):
+ * link them (peer buffers are the other contexts' allocations) and solve
+ * them in one cooperative launch (sms/P CTAs per rank) — the same kernel
+ * code as the multi-GPU path.  res[P] receives every rank's result. */
+int gmres_dist_link_local(gmres_ctx* const* ctxs, int32_t nranks);
+int gmres_solve_virtual(gmres_ctx* const* ctxs, int32_t nranks, const double* const* d_b, const double* const* d_x0,
+                        double* const* d_x, int32_t m, double tol, int32_t ortho, int32_t precision,
+                        const gmres_opts* opts, gmres_result* res);
+
 const char* gmres_last_error(const gmres_ctx* ctx);  /* "" if none; ctx may be NULL */
 void gmres_destroy(gmres_ctx* ctx);
 

@@ -68,6 +68,28 @@ struct gmres_ctx {
   std::vector<int32_t> cycJ_host;
   double phase_ns[PH_N] = {0};
   std::string err;
+  // ---- row partition over ranks (gmres_create_dist)
+  int nranks = 1, rank = 0;
+  int64_t n_global = 0, row_begin = 0;  // this rank owns global rows [row_begin, row_begin + n)
+  int64_t nvec_global = 0;
+  std::vector<int32_t> ghosts;          // sorted global columns of the local rows outside them
+  void* d_gw0 = nullptr;                // full-length (global) work vectors, 8 bytes per row
+  void* d_gw1 = nullptr;
+  double* d_gx = nullptr;               // full-length x
+  double* d_dslots = nullptr;           // all-reduce partials [2][nranks·sms][KST_MAX]
+  unsigned long long* d_dctr = nullptr; // arrival counter (monotonic across launches)
+  unsigned long long* d_epoch = nullptr;  // [2] barrier epochs / all-reduces at the end of the last launch
+  unsigned long long epoch_base = 0;
+  int red_base = 0;
+  bool linked = false, ipc = false;
+  void* peer_w0[MAXR] = {}, *peer_w1[MAXR] = {};
+  double* peer_x[MAXR] = {};
+  double* peer_slots[MAXR] = {};
+  unsigned long long* peer_ctr[MAXR] = {};
+  std::vector<std::vector<int32_t>> send_rows;  // per peer: local rows it gathers (sorted)
+  int* d_send = nullptr;                // [G+1] offsets, rows, peers (rebuilt with the partition)
+  int send_G = -1, send_align = -1;
+  bool dist() const { return nranks > 1; }
 };
 
 namespace {
@@ -90,6 +112,7 @@ int fail(gmres_ctx* c, int code, const std::string& msg) {
   } while (0)
 
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+constexpr int KST_MAX = (MAX_M + 1 + 8 + 3) & ~3;  // k stride bound of the all-reduce partials
 
 // lanes per row in the CSR stream: one thread per row when a 512-row chunk of
 // average rows fits the stage (stencils), else the power of two that keeps
@@ -145,8 +168,15 @@ VLayout vlayout_for(int ortho, int m, int wb, int tile_bytes) {
   return L;
 }
 
+void set_vlayout(Dev& d, const VLayout& vl) {
+  d.vtb = vl.tb;
+  d.vtp = vl.tp;
+  d.vtb_log = vl.lg;
+  d.vbs = vl.bs;
+}
+
 template <class W, int L>
-void* solve_kernel_ptr() { return (void*)&solve_kernel<W, L>; }
+void* solve_kernel_ptr() { return (void*)&solve_kernel<W, L, false>; }
 
 void* pick_solve(int prec, int L) {
   if (prec == GMRES_MIXED) {
@@ -167,6 +197,12 @@ void* pick_solve(int prec, int L) {
     case 16: return solve_kernel_ptr<double, 16>();
     default: return solve_kernel_ptr<double, 32>();
   }
+}
+
+// virtual-rank launches (several row blocks on one device): L ∈ {1, 4}
+void* pick_solve_virtual(int prec, int L) {
+  if (prec == GMRES_MIXED) return L == 1 ? (void*)&solve_kernel<float, 1, true> : (void*)&solve_kernel<float, 4, true>;
+  return L == 1 ? (void*)&solve_kernel<double, 1, true> : (void*)&solve_kernel<double, 4, true>;
 }
 
 template <class W>
@@ -201,7 +237,7 @@ void* pick_kernel(int prec, int kind, int L) {
 
 // stride of the per-CTA partial sums: m+1 Gram-Schmidt coefficients, and at
 // least the 3 values of the residual reduction
-int kmax_for(int m) { return std::max(m + 1, 4); }
+int kmax_for(int m) { return std::max(m + 1, 8); }
 
 // shared staging region: two CSR chunk stages, or two V tiles of ≥ 32 rows
 int tile_bytes_for(int m) { return std::max(TILE_BYTES, 2 * (m + 2) * ROWALIGN * 8); }
@@ -295,6 +331,29 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
   CK(cudaMemcpy(ctx->d_chunk_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
   ctx->part_G = G;
   ctx->part_align = align;
+  if (ctx->dist() && ctx->linked) {  // per-CTA send lists (halo push)
+    std::vector<std::pair<int, int>> ent;  // (local row, peer)
+    for (int q = 0; q < ctx->nranks; ++q)
+      for (int32_t r : ctx->send_rows[q]) ent.push_back({r, q});
+    std::sort(ent.begin(), ent.end());
+    std::vector<int> buf(G + 1 + 2 * ent.size());
+    // offsets: CTA g pushes the entries with rb[g] <= row < rb[g+1]
+    for (int g = 0; g <= G; ++g) {
+      const int lo = g == G ? (int)ent.size()
+                            : (int)(std::lower_bound(ent.begin(), ent.end(), std::make_pair(rb[g], -1)) - ent.begin());
+      buf[g] = lo;
+    }
+    for (size_t i = 0; i < ent.size(); ++i) {
+      buf[G + 1 + i] = ent[i].first;
+      buf[G + 1 + ent.size() + i] = ent[i].second;
+    }
+    cudaFree(ctx->d_send);
+    ctx->d_send = nullptr;
+    CK(cudaMalloc(&ctx->d_send, sizeof(int) * std::max<size_t>(buf.size(), 1)));
+    CK(cudaMemcpy(ctx->d_send, buf.data(), sizeof(int) * buf.size(), cudaMemcpyHostToDevice));
+    ctx->send_G = G;
+    ctx->send_align = align;
+  }
   return 0;
 }
 
@@ -431,6 +490,10 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.out_dbl = ctx->d_out_dbl;
   d.prof = ctx->d_prof;
   d.prof_cta = ctx->d_prof_cta;
+  d.row_base = 0;
+  d.halo = 0;
+  for (int q = 0; q < MAXR; ++q) { d.vec_peer[0][q] = ctx->d_w0; d.vec_peer[1][q] = ctx->d_w1; d.vec_peer[2][q] = nullptr; }
+  d.send_off = d.send_row = d.send_peer = nullptr;
   d.timeout_ns = 20ll * 1000 * 1000 * 1000;
   return d;
 }
@@ -457,23 +520,27 @@ extern "C" {
 
 const char* gmres_last_error(const gmres_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
-int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n, int64_t nnz,
-                 gmres_ctx** out) {
+namespace {
+// n rows of a (possibly row-partitioned) matrix: global rows [row_begin,
+// row_begin + n) of an n_global × n_global matrix, CSR with global columns.
+int create_impl(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n, int64_t nnz, int64_t n_global,
+                int64_t row_begin, int nranks, int rank, gmres_ctx** out) {
   gmres_ctx* ctx = nullptr;
   if (!out) return fail(nullptr, GMRES_EINVAL, "out is NULL");
   *out = nullptr;
   if (!row_ptr || (!col && nnz > 0) || (!val && nnz > 0)) return fail(nullptr, GMRES_EINVAL, "null CSR array");
-  if (n < 1 || nnz < 0 || n > 2000000000LL || nnz > 2147483647LL) return fail(nullptr, GMRES_EINVAL, "bad n/nnz");
+  if (n < 1 || nnz < 0 || n_global > 2000000000LL || nnz > 2147483647LL) return fail(nullptr, GMRES_EINVAL, "bad n/nnz");
+  if (row_begin < 0 || row_begin + n > n_global) return fail(nullptr, GMRES_EINVAL, "rows outside [0, n_global)");
   // CSR invariants
   if (row_ptr[0] != 0 || row_ptr[n] != nnz) return fail(nullptr, GMRES_EBADCSR, "row_ptr[0] != 0 or row_ptr[n] != nnz");
   for (int64_t i = 0; i < n; ++i) {
     if (row_ptr[i + 1] < row_ptr[i])
-      return fail(nullptr, GMRES_EBADCSR, "row_ptr decreases at row " + std::to_string(i));
+      return fail(nullptr, GMRES_EBADCSR, "row_ptr decreases at row " + std::to_string(row_begin + i));
     for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-      if (col[e] < 0 || col[e] >= n)
-        return fail(nullptr, GMRES_EBADCSR, "column out of range in row " + std::to_string(i));
+      if (col[e] < 0 || col[e] >= n_global)
+        return fail(nullptr, GMRES_EBADCSR, "column out of range in row " + std::to_string(row_begin + i));
       if (e > row_ptr[i] && col[e] <= col[e - 1])
-        return fail(nullptr, GMRES_EBADCSR, "columns not strictly increasing in row " + std::to_string(i));
+        return fail(nullptr, GMRES_EBADCSR, "columns not strictly increasing in row " + std::to_string(row_begin + i));
     }
   }
   ctx = new gmres_ctx();
@@ -487,6 +554,11 @@ int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, 
   ctx->nvec = round_up(n, VEC_ALIGN);
   ctx->ldv = ctx->nvec;
   ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ctx->n_global = n_global;
+  ctx->row_begin = row_begin;
+  ctx->nvec_global = round_up(n_global, VEC_ALIGN);
   int rc;
   auto setup = [&]() -> int {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
@@ -503,6 +575,8 @@ int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, 
     CK(cudaMemset(ctx->d_a64, 0, sizeof(double) * (nnz + ARR_PAD)));
     CK(cudaMalloc(&ctx->d_dinv64, sizeof(double) * ctx->nvec));
     CK(cudaMalloc(&ctx->d_dinv32, sizeof(float) * ctx->nvec));
+    CK(cudaMemset(ctx->d_dinv64, 0, sizeof(double) * ctx->nvec));
+    CK(cudaMemset(ctx->d_dinv32, 0, sizeof(float) * ctx->nvec));
     CK(cudaMemcpy(ctx->d_rp, row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
     if (nnz > 0) {
       CK(cudaMemcpy(ctx->d_ci, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
@@ -513,19 +587,46 @@ int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, 
     const int big = 0x7fffffff;
     CK(cudaMemcpy(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice));
     dinv_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>((int)n, ctx->d_rp, ctx->d_ci, ctx->d_a64, ctx->d_dinv64,
-                                                      ctx->d_dinv32, d_bad);
+                                                      ctx->d_dinv32, d_bad, (long long)row_begin);
     CK(cudaGetLastError());
     int bad = big;
     CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     cudaFree(d_bad);
-    if (bad != big) return fail(ctx, GMRES_EZERODIAG, "zero or missing diagonal at row " + std::to_string(bad));
+    if (bad != big)
+      return fail(ctx, GMRES_EZERODIAG, "zero or missing diagonal at row " + std::to_string(row_begin + bad));
+    if (nranks > 1) {
+      // ghost columns (host) and the buffers peers push into / read from
+      for (int64_t i = 0; i < nnz; ++i)
+        if (col[i] < row_begin || col[i] >= row_begin + n) ctx->ghosts.push_back(col[i]);
+      std::sort(ctx->ghosts.begin(), ctx->ghosts.end());
+      ctx->ghosts.erase(std::unique(ctx->ghosts.begin(), ctx->ghosts.end()), ctx->ghosts.end());
+      const size_t gb = sizeof(double) * ctx->nvec_global;
+      CK(cudaMalloc(&ctx->d_gw0, gb));
+      CK(cudaMalloc(&ctx->d_gw1, gb));
+      CK(cudaMalloc(&ctx->d_gx, gb));
+      CK(cudaMemset(ctx->d_gw0, 0, gb));
+      CK(cudaMemset(ctx->d_gw1, 0, gb));
+      CK(cudaMemset(ctx->d_gx, 0, gb));
+      const size_t sb = sizeof(double) * 2 * (size_t)nranks * ctx->sms * KST_MAX;
+      CK(cudaMalloc(&ctx->d_dslots, sb));
+      CK(cudaMalloc(&ctx->d_dctr, 256));
+      CK(cudaMemset(ctx->d_dctr, 0, 256));
+      CK(cudaMalloc(&ctx->d_epoch, sizeof(unsigned long long) * 2));
+      CK(cudaMemset(ctx->d_epoch, 0, sizeof(unsigned long long) * 2));
+    }
     return 0;
   };
   rc = setup();
   if (rc != 0) { g_err = ctx->err; return bail(rc); }
   *out = ctx;
   return GMRES_OK;
+}
+}  // namespace
+
+int gmres_create(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n, int64_t nnz,
+                 gmres_ctx** out) {
+  return create_impl(row_ptr, col, val, n, nnz, n, 0, 1, 0, out);
 }
 
 void gmres_destroy(gmres_ctx* ctx) {
@@ -543,6 +644,23 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_row_begin);
   cudaFree(ctx->d_chunks);
   cudaFree(ctx->d_chunk_off);
+  if (ctx->ipc) {
+    for (int q = 0; q < ctx->nranks; ++q) {
+      if (q == ctx->rank) continue;
+      if (ctx->peer_w0[q]) cudaIpcCloseMemHandle(ctx->peer_w0[q]);
+      if (ctx->peer_w1[q]) cudaIpcCloseMemHandle(ctx->peer_w1[q]);
+      if (ctx->peer_x[q]) cudaIpcCloseMemHandle(ctx->peer_x[q]);
+      if (ctx->peer_slots[q]) cudaIpcCloseMemHandle(ctx->peer_slots[q]);
+      if (ctx->peer_ctr[q]) cudaIpcCloseMemHandle(ctx->peer_ctr[q]);
+    }
+  }
+  cudaFree(ctx->d_gw0);
+  cudaFree(ctx->d_gw1);
+  cudaFree(ctx->d_gx);
+  cudaFree(ctx->d_dslots);
+  cudaFree(ctx->d_dctr);
+  cudaFree(ctx->d_epoch);
+  cudaFree(ctx->d_send);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evk0) cudaEventDestroy(ctx->evk0);
@@ -551,9 +669,23 @@ void gmres_destroy(gmres_ctx* ctx) {
   delete ctx;
 }
 
-int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_x, int32_t m, double tol,
-                       int32_t ortho, int32_t precision, const gmres_opts* opts, gmres_result* res,
-                       double* history, int32_t history_cap, int32_t* history_len, void* stream) {
+namespace {
+// Everything a launch of the fused solve needs for one rank: validation,
+// grid, partition, basis layout, workspace, the a0 cast, x0 and the Dev.
+struct Plan {
+  const void* kern = nullptr;
+  int G = 0;
+  size_t smem = 0;
+  Dev d{};
+  cudaStream_t st = nullptr;
+  int prec = 0;
+  bool rec_inner = false;
+  double* d_xuser = nullptr;  // caller's x (row-partitioned: copied from the internal full-length x)
+};
+
+int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_x, int32_t m, double tol,
+               int32_t ortho, int32_t precision, const gmres_opts* opts, void* stream, int G_force, bool virt,
+               Plan& P) {
   if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
   ctx->err.clear();
   if (!d_b || !d_x) return fail(ctx, GMRES_EINVAL, "b/x is NULL");
@@ -561,27 +693,31 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   if (!(tol > 0.0) || !std::isfinite(tol)) return fail(ctx, GMRES_EINVAL, "tol must be > 0");
   if (ortho != GMRES_MGS && ortho != GMRES_CGSR) return fail(ctx, GMRES_EINVAL, "ortho must be 0 (MGS) or 1 (CGSR)");
   if (int rc = check_prec(ctx, precision)) return rc;
-  if (history_cap < 0) return fail(ctx, GMRES_EINVAL, "history_cap < 0");
+  if (ctx->dist() && !ctx->linked) return fail(ctx, GMRES_EINVAL, "row-partitioned context not linked to its peers");
   double delta = (opts && opts->delta >= 0.0) ? opts->delta : (precision == GMRES_MIXED ? 1e-6 : 0.0);
   if (!std::isfinite(delta)) return fail(ctx, GMRES_EINVAL, "delta must be finite");
   const int max_cycles = (opts && opts->max_cycles > 0) ? opts->max_cycles : 10000;
-  const bool rec_inner = opts && opts->record_inner;
+  P.rec_inner = opts && opts->record_inner;
   int L = (opts && opts->lanes_per_row) ? opts->lanes_per_row : auto_lanes(ctx->n, ctx->nnz);
   if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16 && L != 32)
     return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 1/2/4/8/16/32");
-  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  if (virt && L != 1) L = 4;
+  P.st = stream ? (cudaStream_t)stream : ctx->stream;
+  P.prec = precision;
+  const cudaStream_t st = P.st;
 
-  const void* kern = pick_solve(precision, L);
+  const void* kern = virt ? pick_solve_virtual(precision, L) : pick_solve(precision, L);
   int tile_bytes = tile_bytes_for(m);
   size_t smem = smem_bytes(m, tile_bytes);
   int G = 0;
   if (int rc = grid_for(ctx, kern, smem, opts ? opts->ctas_per_sm : 0, &G)) return rc;
+  if (G_force) G = G_force;
   const VLayout vl = (opts && (opts->tune & 4096)) ? VLayout{} :
                      vlayout_for(ortho, m, precision == GMRES_MIXED ? 4 : 8, tile_bytes);
   if (int rc = ensure_partition(ctx, G, vl.tb ? vl.tb : ROWALIGN)) return rc;
-  // resident MGS (gmres_kernels.cuh mgs_resident): every CTA's rows of w and
-  // v_{i-1} in ≤ MGS_MV 16-byte registers per thread, and a ring of NB = 3 (else
-  // 2) shared buffers of one basis-vector row block for the TMA stream
+  // resident MGS (gmres_kernels.cuh mgs_resident): every CTA's rows of w in
+  // ≤ MGS_MV 16-byte registers per thread, and a ring of NB = 3 (else 2)
+  // shared buffers of one basis-vector row block for the TMA stream
   int mgs_resident = 0, mgs_nbuf = 2;
   {
     const int wb = precision == GMRES_MIXED ? 4 : 8;
@@ -593,7 +729,7 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
       const int tb = std::max(tile_bytes, nb * buf_bytes);
       if (smem_bytes(m, tb) > kMaxDynSmem) continue;
       int G2 = 0;
-      if (grid_for(ctx, kern, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 == G) {
+      if (grid_for(ctx, kern, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 >= G) {
         mgs_resident = 1;
         mgs_nbuf = nb;
         tile_bytes = tb;
@@ -602,25 +738,31 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
     }
   }
   const int hist_cap_dev = max_cycles + 2;
-  const int inner_cap_dev = rec_inner ? (int)std::min<int64_t>((int64_t)max_cycles * m, 1 << 22) : 0;
+  const int inner_cap_dev = P.rec_inner ? (int)std::min<int64_t>((int64_t)max_cycles * m, 1 << 22) : 0;
   if (int rc = ensure_ws(ctx, m, precision, G, hist_cap_dev, inner_cap_dev)) return rc;
 
   CK(cudaEventRecord(ctx->ev0, st));
-  if (int rc = reset_flags(ctx, st)) return rc;
+  if (ctx->dist()) {  // the arrival counter stays monotonic (epoch base): only the flags reset
+    CK(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * 8, st));
+  } else if (int rc = reset_flags(ctx, st)) {
+    return rc;
+  }
   if (precision == GMRES_MIXED) {  // a0: rebuilt inside every timed solve;
     // overflow is flagged on the device and reported by the solve kernel
     if (int rc = launch_cast(ctx, st, ctx->d_flags + 1)) return rc;
     ctx->a32_ready = false;  // validated only by a completed solve
   }
-  if (d_x0 && d_x0 != d_x) CK(cudaMemcpyAsync(d_x, d_x0, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
-  if (!d_x0) CK(cudaMemsetAsync(d_x, 0, sizeof(double) * ctx->n, st));
+  double* xin = ctx->dist() ? ctx->d_gx + ctx->row_begin : d_x;  // the kernel's x (local view)
+  if (d_x0 && d_x0 != xin) CK(cudaMemcpyAsync(xin, d_x0, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
+  if (!d_x0) CK(cudaMemsetAsync(xin, 0, sizeof(double) * ctx->n, st));
+  P.d_xuser = d_x;
   CK(cudaMemsetAsync(ctx->d_prof, 0, sizeof(unsigned long long) * PH_N, st));
   CK(cudaMemsetAsync(ctx->d_prof_cta, 0, sizeof(unsigned long long) * G, st));
   CK(cudaMemsetAsync(ctx->d_out_int, 0, sizeof(int) * 8, st));
 
   Dev d = make_dev(ctx, m, precision, ortho, G);
   d.b = d_b;
-  d.x = d_x;
+  d.x = xin;
   d.tol = tol;
   d.delta = delta;
   d.max_cycles = max_cycles;
@@ -629,29 +771,68 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   d.tile_bytes = tile_bytes;
   d.mgs_resident = mgs_resident;
   d.mgs_nbuf = mgs_nbuf;
-  d.vtb = vl.tb;
-  d.vtp = vl.tp;
-  d.vtb_log = vl.lg;
-  d.vbs = vl.bs;
+  set_vlayout(d, vl);
   d.tune = opts ? opts->tune : 0;
+  if (ctx->dist()) {
+    const size_t wb = precision == GMRES_MIXED ? 4 : 8;
+    d.nranks = ctx->nranks;
+    d.rank = ctx->rank;
+    d.cta0 = ctx->rank * G;
+    d.GG = ctx->nranks * G;
+    d.kst = (d.kmax + 3) & ~3;
+    d.slots = ctx->d_dslots;
+    d.ctr = ctx->d_dctr;
+    for (int q = 0; q < MAXR; ++q) {
+      d.slot_peer[q] = q < ctx->nranks ? ctx->peer_slots[q] : nullptr;
+      d.ctr_peer[q] = q < ctx->nranks ? ctx->peer_ctr[q] : nullptr;
+      d.vec_peer[0][q] = q < ctx->nranks ? ctx->peer_w0[q] : nullptr;
+      d.vec_peer[1][q] = q < ctx->nranks ? ctx->peer_w1[q] : nullptr;
+      d.vec_peer[2][q] = q < ctx->nranks ? (void*)ctx->peer_x[q] : nullptr;
+    }
+    d.sys_scope = ctx->ipc ? 1 : 0;
+    d.row_base = ctx->row_begin;
+    d.halo = 1;
+    d.w0 = (char*)ctx->d_gw0 + wb * ctx->row_begin;
+    d.w1 = (char*)ctx->d_gw1 + wb * ctx->row_begin;
+    d.send_off = ctx->d_send;
+    d.send_row = ctx->d_send + G + 1;
+    d.send_peer = ctx->d_send + G + 1 + (ctx->send_rows.empty() ? 0 : [&] {
+      size_t t = 0;
+      for (auto& v : ctx->send_rows) t += v.size();
+      return t;
+    }());
+    d.epoch0 = ctx->epoch_base;
+    d.red0 = ctx->red_base;
+    d.epoch_out = ctx->d_epoch;
+  }
+  P.kern = kern;
+  P.G = G;
+  P.smem = smem;
+  P.d = d;
+  return 0;
+}
 
+// results of a finished launch (stream synchronised by the caller)
+int finish_solve(gmres_ctx* ctx, const Plan& P, float ms, float kms, gmres_result* res, double* history,
+                 int32_t history_cap, int32_t* history_len) {
+  const cudaStream_t st = P.st;
   gmres_result r{};
-  void* args[] = {&d};
-  CK(cudaEventRecord(ctx->evk0, st));
-  if (int rc = launch_coop(ctx, kern, G, smem, args, st)) return rc;
-  CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->evk1, st));
-  CK(cudaEventRecord(ctx->ev1, st));
   int oi[8];
   double od[4];
   unsigned long long prof[PH_N];
   CK(cudaMemcpyAsync(oi, ctx->d_out_int, sizeof(oi), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(od, ctx->d_out_dbl, sizeof(od), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(prof, ctx->d_prof, sizeof(prof), cudaMemcpyDeviceToHost, st));
+  if (ctx->dist()) {
+    unsigned long long ep[2];
+    CK(cudaMemcpyAsync(ep, ctx->d_epoch, sizeof(ep), cudaMemcpyDeviceToHost, st));
+    if (P.d_xuser != P.d.x)
+      CK(cudaMemcpyAsync(P.d_xuser, P.d.x, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->epoch_base = ep[0];
+    ctx->red_base = (int)ep[1];
+  }
   CK(cudaStreamSynchronize(st));
-  float ms = 0.f, kms = 0.f;
-  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-  CK(cudaEventElapsedTime(&kms, ctx->evk0, ctx->evk1));
   r.kernel_ms = kms;
   r.status = oi[0];
   r.cycles = oi[1];
@@ -660,13 +841,13 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   r.final_relres = od[0];
   r.device_ms = ms;
   for (int i = 0; i < PH_N; ++i) ctx->phase_ns[i] = (double)prof[i];
-  if (d.profile) {  // per-CTA own SpMV time: [5] max, [6] mean
-    std::vector<unsigned long long> pc(G);
-    CK(cudaMemcpy(pc.data(), ctx->d_prof_cta, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost));
+  if (P.d.profile) {  // per-CTA own SpMV time: [5] max, [6] mean
+    std::vector<unsigned long long> pc(P.G);
+    CK(cudaMemcpy(pc.data(), ctx->d_prof_cta, sizeof(unsigned long long) * P.G, cudaMemcpyDeviceToHost));
     double mx = 0, sm = 0;
     for (auto v : pc) { mx = std::max(mx, (double)v); sm += (double)v; }
     ctx->phase_ns[5] = mx;
-    ctx->phase_ns[6] = sm / G;
+    ctx->phase_ns[6] = sm / P.G;
     ctx->phase_ns[7] = 0;
   }
   const int hl = std::min(r.history_len, std::min(history_cap, ctx->hist_cap));
@@ -676,17 +857,247 @@ int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, do
   ctx->cycJ_host.assign(std::max(0, std::min(r.cycles, ctx->hist_cap)), 0);
   if (!ctx->cycJ_host.empty())
     CK(cudaMemcpy(ctx->cycJ_host.data(), ctx->d_cycJ, sizeof(int) * ctx->cycJ_host.size(), cudaMemcpyDeviceToHost));
-  if (rec_inner && oi[4] > 0) {
+  if (P.rec_inner && oi[4] > 0) {
     const int il = std::min(oi[4], ctx->inner_cap);
     ctx->inner_host.resize(il);
     CK(cudaMemcpy(ctx->inner_host.data(), ctx->d_inner, sizeof(double) * il, cudaMemcpyDeviceToHost));
   }
   if (res) *res = r;
   if (r.status == ST_ETIMEOUT) return fail(ctx, GMRES_ETIMEOUT, "device watchdog fired in a grid barrier");
-  if (precision == GMRES_MIXED && r.status != ST_EFP32RANGE) ctx->a32_ready = true;
+  if (P.prec == GMRES_MIXED && r.status != ST_EFP32RANGE) ctx->a32_ready = true;
   if (r.status == ST_EFP32RANGE) return fail(ctx, GMRES_EFP32RANGE, "matrix or residual entry outside the fp32 range");
   if (r.status == ST_ENONFINITE) return fail(ctx, GMRES_ENONFINITE, "non-finite value in the residual or Arnoldi process");
   return r.status;
+}
+}  // namespace
+
+int gmres_solve_device(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_x, int32_t m, double tol,
+                       int32_t ortho, int32_t precision, const gmres_opts* opts, gmres_result* res,
+                       double* history, int32_t history_cap, int32_t* history_len, void* stream) {
+  if (history_cap < 0) return fail(ctx, GMRES_EINVAL, "history_cap < 0");
+  if (ctx && ctx->dist() && !ctx->ipc)
+    return fail(ctx, GMRES_EINVAL, "in-process (virtual) ranks are solved together by gmres_solve_virtual");
+  Plan P;
+  if (int rc = plan_solve(ctx, d_b, d_x0, d_x, m, tol, ortho, precision, opts, stream, 0, false, P)) return rc;
+  DevSet ds{};
+  ds.d[0] = P.d;
+  ds.G = P.G;
+  ds.nv = 1;
+  void* args[] = {&ds};
+  CK(cudaEventRecord(ctx->evk0, P.st));
+  if (int rc = launch_coop(ctx, P.kern, P.G, P.smem, args, P.st)) return rc;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->evk1, P.st));
+  CK(cudaEventRecord(ctx->ev1, P.st));
+  CK(cudaStreamSynchronize(P.st));
+  float ms = 0.f, kms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  CK(cudaEventElapsedTime(&kms, ctx->evk0, ctx->evk1));
+  return finish_solve(ctx, P, ms, kms, res, history, history_cap, history_len);
+}
+
+// ------------------------------------------------ row partition over ranks (§8 e)
+namespace {
+// sorted unique global columns of local rows [0, n) (global rows
+// [row_begin, row_begin + n)) that lie outside them
+void ghosts_of(const int32_t* row_ptr, const int32_t* col, int64_t n, int64_t row_begin, std::vector<int32_t>& g) {
+  g.clear();
+  for (int64_t e = 0; e < row_ptr[n]; ++e)
+    if (col[e] < row_begin || col[e] >= row_begin + n) g.push_back(col[e]);
+  std::sort(g.begin(), g.end());
+  g.erase(std::unique(g.begin(), g.end()), g.end());
+}
+// local rows of [row_begin, row_begin + n) that appear in a peer's ghost list
+void sends_to(int64_t row_begin, int64_t n, const int32_t* pg, int64_t np, std::vector<int32_t>& rows) {
+  rows.clear();
+  const int32_t* lo = std::lower_bound(pg, pg + np, (int32_t)row_begin);
+  for (const int32_t* p = lo; p < pg + np && *p < row_begin + n; ++p) rows.push_back((int32_t)(*p - row_begin));
+}
+int copy_out(const std::vector<int32_t>& v, int32_t* out, int64_t cap, int64_t* count) {
+  if (count) *count = (int64_t)v.size();
+  if (out) std::memcpy(out, v.data(), sizeof(int32_t) * std::min<int64_t>(cap, (int64_t)v.size()));
+  return 0;
+}
+constexpr uint32_t BLOB_MAGIC = 0x47324230u;  // "G2B0"
+struct BlobHdr {
+  uint32_t magic;
+  int32_t rank, nranks, pad;
+  int64_t row_begin, n_local, n_global, n_ghost;
+  cudaIpcMemHandle_t h[5];  // w0, w1, x, all-reduce partials, arrival counter
+};
+void relink(gmres_ctx* c) { c->part_G = 0; c->linked = true; }
+}  // namespace
+
+int gmres_dist_ghosts(const int32_t* row_ptr, const int32_t* col, int64_t n_local, int64_t row_begin, int32_t* ghosts,
+                      int64_t cap, int64_t* count) {
+  if (!row_ptr || (!col && row_ptr[n_local] > 0) || n_local < 0) return fail(nullptr, GMRES_EINVAL, "bad arguments");
+  std::vector<int32_t> g;
+  ghosts_of(row_ptr, col, n_local, row_begin, g);
+  return copy_out(g, ghosts, cap, count);
+}
+
+int gmres_dist_sends(int64_t row_begin, int64_t n_local, const int32_t* peer_ghosts, int64_t n_peer_ghosts,
+                     int32_t* rows, int64_t cap, int64_t* count) {
+  if ((!peer_ghosts && n_peer_ghosts > 0) || n_local < 0) return fail(nullptr, GMRES_EINVAL, "bad arguments");
+  std::vector<int32_t> r;
+  sends_to(row_begin, n_local, peer_ghosts, n_peer_ghosts, r);
+  return copy_out(r, rows, cap, count);
+}
+
+int gmres_dist_partition(const int32_t* row_ptr, int64_t n, int32_t nranks, int64_t align, int64_t* bounds) {
+  if (!row_ptr || !bounds || n < 1 || nranks < 1 || nranks > MAXR || align < 1) return fail(nullptr, GMRES_EINVAL, "bad arguments");
+  // balance rows + nnz (the per-rank cost of a restart cycle: vectors and A),
+  // boundaries at multiples of align, last = n
+  const double total = (double)n + (double)row_ptr[n];
+  bounds[0] = 0;
+  for (int q = 1; q < nranks; ++q) {
+    const double target = total * q / nranks;
+    int64_t lo = bounds[q - 1] / align, hi = n / align;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if ((double)(mid * align) + (double)row_ptr[mid * align] < target) lo = mid + 1; else hi = mid;
+    }
+    bounds[q] = lo * align;
+  }
+  bounds[nranks] = n;
+  for (int q = 0; q < nranks; ++q)
+    if (bounds[q + 1] <= bounds[q]) return fail(nullptr, GMRES_EINVAL, "too many ranks for this matrix");
+  return 0;
+}
+
+int gmres_create_dist(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n_global,
+                      int64_t row_begin, int64_t n_local, int32_t nranks, int32_t rank, gmres_ctx** out) {
+  if (nranks < 2 || nranks > MAXR || rank < 0 || rank >= nranks) return fail(nullptr, GMRES_EINVAL, "bad nranks/rank");
+  if (row_begin % VEC_ALIGN || (n_local % VEC_ALIGN && row_begin + n_local != n_global))
+    return fail(nullptr, GMRES_EINVAL, "rank row blocks must start and end at multiples of 256 rows (except the last end)");
+  if (!row_ptr) return fail(nullptr, GMRES_EINVAL, "null CSR array");
+  return create_impl(row_ptr, col, val, n_local, row_ptr[n_local], n_global, row_begin, nranks, rank, out);
+}
+
+int gmres_dist_link_local(gmres_ctx* const* ctxs, int32_t nranks) {
+  if (!ctxs || nranks < 2 || nranks > MAXV) return fail(nullptr, GMRES_EINVAL, "need 2..4 in-process ranks");
+  for (int i = 0; i < nranks; ++i) {
+    gmres_ctx* c = ctxs[i];
+    if (!c || c->nranks != nranks || c->rank != i || c->n_global != ctxs[0]->n_global || c->device != ctxs[0]->device)
+      return fail(c, GMRES_EINVAL, "contexts must be ranks 0..P-1 of one matrix on one device, in order");
+  }
+  for (int i = 0; i < nranks; ++i) {
+    gmres_ctx* c = ctxs[i];
+    c->send_rows.assign(nranks, {});
+    for (int q = 0; q < nranks; ++q) {
+      c->peer_w0[q] = ctxs[q]->d_gw0;
+      c->peer_w1[q] = ctxs[q]->d_gw1;
+      c->peer_x[q] = ctxs[q]->d_gx;
+      c->peer_slots[q] = ctxs[q]->d_dslots;
+      c->peer_ctr[q] = ctxs[q]->d_dctr;
+      if (q != i) sends_to(c->row_begin, c->n, ctxs[q]->ghosts.data(), (int64_t)ctxs[q]->ghosts.size(), c->send_rows[q]);
+    }
+    c->ipc = false;
+    relink(c);
+  }
+  return 0;
+}
+
+int gmres_dist_export(gmres_ctx* ctx, void* blob, int64_t cap, int64_t* len) {
+  if (!ctx || !ctx->dist() || !len) return fail(ctx, GMRES_EINVAL, "not a row-partitioned context");
+  const int64_t need = (int64_t)sizeof(BlobHdr) + (int64_t)sizeof(int32_t) * (int64_t)ctx->ghosts.size();
+  *len = need;
+  if (!blob) return 0;
+  if (cap < need) return fail(ctx, GMRES_EINVAL, "blob buffer too small");
+  BlobHdr h{};
+  h.magic = BLOB_MAGIC;
+  h.rank = ctx->rank;
+  h.nranks = ctx->nranks;
+  h.row_begin = ctx->row_begin;
+  h.n_local = ctx->n;
+  h.n_global = ctx->n_global;
+  h.n_ghost = (int64_t)ctx->ghosts.size();
+  void* bufs[5] = {ctx->d_gw0, ctx->d_gw1, ctx->d_gx, ctx->d_dslots, ctx->d_dctr};
+  for (int i = 0; i < 5; ++i) CK(cudaIpcGetMemHandle(&h.h[i], bufs[i]));
+  std::memcpy(blob, &h, sizeof(h));
+  if (!ctx->ghosts.empty())
+    std::memcpy((char*)blob + sizeof(h), ctx->ghosts.data(), sizeof(int32_t) * ctx->ghosts.size());
+  return 0;
+}
+
+int gmres_dist_import(gmres_ctx* ctx, const void* blobs, const int64_t* offsets) {
+  if (!ctx || !ctx->dist() || !blobs || !offsets) return fail(ctx, GMRES_EINVAL, "bad arguments");
+  ctx->send_rows.assign(ctx->nranks, {});
+  for (int q = 0; q < ctx->nranks; ++q) {
+    const char* b = (const char*)blobs + offsets[q];
+    BlobHdr h;
+    std::memcpy(&h, b, sizeof(h));
+    if (h.magic != BLOB_MAGIC || h.rank != q || h.nranks != ctx->nranks || h.n_global != ctx->n_global ||
+        offsets[q + 1] - offsets[q] != (int64_t)sizeof(h) + (int64_t)sizeof(int32_t) * h.n_ghost)
+      return fail(ctx, GMRES_EINVAL, "malformed blob of rank " + std::to_string(q));
+    if (q == ctx->rank) {
+      ctx->peer_w0[q] = ctx->d_gw0;
+      ctx->peer_w1[q] = ctx->d_gw1;
+      ctx->peer_x[q] = ctx->d_gx;
+      ctx->peer_slots[q] = ctx->d_dslots;
+      ctx->peer_ctr[q] = ctx->d_dctr;
+      continue;
+    }
+    void* p[5];
+    for (int i = 0; i < 5; ++i) CK(cudaIpcOpenMemHandle(&p[i], h.h[i], cudaIpcMemLazyEnablePeerAccess));
+    ctx->peer_w0[q] = p[0];
+    ctx->peer_w1[q] = p[1];
+    ctx->peer_x[q] = (double*)p[2];
+    ctx->peer_slots[q] = (double*)p[3];
+    ctx->peer_ctr[q] = (unsigned long long*)p[4];
+    sends_to(ctx->row_begin, ctx->n, (const int32_t*)(b + sizeof(h)), h.n_ghost, ctx->send_rows[q]);
+  }
+  ctx->ipc = true;
+  relink(ctx);
+  return 0;
+}
+
+int gmres_solve_virtual(gmres_ctx* const* ctxs, int32_t nranks, const double* const* d_b, const double* const* d_x0,
+                        double* const* d_x, int32_t m, double tol, int32_t ortho, int32_t precision,
+                        const gmres_opts* opts, gmres_result* res) {
+  if (!ctxs || nranks < 2 || nranks > MAXV || !d_b || !d_x) return fail(nullptr, GMRES_EINVAL, "bad arguments");
+  for (int i = 0; i < nranks; ++i)
+    if (!ctxs[i] || !ctxs[i]->linked || ctxs[i]->ipc || ctxs[i]->nranks != nranks || ctxs[i]->rank != i)
+      return fail(ctxs[i], GMRES_EINVAL, "contexts must be linked in-process ranks 0..P-1");
+  gmres_ctx* c0 = ctxs[0];
+  gmres_ctx* ctx = c0;  // (error reporting)
+  const int G = c0->sms / nranks;  // every rank gets an equal share of the device
+  Plan P[MAXV];
+  for (int i = 0; i < nranks; ++i)
+    if (int rc = plan_solve(ctxs[i], d_b[i], d_x0 ? d_x0[i] : nullptr, d_x[i], m, tol, ortho, precision, opts, nullptr,
+                            G, true, P[i]))
+      return rc;
+  for (int i = 0; i < nranks; ++i) {
+    cudaError_t e = cudaStreamSynchronize(ctxs[i]->stream);
+    if (e != cudaSuccess) return fail(ctxs[i], GMRES_ECUDA, cudaGetErrorString(e));
+  }
+  size_t smem = 0;
+  for (int i = 0; i < nranks; ++i) {
+    if (P[i].kern != P[0].kern) return fail(c0, GMRES_EINVAL, "ranks need the same kernel (lanes per row)");
+    smem = std::max(smem, P[i].smem);
+  }
+  int per_sm = 0;
+  CK(cudaFuncSetAttribute(P[0].kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P[0].kern, NT, smem));
+  if (per_sm < 1) return fail(c0, GMRES_ECUDA, "solve kernel cannot be resident");
+  DevSet ds{};
+  for (int i = 0; i < nranks; ++i) ds.d[i] = P[i].d;
+  ds.G = G;
+  ds.nv = nranks;
+  void* args[] = {&ds};
+  CK(cudaEventRecord(c0->evk0, c0->stream));
+  if (int rc = launch_coop(c0, P[0].kern, G * nranks, smem, args, c0->stream)) return rc;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c0->evk1, c0->stream));
+  CK(cudaStreamSynchronize(c0->stream));
+  float kms = 0.f;
+  CK(cudaEventElapsedTime(&kms, c0->evk0, c0->evk1));
+  int rc_all = 0;
+  for (int i = 0; i < nranks; ++i) {
+    const int rc = finish_solve(ctxs[i], P[i], kms, kms, res ? &res[i] : nullptr, nullptr, 0, nullptr);
+    if (i == 0 || rc < 0) rc_all = rc;
+  }
+  return rc_all;
 }
 
 int gmres_solve(gmres_ctx* ctx, const double* b, const double* x0, double* x_out, int32_t m, double tol,
@@ -754,6 +1165,7 @@ namespace {
 int comp_setup(gmres_ctx* ctx, int prec, int m_req, int kind, int L, const void** kern, int* G, size_t* smem,
                int* m_ws, int align = ROWALIGN) {
   if (int rc = check_prec(ctx, prec)) return rc;
+  if (ctx->dist()) return fail(ctx, GMRES_EINVAL, "component entry points take a single-rank context");
   if (prec == GMRES_MIXED)
     if (int rc = ensure_a32(ctx, ctx->stream)) return rc;
   const int m = (ctx->ws_m > 0 && ctx->ws_prec == prec) ? std::max(m_req, ctx->ws_m) : m_req;
@@ -783,12 +1195,6 @@ int pack_blocked(gmres_ctx* ctx, int prec, const void* d_V, int64_t ldv, int nco
   return 0;
 }
 
-void set_vlayout(Dev& d, const VLayout& vl) {
-  d.vtb = vl.tb;
-  d.vtp = vl.tp;
-  d.vtb_log = vl.lg;
-  d.vbs = vl.bs;
-}
 }  // namespace
 
 int gmres_k_spmv(gmres_ctx* ctx, int32_t precision, const void* d_v, void* d_w) {

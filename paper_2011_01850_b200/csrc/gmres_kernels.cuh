@@ -92,6 +92,24 @@ struct Dev {
   int cta0;             // global index of this rank's CTA 0 (rank * G)
   int nranks, rank;
   int sys_scope;        // != 0: peers are other GPUs (system-scope release/acquire)
+  // row partition over ranks (§8 e): this rank owns global rows
+  // [row_base, row_base + n); n-vectors are addressed by LOCAL row through
+  // views into full-length buffers (w0, w1, x), CSR columns are GLOBAL, so a
+  // gather reads view[col − row_base].  The rows a peer gathers are pushed
+  // into that peer's buffer (vec_peer: global-index bases of every rank's w0,
+  // w1, x) by the CTA owning them, before the release of the next all-reduce.
+  long long row_base;
+  int halo;             // != 0: push halo rows (nranks > 1)
+  // barrier epochs / all-reduce count at launch (row-partitioned solves keep
+  // the arrival counters monotonic across launches instead of resetting them,
+  // so no rank can wipe a faster rank's arrival); final values → epoch_out
+  unsigned long long epoch0;
+  int red0;
+  unsigned long long* epoch_out;  // [0] barrier epochs, [1] all-reduces (CTA 0)
+  void* vec_peer[3][MAXR];
+  const int* send_off;  // [G+1] per-CTA ranges of the send list
+  const int* send_row;  // local row to push
+  const int* send_peer; // destination rank
   double* R;            // rotated Hessenberg, (m+1) x m, ld m+1 (CTA 0)
   double* y;            // m
   int* abort_flag;
@@ -213,8 +231,9 @@ struct Shm {
   int abort;
   int flag;
   unsigned long long epoch;          // grid barriers passed by this CTA (thread 0)
+  int cta;                           // CTA index within its rank (blockIdx.x unless virtual ranks)
   int red_epoch;                     // all-reduces done (partial buffer parity; thread 0 writes)
-  double red[NW * 4];
+  double red[NW * 8];
   double red2[NW * 4];
 };
 
@@ -236,8 +255,9 @@ __device__ __forceinline__ void stage_wait(const Dev& d, Shm& sh, int grp, int s
 
 __device__ __forceinline__ void group_sync(int) { __syncwarp(); }
 
-__device__ __forceinline__ void init_shm(Shm& sh) {
+__device__ __forceinline__ void init_shm(Shm& sh, int cta) {
   if (threadIdx.x == 0) {
+    sh.cta = cta;
     sh.epoch = 0;
     sh.red_epoch = 0;
     sh.abort = 0;
@@ -311,8 +331,8 @@ __device__ __forceinline__ bool grid_sync(const Dev& d, Shm& sh) {
 }
 
 // push this CTA's K partials into buffer buf of every rank's array
-__device__ __forceinline__ void push_partials(const Dev& d, const double* s_part, int K, int buf) {
-  const int gc = d.cta0 + (int)blockIdx.x;
+__device__ __forceinline__ void push_partials(const Dev& d, const Shm& sh, const double* s_part, int K, int buf) {
+  const int gc = d.cta0 + sh.cta;
   for (int t = threadIdx.x; t < K * d.nranks; t += NT) {
     const int q = t / K, k = t - q * K;
     slot_row(d, d.slot_peer[q], buf, gc)[k] = s_part[k];
@@ -357,7 +377,7 @@ __device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool
 #pragma unroll
     for (int o = NW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      const int gc = d.cta0 + (int)blockIdx.x;
+      const int gc = d.cta0 + sh.cta;
       for (int q = 0; q < d.nranks; ++q) slot_row(d, d.slot_peer[q], buf, gc)[0] = s;
       sh.abort = arrive_wait(d, sh) ? 0 : 1;
       sh.red_epoch++;
@@ -386,7 +406,7 @@ constexpr int GCH = 8;  // independent partial loads in flight per lane
 __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const double* s_part, int K, double* s_out,
                                                double* s_tmp, bool /*acq*/ = true) {
   const int buf = sh.red_epoch & 1;
-  push_partials(d, s_part, K, buf);
+  push_partials(d, sh, s_part, K, buf);
   __syncthreads();
   if (threadIdx.x == 0) {
     sh.abort = arrive_wait(d, sh) ? 0 : 1;
@@ -423,6 +443,26 @@ __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const doub
   __syncthreads();
   return true;
 }
+
+// ---------------------------------------------------- halo push (§8 e)
+// Push the rows of `loc` (this rank's local view of buffer `which`: 0 = w0,
+// 1 = w1, 2 = x) that peers gather into their full-length copies of it, at the
+// same global index.  Called by every CTA after its own rows of `loc` are
+// final and before the all-reduce/barrier whose release publishes them
+// (no-op on one rank).
+template <class T>
+__device__ __forceinline__ void halo_push(const Dev& d, const Shm& sh, const T* loc, int which) {
+  if (!d.halo) return;
+  __syncthreads();  // the CTA's final values of loc are written
+  const int e0 = d.send_off[sh.cta], e1 = d.send_off[sh.cta + 1];
+  for (int e = e0 + threadIdx.x; e < e1; e += NT) {
+    const int row = d.send_row[e];
+    T* pb = reinterpret_cast<T*>(d.vec_peer[which][d.send_peer[e]]);
+    pb[d.row_base + row] = loc[row];
+  }
+}
+template <class W>
+__device__ __forceinline__ int wbuf_index(const Dev& d, const W* w) { return w == (const W*)d.w0 ? 0 : 1; }
 
 // ---------------------------------------------------- CSR stream (a1, a2)
 // The CTA's rows are cut (on the host) into chunks of ≤ CHUNK_RMAX rows and
@@ -499,8 +539,9 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
   using Ops = AccOps<AT>;
   using PT = decltype(pre(0, (RT)0));
   const int grp = threadIdx.x / GT, gt = threadIdx.x % GT;
-  const int c0 = d.chunk_off[blockIdx.x], c1 = d.chunk_off[blockIdx.x + 1] - 1;
+  const int c0 = d.chunk_off[sh.cta], c1 = d.chunk_off[sh.cta + 1] - 1;
   const int nk = c1 - c0 > grp ? (c1 - c0 - grp + NGRP - 1) / NGRP : 0;  // chunks of this pipeline
+  const int gro = (int)d.row_base;  // columns are global: local row r's diagonal is column r + gro
   constexpr int NS = NSTG<AT>(), SB = stage_bytes<AT>();
   constexpr int GB = 8;
   char* gbase = s_stage + grp * NS * SB;
@@ -553,7 +594,7 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
 #pragma unroll
       for (int u = 0; u < GB; ++u) {
         if (pb + u * L < p1) acc = Ops::add(acc, Ops::mul(a[u], g[u]));
-        if (cc[u] == row) diag = g[u];
+        if (cc[u] == row + gro) diag = g[u];
       }
     }
     return acc;
@@ -599,8 +640,8 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
             for (int u = 0; u < GB; ++u) {
               if (p1 + u < q1) acc1 = Ops::add(acc1, Ops::mul(a1[u], g1[u]));
               if (p2 + u < q2) acc2 = Ops::add(acc2, Ops::mul(a2[u], g2[u]));
-              if (k1[u] == rb + lr) dg1 = g1[u];
-              if (k2[u] == rb2 + lr) dg2 = g2[u];
+              if (k1[u] == rb + lr + gro) dg1 = g1[u];
+              if (k2[u] == rb2 + lr + gro) dg2 = g2[u];
             }
             p1 += GB;
             p2 += GB;
@@ -658,7 +699,7 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
           const int col = __ldg(d.ci + p);
           const AT g = gat(col);
           acc = Ops::add(acc, Ops::mul(__ldg(vals + p), g));
-          if (col == row) dg = g;
+          if (col == row + gro) dg = g;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -688,9 +729,9 @@ template <class W, int L>
 __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict__ r_out, double& zz, double& rr,
                             double& bb, int& err) {
   const W* dinv = (const W*)d.dinvW;
-  const double* __restrict__ x = d.x;
+  const double* __restrict__ xg = d.x - d.row_base;  // global-index view (CSR columns are global)
   struct P2 { double b; W di; };
-  auto gat = [&](int col) -> double { return x[col]; };
+  auto gat = [&](int col) -> double { return xg[col]; };
   auto pre = [&](int row, W di) -> P2 { return P2{d.b[row], di}; };
   auto epi = [&](int row, double acc, P2 pv, double) {
     const double bi = pv.b;
@@ -715,7 +756,8 @@ template <class W, int L>
 __device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
                            W* __restrict__ dst, W* __restrict__ V, int vc) {
   const W* dinv = (const W*)d.dinvW;
-  auto gat = [&](int col) -> W { return RN<W>((double)src[col] * inv); };
+  const W* __restrict__ srcg = src - d.row_base;  // global-index view (CSR columns are global)
+  auto gat = [&](int col) -> W { return RN<W>((double)srcg[col] * inv); };
   auto pre = [&](int, W di) -> W { return di; };
   auto epi = [&](int row, W acc, W di, W vj) {
     dst[row] = mulw(di, acc);
@@ -1020,6 +1062,7 @@ struct SmemLayout {
   }
 };
 
+#define CTA_INDEX ((int)blockIdx.x)
 #define G200_SMEM_CARVE(W)                                                  \
   extern __shared__ __align__(128) char dsm[];                              \
   __shared__ Shm sh;                                                        \
@@ -1037,7 +1080,7 @@ struct SmemLayout {
   char* s_tiles = dsm + lay.off_tiles;                                      \
   (void)s_part; (void)s_out; (void)s_tmp; (void)s_h; (void)s_cs; (void)s_sn; \
   (void)s_s; (void)s_y; (void)s_rhs; (void)s_coefW; (void)s_tiles;          \
-  init_shm(sh);
+  init_shm(sh, CTA_INDEX);
 
 // ------------------------------------------------------------------ a3 (resident)
 // MGS with the CTA's rows of w in registers and the basis
@@ -1092,7 +1135,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     }
   }
   W hprev = (W)0;
-  const bool lead = d.profile && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
   unsigned long long tp = lead ? globaltimer() : 0ull;
   auto tick = [&](int slot) {
     if (lead) { const unsigned long long t = globaltimer(); d.prof[slot] += t - tp; tp = t; }
@@ -1148,7 +1191,8 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     }
   }
   if (threadIdx.x == 0) sh.vphase = ph;  // read by every thread at entry, before the syncs below
-  return allreduce1(d, sh, nn, true, NN);
+  NN = nn;  // this thread's share of ‖w‖²; the caller pushes the halo and all-reduces it
+  return true;
 }
 
 // Orthogonalisation of w (own rows) against V[:, 0..j) and its norm: MGS
@@ -1158,8 +1202,12 @@ template <class W>
 __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
                             double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
                             char* s_tiles, double& NN) {
-  if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4))
-    return mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, NN);
+  if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4)) {
+    double nn = 0.0;
+    if (!mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
+    halo_push(d, sh, (const W*)w, wbuf_index(d, w));
+    return allreduce1(d, sh, nn, true, NN);
+  }
   if (d.ortho == 0) {
     W hprev = (W)0;
     const bool pf = !(d.tune & 1) && r1 > r0;
@@ -1177,10 +1225,11 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
       hprev = RN<W>(h);
     }
     const double acc = mgs_sweep<W>(r0, r1, w, V + (long long)(j - 1) * ldv, hprev, nullptr);
+    halo_push(d, sh, (const W*)w, wbuf_index(d, w));
     return allreduce1(d, sh, acc, true, NN);
   }
   double nn = 0.0;
-  const bool lead = d.profile && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
   unsigned long long tp = lead ? globaltimer() : 0ull;
   auto sub = [&](int slot) {
     if (d.profile) {
@@ -1210,6 +1259,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   __syncthreads();
   nn = 0.0;
   rowtile_pass<W, 3>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  halo_push(d, sh, (const W*)w, wbuf_index(d, w));
   sub(4);
   if (!allreduce1(d, sh, nn, true, NN)) return false;
   sub(5);
@@ -1217,35 +1267,70 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
 }
 
 // ---------------------------------------------------------- the solve
-template <class W, int L>
-__global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
+// One launch runs the whole restarted solve of one rank (d = ds.d[0], G CTAs)
+// or of ds.nv "virtual ranks" on one device (rank v = CTAs [v·G, (v+1)·G)):
+// the same code, with peer buffers that are other allocations on the device —
+// how the multi-rank path is exercised with one GPU (one cooperative launch:
+// the ranks' CTAs wait on one another).
+constexpr int MAXV = 4;
+struct DevSet {
+  Dev d[MAXV];
+  int G;   // CTAs per rank
+  int nv;  // ranks in this launch (1 = one rank per process/GPU)
+};
+
+template <class W, int L, bool VR>
+__global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ DevSet ds) {
+  // (VR = false: a static index keeps every field of d a constant-bank operand)
+  const int vr = VR ? (int)blockIdx.x / ds.G : 0;
+  const Dev& d = ds.d[VR ? vr : 0];
+#undef CTA_INDEX
+#define CTA_INDEX ((int)blockIdx.x - vr * ds.G)
   G200_SMEM_CARVE(W)
-  const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
+#undef CTA_INDEX
+#define CTA_INDEX ((int)blockIdx.x)
+  const int cta = sh.cta;
+  if (threadIdx.x == 0) { sh.epoch = d.epoch0; sh.red_epoch = d.red0; }
+  __syncthreads();
+  const int r0 = d.row_begin[cta], r1 = d.row_begin[cta + 1];
   W* const wb0 = reinterpret_cast<W*>(d.w0);
   W* const wb1 = reinterpret_cast<W*>(d.w1);
   W* const V = reinterpret_cast<W*>(d.V);
   const long long ldv = d.ldv;
-  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const bool lead = cta == 0 && threadIdx.x == 0;
   unsigned long long tprev = lead ? globaltimer() : 0ull;
   auto tick = [&](int ph) {
     if (lead) { const unsigned long long t = globaltimer(); d.prof[ph] += t - tprev; tprev = t; }
   };
 
   int k = 0, total_inner = 0, inner_len = 0, status = ST_OK;
-  if (*(volatile int*)d.err_flag & ERRF_RANGE) {  // A32 cast overflow (cast32_kernel, same stream)
-    if (lead) { d.out_int[0] = ST_EFP32RANGE; d.out_int[1] = 0; d.out_int[2] = 0; d.out_int[4] = 0; }
-    return;
+  // (every rank reads its own flag: the cast overflow check is the same on all
+  // ranks only if the caller built A32 on all of them; ranks agree on it via
+  // the residual all-reduce below, which carries the error bits)
+  if (d.halo) {  // x0's rows that peers gather
+    halo_push(d, sh, (const double*)d.x, 2);
+    if (!grid_sync(d, sh)) status = ST_ETIMEOUT;
   }
-  for (;;) {
+  for (; status == ST_OK;) {
     // ---------------- residual, stop test (Alg. 1 lines 86–92)
     double v3[3] = {0.0, 0.0, 0.0};
     int err = 0;
     resid_phase<W, L>(d, sh, s_tiles, wb0, v3[0], v3[1], v3[2], err);
     if (err) atomicOr(d.err_flag, err);
+    __syncthreads();
+    // error indicators of every rank travel inside the sums, so all ranks stop
+    // alike: non-finite → NaN in ‖z‖², fp32 overflow (this residual, or the A32
+    // cast before the launch) → +Inf in ‖r‖² (a sum of fp32 squares is finite)
+    if (threadIdx.x == 0) {
+      const int f = *(volatile int*)d.err_flag;
+      if (f & ERRF_NONFINITE) v3[0] = __longlong_as_double(0x7ff8000000000000ll);
+      if (f & ERRF_RANGE) v3[1] = __longlong_as_double(0x7ff0000000000000ll);
+    }
+    halo_push(d, sh, (const W*)wb0, 0);
     block_sum<3>(v3, sh, s_part);
     if (!grid_allreduce(d, sh, s_part, 3, s_out, s_tmp)) { status = ST_ETIMEOUT; break; }
     const double ZZ = s_out[0], RR = s_out[1], nb = sqrt(s_out[2]);
-    const int ef = *(volatile int*)d.err_flag;
+    const int ef = *(volatile int*)d.err_flag;  // (other ranks' errors arrive as NaN/Inf in ZZ/RR)
     if (nb == 0.0) {  // b = 0 → x = 0, no cycle (reading R13)
       for (int i = r0 + threadIdx.x; i < min(r1, d.n); i += NT) d.x[i] = 0.0;
       if (lead) { if (d.hist_cap > 0) d.history[0] = 0.0; d.out_int[3] = 1; d.out_dbl[0] = 0.0; }
@@ -1260,7 +1345,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     }
     tick(PH_RESID);
     if (ef & ERRF_NONFINITE || !isfinite(ZZ) || !isfinite(nb)) { status = ST_ENONFINITE; break; }
-    if (ef & ERRF_RANGE) { status = ST_EFP32RANGE; break; }
+    if ((ef & ERRF_RANGE) || RR > DBL_MAX) { status = ST_EFP32RANGE; break; }
     if (rho <= d.tol) { status = ST_OK; break; }
     if (k >= d.max_cycles) { status = ST_NOT_CONVERGED; break; }
     const double beta = sqrt(RR);
@@ -1280,7 +1365,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
       const unsigned long long ts0 = d.profile && threadIdx.x == 0 ? globaltimer() : 0ull;
       spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V, j - 1);
       if (d.profile) {
-        if (threadIdx.x == 0) d.prof_cta[blockIdx.x] += globaltimer() - ts0;
+        if (threadIdx.x == 0) d.prof_cta[cta] += globaltimer() - ts0;
         if (!grid_sync(d, sh)) { fail = true; break; }
       }
       tick(PH_SPMV);
@@ -1296,7 +1381,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
       if (threadIdx.x == 0) {
         s_h[j] = hn;
         const double sabs = hess_step(j, s_h, s_cs, s_sn, s_s);
-        if (blockIdx.x == 0) {
+        if (cta == 0) {
           for (int i = 0; i <= j; ++i) d.R[(size_t)(j - 1) * (d.m + 1) + i] = s_h[i];
           if (inner_len < d.inner_cap) d.inner_hist[inner_len] = sabs / beta;
         }
@@ -1315,12 +1400,13 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     total_inner += J;
     if (lead && k < d.hist_cap) d.cycle_J[k] = J;
     // ------------ y = R⁻¹ s, x ← x + V_J y  (lines 143–147)
-    if (blockIdx.x == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);
+    if (cta == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     for (int i = threadIdx.x; i < J; i += NT) s_y[i] = __ldcg(d.y + i);
     __syncthreads();
     double dummy = 0.0;
     rowtile_pass<W, 4>(d, sh, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
+    halo_push(d, sh, (const double*)d.x, 2);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     tick(PH_UPDATE);
     ++k;
@@ -1330,6 +1416,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(Dev d) {
     d.out_int[1] = k;
     d.out_int[2] = total_inner;
     d.out_int[4] = inner_len;
+    if (d.epoch_out) { d.epoch_out[0] = sh.epoch; d.epoch_out[1] = (unsigned long long)sh.red_epoch; }
   }
 }
 
@@ -1358,11 +1445,12 @@ __global__ void pack_vblocked_kernel(const W* __restrict__ src, long long ldv, i
 
 // Jacobi M = diag(A) (reading R11): dinv64 = 1/a_ii (fp64), dinv32 = RN32(dinv64).
 __global__ void dinv_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                            const double* __restrict__ a, double* dinv64, float* dinv32, int* bad_row) {
+                            const double* __restrict__ a, double* dinv64, float* dinv32, int* bad_row,
+                            long long row_base) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double dg = 0.0;
     for (int p = rp[i]; p < rp[i + 1]; ++p)
-      if (ci[p] == i) dg = a[p];
+      if (ci[p] == i + row_base) dg = a[p];
     if (dg == 0.0 || !isfinite(dg)) {
       atomicMin(bad_row, i);
       dinv64[i] = 0.0;

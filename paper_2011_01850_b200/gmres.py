@@ -83,6 +83,18 @@ def load_library():
     for f in ("gmres_k_spmv", "gmres_k_resid", "gmres_k_ortho", "gmres_k_xupdate", "gmres_k_hessenberg",
               "gmres_k_cast32", "gmres_k_matrix", "gmres_k_micro"):
         getattr(L, f).restype = ctypes.c_int
+    p64 = ctypes.POINTER(i64)
+    L.gmres_dist_partition.argtypes = [vp, i64, i32, i64, vp]
+    L.gmres_dist_ghosts.argtypes = [vp, vp, i64, i64, vp, i64, p64]
+    L.gmres_dist_sends.argtypes = [i64, i64, vp, i64, vp, i64, p64]
+    L.gmres_create_dist.argtypes = [vp, vp, vp, i64, i64, i64, i32, i32, ctypes.POINTER(vp)]
+    L.gmres_dist_export.argtypes = [vp, vp, i64, p64]
+    L.gmres_dist_import.argtypes = [vp, vp, vp]
+    L.gmres_dist_link_local.argtypes = [vp, i32]
+    L.gmres_solve_virtual.argtypes = [vp, i32, vp, vp, vp, i32, dbl, i32, i32, pO, vp]
+    for f in ("gmres_dist_partition", "gmres_dist_ghosts", "gmres_dist_sends", "gmres_create_dist",
+              "gmres_dist_export", "gmres_dist_import", "gmres_dist_link_local", "gmres_solve_virtual"):
+        getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
 
@@ -151,6 +163,40 @@ class Solver:
     @classmethod
     def from_csr(cls, A):
         return cls(A.row_ptr, A.col, A.val)
+
+    @classmethod
+    def from_csr_dist(cls, row_ptr, col, val, n_global, row_begin, nranks, rank):
+        """gmres_create_dist: this rank's rows (local CSR, global columns) of a row-partitioned matrix."""
+        self = cls.__new__(cls)
+        self._lib = load_library()
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        self.n = self.row_ptr.shape[0] - 1
+        self.nnz = int(col.shape[0])
+        self.row_begin, self.n_global, self.nranks, self.rank = int(row_begin), int(n_global), int(nranks), int(rank)
+        h = ctypes.c_void_p()
+        rc = self._lib.gmres_create_dist(_p(self.row_ptr), _p(col), _p(val), self.n_global, self.row_begin, self.n,
+                                         self.nranks, self.rank, ctypes.byref(h))
+        if rc != 0:
+            raise GmresError(rc, self._lib.gmres_last_error(None).decode())
+        self._h = h
+        return self
+
+    def export_blob(self) -> bytes:
+        """gmres_dist_export: ghost list + CUDA IPC handles of this rank (to all-gather)."""
+        ln = ctypes.c_int64()
+        self._ck(self._lib.gmres_dist_export(self._h, None, 0, ctypes.byref(ln)))
+        buf = np.zeros(ln.value, np.uint8)
+        self._ck(self._lib.gmres_dist_export(self._h, _p(buf), buf.size, ctypes.byref(ln)))
+        return buf.tobytes()
+
+    def import_blobs(self, blobs):
+        """gmres_dist_import: the blobs of all ranks, in rank order."""
+        off = np.zeros(len(blobs) + 1, np.int64)
+        off[1:] = np.cumsum([len(b) for b in blobs])
+        cat = np.frombuffer(b"".join(blobs), np.uint8).copy()
+        self._ck(self._lib.gmres_dist_import(self._h, _p(cat), _p(off)))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -282,3 +328,80 @@ class Solver:
         self._ck(self._lib.gmres_k_hessenberg(self._h, int(m), int(J), Hc.ctypes.data_as(ctypes.c_void_p),
                                               float(beta), _p(R), _p(s), _p(y)))
         return R.reshape(m, m + 1).T, s, y
+
+
+# ------------------------------------------------------------ row partition (§8 e)
+def dist_partition(row_ptr, nranks: int, align: int = 256) -> np.ndarray:
+    """gmres_dist_partition: row boundaries [0, …, n] of an nnz-balanced split at multiples of align (host)."""
+    L = load_library()
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    out = np.zeros(nranks + 1, np.int64)
+    rc = L.gmres_dist_partition(_p(rp), rp.size - 1, int(nranks), int(align), _p(out))
+    if rc != 0:
+        raise GmresError(rc, L.gmres_last_error(None).decode())
+    return out
+
+
+def dist_ghosts(row_ptr, col, row_begin: int) -> np.ndarray:
+    """gmres_dist_ghosts: sorted global columns of a rank's local rows outside them (host)."""
+    L = load_library()
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    c = np.ascontiguousarray(col, np.int32)
+    cnt = ctypes.c_int64()
+    L.gmres_dist_ghosts(_p(rp), _p(c), rp.size - 1, int(row_begin), None, 0, ctypes.byref(cnt))
+    out = np.zeros(cnt.value, np.int32)
+    rc = L.gmres_dist_ghosts(_p(rp), _p(c), rp.size - 1, int(row_begin), _p(out), out.size, ctypes.byref(cnt))
+    if rc != 0:
+        raise GmresError(rc, L.gmres_last_error(None).decode())
+    return out
+
+
+def dist_sends(row_begin: int, n_local: int, peer_ghosts) -> np.ndarray:
+    """gmres_dist_sends: this rank's local rows a peer gathers (host)."""
+    L = load_library()
+    pg = np.ascontiguousarray(peer_ghosts, np.int32)
+    cnt = ctypes.c_int64()
+    L.gmres_dist_sends(int(row_begin), int(n_local), _p(pg), pg.size, None, 0, ctypes.byref(cnt))
+    out = np.zeros(cnt.value, np.int32)
+    rc = L.gmres_dist_sends(int(row_begin), int(n_local), _p(pg), pg.size, _p(out), out.size, ctypes.byref(cnt))
+    if rc != 0:
+        raise GmresError(rc, L.gmres_last_error(None).decode())
+    return out
+
+
+def split_rows(A, bounds):
+    """Local CSR pieces (row_ptr, col, val) of the row blocks [bounds[q], bounds[q+1]) (global columns)."""
+    parts = []
+    for q in range(len(bounds) - 1):
+        r0, r1 = int(bounds[q]), int(bounds[q + 1])
+        e0, e1 = int(A.row_ptr[r0]), int(A.row_ptr[r1])
+        parts.append((A.row_ptr[r0:r1 + 1] - e0, A.col[e0:e1], A.val[e0:e1]))
+    return parts
+
+
+def link_local(solvers):
+    """gmres_dist_link_local: in-process ranks on one device."""
+    L = load_library()
+    arr = (ctypes.c_void_p * len(solvers))(*[s._h.value for s in solvers])
+    rc = L.gmres_dist_link_local(arr, len(solvers))
+    if rc != 0:
+        raise GmresError(rc, L.gmres_last_error(solvers[0]._h).decode())
+
+
+def solve_virtual(solvers, bs, xs, x0s=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None,
+                  max_cycles=None, lanes=0, tune=0):
+    """gmres_solve_virtual: all in-process ranks in one cooperative launch (torch float64 tensors)."""
+    L = load_library()
+    P = len(solvers)
+    H = (ctypes.c_void_p * P)(*[s._h.value for s in solvers])
+    B = (ctypes.c_void_p * P)(*[b.data_ptr() for b in bs])
+    X = (ctypes.c_void_p * P)(*[x.data_ptr() for x in xs])
+    X0 = None if x0s is None else (ctypes.c_void_p * P)(*[x.data_ptr() for x in x0s])
+    res = (_Result * P)()
+    o = Solver._opts(delta, max_cycles, False, lanes, 0, False, tune)
+    rc = L.gmres_solve_virtual(H, P, B, X0, X, int(m), float(tol), _ortho(ortho), _prec(precision), ctypes.byref(o),
+                               res)
+    if rc < 0:
+        raise GmresError(rc, L.gmres_last_error(solvers[0]._h).decode())
+    return [SolveResult(r.status, r.cycles, r.inner_iters, r.final_relres, r.device_ms, np.zeros(0),
+                        kernel_ms=r.kernel_ms) for r in res]
