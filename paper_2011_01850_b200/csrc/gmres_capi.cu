@@ -58,10 +58,19 @@ struct gmres_ctx {
   int hist_cap = 0;
   double* d_inner = nullptr;
   int inner_cap = 0;
+  // current row partition over the grid (aliases of an entry of `parts`)
   int* d_row_begin = nullptr;
   int4* d_chunks = nullptr;
   int* d_chunk_off = nullptr;
   int part_G = 0, part_align = 0;
+  struct Part {  // cached partitions: MGS (32-row) and CGSR (block-aligned) solves alternate
+    int G, align, max_rows;
+    int* d_row_begin;
+    int4* d_chunks;
+    int* d_chunk_off;
+    int* d_send;
+  };
+  std::vector<Part> parts;
   int part_max_rows = 0;  // largest CTA row block of the partition
   // last solve
   std::vector<double> inner_host;
@@ -88,7 +97,6 @@ struct gmres_ctx {
   unsigned long long* peer_ctr[MAXR] = {};
   std::vector<std::vector<int32_t>> send_rows;  // per peer: local rows it gathers (sorted)
   int* d_send = nullptr;                // [G+1] offsets, rows, peers (rebuilt with the partition)
-  int send_G = -1, send_align = -1;
   bool dist() const { return nranks > 1; }
 };
 
@@ -308,53 +316,74 @@ void make_chunks(const std::vector<int32_t>& rp, int64_t n, const std::vector<in
   off[G] = (int)ent.size();
 }
 
-int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
-  if (ctx->part_G == G && ctx->part_align == align && ctx->d_row_begin) return 0;
-  std::vector<int> rb;
-  make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, align, rb);
-  ctx->part_max_rows = 0;
-  for (int g = 0; g < G; ++g) ctx->part_max_rows = std::max(ctx->part_max_rows, rb[g + 1] - rb[g]);
-  std::vector<int4> ent;
-  std::vector<int> off;
-  make_chunks(ctx->h_rp, ctx->n, rb, ent, off);
-  cudaFree(ctx->d_row_begin);
-  cudaFree(ctx->d_chunks);
-  cudaFree(ctx->d_chunk_off);
+void free_parts(gmres_ctx* ctx) {
+  for (auto& p : ctx->parts) {
+    cudaFree(p.d_row_begin);
+    cudaFree(p.d_chunks);
+    cudaFree(p.d_chunk_off);
+    cudaFree(p.d_send);
+  }
+  ctx->parts.clear();
   ctx->d_row_begin = nullptr;
   ctx->d_chunks = nullptr;
   ctx->d_chunk_off = nullptr;
-  CK(cudaMalloc(&ctx->d_row_begin, sizeof(int) * (G + 1)));
-  CK(cudaMemcpy(ctx->d_row_begin, rb.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&ctx->d_chunks, sizeof(int4) * ent.size()));
-  CK(cudaMemcpy(ctx->d_chunks, ent.data(), sizeof(int4) * ent.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&ctx->d_chunk_off, sizeof(int) * (G + 1)));
-  CK(cudaMemcpy(ctx->d_chunk_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
-  ctx->part_G = G;
-  ctx->part_align = align;
+  ctx->d_send = nullptr;
+  ctx->part_G = 0;
+}
+
+int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
+  for (auto& p : ctx->parts) {
+    if (p.G == G && p.align == align) {
+      ctx->d_row_begin = p.d_row_begin;
+      ctx->d_chunks = p.d_chunks;
+      ctx->d_chunk_off = p.d_chunk_off;
+      ctx->d_send = p.d_send;
+      ctx->part_G = G;
+      ctx->part_align = align;
+      ctx->part_max_rows = p.max_rows;
+      return 0;
+    }
+  }
+  if (ctx->parts.size() >= 4) free_parts(ctx);
+  std::vector<int> rb;
+  make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, align, rb);
+  gmres_ctx::Part P{G, align, 0, nullptr, nullptr, nullptr, nullptr};
+  for (int g = 0; g < G; ++g) P.max_rows = std::max(P.max_rows, rb[g + 1] - rb[g]);
+  std::vector<int4> ent;
+  std::vector<int> off;
+  make_chunks(ctx->h_rp, ctx->n, rb, ent, off);
+  auto bail = [&](cudaError_t e) {
+    cudaFree(P.d_row_begin); cudaFree(P.d_chunks); cudaFree(P.d_chunk_off); cudaFree(P.d_send);
+    return fail(ctx, e == cudaErrorMemoryAllocation ? GMRES_ENOMEM : GMRES_ECUDA, cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaMalloc(&P.d_row_begin, sizeof(int) * (G + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(P.d_row_begin, rb.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&P.d_chunks, sizeof(int4) * ent.size());
+  if (e == cudaSuccess) e = cudaMemcpy(P.d_chunks, ent.data(), sizeof(int4) * ent.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&P.d_chunk_off, sizeof(int) * (G + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(P.d_chunk_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return bail(e);
   if (ctx->dist() && ctx->linked) {  // per-CTA send lists (halo push)
-    std::vector<std::pair<int, int>> ent;  // (local row, peer)
+    std::vector<std::pair<int, int>> se;  // (local row, peer)
     for (int q = 0; q < ctx->nranks; ++q)
-      for (int32_t r : ctx->send_rows[q]) ent.push_back({r, q});
-    std::sort(ent.begin(), ent.end());
-    std::vector<int> buf(G + 1 + 2 * ent.size());
+      for (int32_t r : ctx->send_rows[q]) se.push_back({r, q});
+    std::sort(se.begin(), se.end());
+    std::vector<int> buf(G + 1 + 2 * se.size());
     // offsets: CTA g pushes the entries with rb[g] <= row < rb[g+1]
     for (int g = 0; g <= G; ++g) {
-      const int lo = g == G ? (int)ent.size()
-                            : (int)(std::lower_bound(ent.begin(), ent.end(), std::make_pair(rb[g], -1)) - ent.begin());
-      buf[g] = lo;
+      buf[g] = g == G ? (int)se.size()
+                      : (int)(std::lower_bound(se.begin(), se.end(), std::make_pair(rb[g], -1)) - se.begin());
     }
-    for (size_t i = 0; i < ent.size(); ++i) {
-      buf[G + 1 + i] = ent[i].first;
-      buf[G + 1 + ent.size() + i] = ent[i].second;
+    for (size_t i = 0; i < se.size(); ++i) {
+      buf[G + 1 + i] = se[i].first;
+      buf[G + 1 + se.size() + i] = se[i].second;
     }
-    cudaFree(ctx->d_send);
-    ctx->d_send = nullptr;
-    CK(cudaMalloc(&ctx->d_send, sizeof(int) * std::max<size_t>(buf.size(), 1)));
-    CK(cudaMemcpy(ctx->d_send, buf.data(), sizeof(int) * buf.size(), cudaMemcpyHostToDevice));
-    ctx->send_G = G;
-    ctx->send_align = align;
+    e = cudaMalloc(&P.d_send, sizeof(int) * std::max<size_t>(buf.size(), 1));
+    if (e == cudaSuccess) e = cudaMemcpy(P.d_send, buf.data(), sizeof(int) * buf.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(e);
   }
-  return 0;
+  ctx->parts.push_back(P);
+  return ensure_partition(ctx, G, align);
 }
 
 // workspace for (m, prec, G); zero-filled so that padding rows stay 0
@@ -641,9 +670,7 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_ws);
   cudaFree(ctx->d_hb);
   cudaFree(ctx->d_hx);
-  cudaFree(ctx->d_row_begin);
-  cudaFree(ctx->d_chunks);
-  cudaFree(ctx->d_chunk_off);
+  free_parts(ctx);
   if (ctx->ipc) {
     for (int q = 0; q < ctx->nranks; ++q) {
       if (q == ctx->rank) continue;
@@ -660,7 +687,6 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_dslots);
   cudaFree(ctx->d_dctr);
   cudaFree(ctx->d_epoch);
-  cudaFree(ctx->d_send);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evk0) cudaEventDestroy(ctx->evk0);
@@ -925,7 +951,7 @@ struct BlobHdr {
   int64_t row_begin, n_local, n_global, n_ghost;
   cudaIpcMemHandle_t h[5];  // w0, w1, x, all-reduce partials, arrival counter
 };
-void relink(gmres_ctx* c) { c->part_G = 0; c->linked = true; }
+void relink(gmres_ctx* c) { free_parts(c); c->linked = true; }
 }  // namespace
 
 int gmres_dist_ghosts(const int32_t* row_ptr, const int32_t* col, int64_t n_local, int64_t row_begin, int32_t* ghosts,

@@ -111,3 +111,51 @@ def test_dist_errors():
     G.link_local(S)
     with pytest.raises(G.GmresError):   # virtual ranks are solved together
         S[0].solve_device(b, torch.zeros_like(b))
+
+
+def _ipc_worker(rank, port, errq):
+    import os
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        A = inputs.make("C2", 16).A
+        bounds = G.dist_partition(A.row_ptr, 2, 256)
+        rp, c, v = G.split_rows(A, bounds)[rank]
+        S = G.Solver.from_csr_dist(rp, c, v, A.n, bounds[rank], 2, rank)
+        blobs = [None, None]
+        dist.all_gather_object(blobs, S.export_blob())
+        S.import_blobs(blobs)        # opens the peer's CUDA IPC handles
+        dist.barrier()
+        S.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException as e:
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+def test_ipc_export_import_two_processes():
+    """One process per GPU plumbing: blobs (ghosts + CUDA IPC handles) exchanged and
+    opened by two processes.  (Both share cuda:0 here, so no solve is launched:
+    kernels of different processes that wait on one another must not share a GPU.)"""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, port, errq)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(180)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(p.exitcode == 0 for p in ps)
