@@ -104,6 +104,14 @@ int gmres_get_cycle_iters(gmres_ctx* ctx, int32_t* buf, int32_t cap, int32_t* le
  * over CTAs of the CTA's own SpMV time.  Returns the count written. */
 int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap);
 
+/* Instrumentation (outside any timed region): copy columns [col0, col0+ncols)
+ * of the Krylov basis V left by the last solve on ctx — the basis of its last
+ * cycle, v_1..v_J in columns 0..J−1 — into d_dst (device, column-major,
+ * leading dimension ld ≥ n, element type = that solve's working precision:
+ * float for mixed, double for fp64).  Used for ‖I − VᵀV‖ (BASELINE.json C5).
+ * EINVAL before any solve or for columns outside [0, m]. */
+int gmres_get_basis(gmres_ctx* ctx, int32_t col0, int32_t ncols, void* d_dst, int64_t ld);
+
 /* ------------------------------------------------------------------------
  * Row-partitioned solve over P ranks (the paper's future work,
  * PAPER.md:491-495).  Rank q owns the contiguous global rows

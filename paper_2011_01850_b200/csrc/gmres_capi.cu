@@ -18,6 +18,9 @@
 
 using namespace g200;
 
+// V layout of a solve (gmres_kernels.cuh Dev): column-major (tb = 0) or row-blocked
+struct VLayout { int tb = 0, tp = 0, lg = 0; long long bs = 0; };
+
 struct gmres_ctx {
   int device = 0;
   int sms = 0;
@@ -77,6 +80,9 @@ struct gmres_ctx {
   std::vector<int32_t> cycJ_host;
   double phase_ns[PH_N] = {0};
   std::string err;
+  // basis of the last solve (gmres_get_basis): layout, m, precision
+  int last_m = 0, last_prec = -1;
+  VLayout last_vl;
   // ---- row partition over ranks (gmres_create_dist)
   int nranks = 1, rank = 0;
   int64_t n_global = 0, row_begin = 0;  // this rank owns global rows [row_begin, row_begin + n)
@@ -158,7 +164,6 @@ void make_partition(const std::vector<int32_t>& rp, int64_t n, int64_t nvec, int
 // V layout of a solve (gmres_kernels.cuh Dev): CGSR → row-blocked with the
 // largest power-of-two block height in [32, 256] whose (m+1)-column block fits
 // half the staging region; MGS (and CGSR at very large m) → column-major.
-struct VLayout { int tb = 0, tp = 0, lg = 0; long long bs = 0; };
 VLayout vlayout_for(int ortho, int m, int wb, int tile_bytes) {
   VLayout L;
   if (ortho != GMRES_CGSR) return L;
@@ -835,6 +840,9 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   P.G = G;
   P.smem = smem;
   P.d = d;
+  ctx->last_m = m;
+  ctx->last_prec = precision;
+  ctx->last_vl = vl;
   return 0;
 }
 
@@ -1159,6 +1167,23 @@ int gmres_get_cycle_iters(gmres_ctx* ctx, int32_t* buf, int32_t cap, int32_t* le
   const int n = (int)ctx->cycJ_host.size();
   if (buf) std::memcpy(buf, ctx->cycJ_host.data(), sizeof(int32_t) * std::min(n, std::max(cap, 0)));
   if (len) *len = n;
+  return 0;
+}
+
+int gmres_get_basis(gmres_ctx* ctx, int32_t col0, int32_t ncols, void* d_dst, int64_t ld) {
+  if (!ctx || !d_dst || ctx->last_prec < 0) return fail(ctx, GMRES_EINVAL, "no solve yet / null argument");
+  if (col0 < 0 || ncols < 1 || col0 + ncols > ctx->last_m + 1 || ld < ctx->n)
+    return fail(ctx, GMRES_EINVAL, "columns outside [0, m] or ld < n");
+  const VLayout& vl = ctx->last_vl;
+  if (ctx->last_prec == GMRES_MIXED)
+    unpack_basis_kernel<float><<<ctx->sms * 4, 256, 0, ctx->stream>>>((const float*)ctx->d_V, ctx->ldv, vl.tb, vl.lg,
+                                                                     vl.tp, vl.bs, col0, ncols, ctx->n, (float*)d_dst, ld);
+  else
+    unpack_basis_kernel<double><<<ctx->sms * 4, 256, 0, ctx->stream>>>((const double*)ctx->d_V, ctx->ldv, vl.tb, vl.lg,
+                                                                      vl.tp, vl.bs, col0, ncols, ctx->n, (double*)d_dst,
+                                                                      ld);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 

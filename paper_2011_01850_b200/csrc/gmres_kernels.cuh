@@ -1443,6 +1443,19 @@ __global__ void pack_vblocked_kernel(const W* __restrict__ src, long long ldv, i
   }
 }
 
+// basis columns (either layout) → caller's column-major buffer (instrumentation)
+template <class W>
+__global__ void unpack_basis_kernel(const W* __restrict__ V, long long ldv, int tb, int tb_log, int tp, long long bs,
+                                    int col0, int ncols, long long n, W* __restrict__ dst, long long ld) {
+  const long long tot = n * ncols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n);
+    const long long r = e - (long long)c * n;
+    const long long src = tb ? (r >> tb_log) * bs + (long long)(col0 + c) * tp + (r & (tb - 1)) : (long long)(col0 + c) * ldv + r;
+    dst[(long long)c * ld + r] = V[src];
+  }
+}
+
 // Jacobi M = diag(A) (reading R11): dinv64 = 1/a_ii (fp64), dinv32 = RN32(dinv64).
 __global__ void dinv_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                             const double* __restrict__ a, double* dinv64, float* dinv32, int* bad_row,

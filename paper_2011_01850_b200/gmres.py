@@ -67,6 +67,8 @@ def load_library():
     L.gmres_get_cycle_iters.argtypes = [vp, vp, i32, ctypes.POINTER(i32)]
     L.gmres_get_cycle_iters.restype = ctypes.c_int
     L.gmres_get_phase_ns.argtypes = [vp, vp, i32]
+    L.gmres_get_basis.argtypes = [vp, i32, i32, vp, i64]
+    L.gmres_get_basis.restype = ctypes.c_int
     L.gmres_get_phase_ns.restype = ctypes.c_int
     L.gmres_last_error.argtypes = [vp]
     L.gmres_last_error.restype = ctypes.c_char_p
@@ -284,6 +286,14 @@ class Solver:
                                           ctypes.byref(hl), ctypes.c_void_p(st.cuda_stream))
         out = self._finish(rc, res, hist, hl, record_inner)
         out.x = x
+        return out
+
+    def basis(self, ncols, precision, col0=0):
+        """gmres_get_basis: columns of the last solve's Krylov basis as a (ncols, n) torch tensor."""
+        import torch
+        dt = torch.float32 if _prec(precision) == MIXED else torch.float64
+        out = torch.empty((int(ncols), self.n), dtype=dt, device="cuda")
+        self._ck(self._lib.gmres_get_basis(self._h, int(col0), int(ncols), _p(out), self.n))
         return out
 
     # ------------------------------------------------------ components

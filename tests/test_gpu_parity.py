@@ -335,3 +335,30 @@ def test_full_size(name):
     for prec in (G.MIXED, G.FP64):
         _sampled_spmv_rows(P, S, prec, rng)
     S.close()
+
+
+# ------------------------------------------------------------------ basis getter (C5 orthogonality report)
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])   # column-major / row-blocked basis layouts
+@pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
+def test_basis_matches_oracle_first_cycle(ortho, prec):
+    P = inputs.make("C2", 16)
+    A = P.A
+    S = G.Solver.from_csr(A)
+    m = 20
+    bd = tdev(P.b)
+    xd = torch.zeros_like(bd)
+    r = S.solve_device(bd, xd, m=m, ortho=ortho, precision=prec, max_cycles=1, tol=1e-14, delta=0.0)
+    J = int(r.cycle_iters[0])
+    V = S.basis(J, prec).cpu().numpy().astype(np.float64).T          # n × J
+    aW, dW = O.working_copy(A, prec)
+    r0 = O.resid(prec, A, P.b, np.zeros(A.n), dW)[1]
+    cyc = O.arnoldi(prec, ortho, A, r0, m, 0.0)
+    assert cyc.J == J
+    Vo = cyc.V[:, :J].astype(np.float64)
+    err = np.linalg.norm(V - Vo, axis=0)
+    # fp64: rounding-order differences only; fp32: they grow slowly along the cycle
+    assert np.all(err[:5] <= (1e-12 if prec == G.FP64 else 1e-5)), err[:5]
+    assert np.allclose(np.linalg.norm(V, axis=0), 1.0, atol=1e-12 if prec == G.FP64 else 1e-6)
+    loss = np.abs(np.eye(J) - V.T @ V).max()
+    loss_o = np.abs(np.eye(J) - Vo.T @ Vo).max()
+    assert loss <= 10 * loss_o + (1e-13 if prec == G.FP64 else 1e-6), (loss, loss_o)
