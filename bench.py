@@ -269,11 +269,15 @@ def run_ours(args, rank, world, local_rank):
                           "phase_ms": {k: v / 1e6 for k, v in zip(["resid", "spmv", "ortho", "givens", "update"],
                                                                     r.phase_ns[:5])}}
     achieved = sum(byts) / (sum(kms) * 1e-3) / 1e9
+    # DRAM traffic per launch: the traffic/algorithmic ratio ncu measured for each
+    # variant's launch (profiles/traffic.json) applied to the timed launches
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1:
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            tr = [tj["mgs" if o == 0 else "cgsr"]["ratio"] * mb for (o, _), mb in zip(per, byts)]
+            traffic = sum(tr) / len(tr)
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
