@@ -92,10 +92,14 @@ void cgsr(int64_t n, int j, const W* V, int64_t ldv, W* w, double* h, int passes
   }
 }
 
-// v ← RN_W(w · inv), inv = 1/‖·‖ computed in fp64 (Alg. 1 lines 94, 105).
+// v ← RN_W(w · RN_W(inv)), inv = 1/‖·‖ computed in fp64 (Alg. 1 lines 94, 105):
+// the normalisation is a working-precision scal by the rounded reciprocal —
+// inside the single-precision span of the mixed solver (
+// DESIGN.md reading R21).  In fp64 mode RN_W is the identity.
 template <class W>
 void scale(int64_t n, const W* w, double inv, W* v) {
-  for (int64_t l = 0; l < n; ++l) v[l] = rn<W>((double)w[l] * inv);
+  const W iw = rn<W>(inv);
+  for (int64_t l = 0; l < n; ++l) v[l] = w[l] * iw;
 }
 
 // Back-substitution R y = s (Alg. 1, H⁻¹ s with H upper triangular

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -72,8 +73,13 @@ struct gmres_ctx {
     int4* d_chunks;
     int* d_chunk_off;
     int* d_send;
+    int2* d_stages;
+    int* d_stage_off;
   };
   std::vector<Part> parts;
+  int2* d_stages = nullptr;      // block-stream stages of the current partition
+  int* d_stage_off = nullptr;
+  bool block_ok = false;         // every row has ≤ BS_MAXROW nonzeros: use the block CSR stream
   int part_max_rows = 0;  // largest CTA row block of the partition
   // last solve
   std::vector<double> inner_host;
@@ -321,13 +327,48 @@ void make_chunks(const std::vector<int32_t>& rp, int64_t n, const std::vector<in
   off[G] = (int)ent.size();
 }
 
+// block-stream stages of every CTA's rows (gmres_kernels.cuh csr_block_stream):
+// ≤ BS_BYTES of row_ptr / per-row operand / col / val slices at the widest types
+// (fp64 values and operand), boundaries at multiples of 4 rows
+void make_stages(const std::vector<int32_t>& rp, int64_t n, const std::vector<int>& rb, std::vector<int2>& ent,
+                 std::vector<int>& off) {
+  const int G = (int)rb.size() - 1;
+  auto bytes = [&](int64_t s, int64_t e) {
+    const int64_t rows = e - s, ea = rp[s] & ~3LL, eb = (rp[e] + 3) & ~3LL;
+    return ((rows + 1 + 3) & ~3LL) * 4 + ((rows * 8 + 15) & ~15LL) + (eb - ea) * 12;
+  };
+  ent.clear();
+  off.assign(G + 1, 0);
+  for (int g = 0; g < G; ++g) {
+    off[g] = (int)ent.size();
+    const int64_t r0 = std::min<int64_t>(rb[g], n), r1 = std::min<int64_t>(rb[g + 1], n);
+    int64_t s = r0;
+    while (s < r1) {
+      int64_t e = std::min(s + 4, r1);
+      while (e < r1) {
+        const int64_t e2 = std::min(e + 4, r1);
+        if (bytes(s, e2) > BS_BYTES) break;
+        e = e2;
+      }
+      ent.push_back(make_int2((int)s, rp[s]));
+      s = e;
+    }
+    ent.push_back(make_int2((int)r1, rp[r1]));  // sentinel
+  }
+  off[G] = (int)ent.size();
+}
+
 void free_parts(gmres_ctx* ctx) {
   for (auto& p : ctx->parts) {
     cudaFree(p.d_row_begin);
     cudaFree(p.d_chunks);
     cudaFree(p.d_chunk_off);
     cudaFree(p.d_send);
+    cudaFree(p.d_stages);
+    cudaFree(p.d_stage_off);
   }
+  ctx->d_stages = nullptr;
+  ctx->d_stage_off = nullptr;
   ctx->parts.clear();
   ctx->d_row_begin = nullptr;
   ctx->d_chunks = nullptr;
@@ -343,6 +384,8 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
       ctx->d_chunks = p.d_chunks;
       ctx->d_chunk_off = p.d_chunk_off;
       ctx->d_send = p.d_send;
+      ctx->d_stages = p.d_stages;
+      ctx->d_stage_off = p.d_stage_off;
       ctx->part_G = G;
       ctx->part_align = align;
       ctx->part_max_rows = p.max_rows;
@@ -352,13 +395,14 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
   if (ctx->parts.size() >= 4) free_parts(ctx);
   std::vector<int> rb;
   make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, align, rb);
-  gmres_ctx::Part P{G, align, 0, nullptr, nullptr, nullptr, nullptr};
+  gmres_ctx::Part P{G, align, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   for (int g = 0; g < G; ++g) P.max_rows = std::max(P.max_rows, rb[g + 1] - rb[g]);
   std::vector<int4> ent;
   std::vector<int> off;
   make_chunks(ctx->h_rp, ctx->n, rb, ent, off);
   auto bail = [&](cudaError_t e) {
     cudaFree(P.d_row_begin); cudaFree(P.d_chunks); cudaFree(P.d_chunk_off); cudaFree(P.d_send);
+    cudaFree(P.d_stages); cudaFree(P.d_stage_off);
     return fail(ctx, e == cudaErrorMemoryAllocation ? GMRES_ENOMEM : GMRES_ECUDA, cudaGetErrorString(e));
   };
   cudaError_t e = cudaMalloc(&P.d_row_begin, sizeof(int) * (G + 1));
@@ -368,6 +412,16 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
   if (e == cudaSuccess) e = cudaMalloc(&P.d_chunk_off, sizeof(int) * (G + 1));
   if (e == cudaSuccess) e = cudaMemcpy(P.d_chunk_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return bail(e);
+  if (ctx->block_ok) {
+    std::vector<int2> st;
+    std::vector<int> soff;
+    make_stages(ctx->h_rp, ctx->n, rb, st, soff);
+    e = cudaMalloc(&P.d_stages, sizeof(int2) * st.size());
+    if (e == cudaSuccess) e = cudaMemcpy(P.d_stages, st.data(), sizeof(int2) * st.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P.d_stage_off, sizeof(int) * (G + 1));
+    if (e == cudaSuccess) e = cudaMemcpy(P.d_stage_off, soff.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(e);
+  }
   if (ctx->dist() && ctx->linked) {  // per-CTA send lists (halo push)
     std::vector<std::pair<int, int>> se;  // (local row, peer)
     for (int q = 0; q < ctx->nranks; ++q)
@@ -515,6 +569,9 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.row_begin = ctx->d_row_begin;
   d.chunks = ctx->d_chunks;
   d.chunk_off = ctx->d_chunk_off;
+  d.stages = ctx->d_stages;
+  d.stage_off = ctx->d_stage_off;
+  d.block_stream = (ctx->block_ok && ctx->d_stages) ? 1 : 0;
   d.history = ctx->d_hist;
   d.cycle_J = ctx->d_cycJ;
   d.hist_cap = ctx->hist_cap;
@@ -588,6 +645,11 @@ int create_impl(const int32_t* row_ptr, const int32_t* col, const double* val, i
   ctx->nvec = round_up(n, VEC_ALIGN);
   ctx->ldv = ctx->nvec;
   ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
+  {
+    int64_t mx = 0;
+    for (int64_t i = 0; i < n; ++i) mx = std::max<int64_t>(mx, row_ptr[i + 1] - row_ptr[i]);
+    ctx->block_ok = mx <= BS_MAXROW && !std::getenv("G200_NO_BLOCK_STREAM");
+  }
   ctx->nranks = nranks;
   ctx->rank = rank;
   ctx->n_global = n_global;

@@ -44,6 +44,10 @@ constexpr int ST_OFF_A = ST_OFF_CI + (CHUNK_CAP + 8) * 4;   // 1472: col slice, 
 template <class AT> __host__ __device__ constexpr int NSTG() { return sizeof(AT) == 4 ? 4 : 3; }
 template <class AT> __host__ __device__ constexpr int stage_bytes() { return ST_OFF_A + (CHUNK_CAP + 8) * (int)sizeof(AT); }
 constexpr int MAXSTG = 4;
+// block stream (short-row matrices): a ring of NBS per-CTA stages of BS_BYTES each
+constexpr int NBS = 3;
+constexpr int BS_BYTES = 57344;
+constexpr int BS_MAXROW = 64;  // longest row the block stream takes (else the chunk stream)
 constexpr int TILE_BYTES = NGRP * 3 * (ST_OFF_A + (CHUNK_CAP + 8) * 8);  // 172032 (≥ the fp32 ring, 161792)
 constexpr int MAX_M = 256;                               // restart length limit (shared-memory bound)
 constexpr int ARR_PAD = 8;   // elements of slack after rp/col/val (TMA rounds up to 16 B)
@@ -115,6 +119,9 @@ struct Dev {
   int* abort_flag;
   int* err_flag;
   const int* row_begin; // G+1 row boundaries (multiples of ROWALIGN, last = nvec)
+  const int2* stages;   // block stream: per-CTA stages {row_begin, nnz_begin} + a sentinel
+  const int* stage_off; // G+1 offsets into stages
+  int block_stream;     // != 0: the CSR stream runs csr_block_stream (rows ≤ BS_MAXROW nnz)
   const int4* chunks;   // CSR chunks {row_begin, nnz_begin, direct, 0}; per CTA a sentinel
   const int* chunk_off; // G+1 offsets into chunks (CTA g: [off[g], off[g+1]-1) + sentinel)
   double tol, delta;
@@ -225,6 +232,9 @@ struct Shm {
   unsigned long long mbar[NGRP][MAXSTG];  // TMA stage barriers (per CSR-stream group)
   unsigned long long mbar_v[3];      // TMA barriers of the resident-MGS basis buffers
   unsigned long long mbar_t[3];      // TMA barriers of the row-tile passes' V tiles
+  unsigned long long mbar_b[NBS];    // TMA barriers of the block stream's stages
+  int bcnt[NBS];                     // warps done with a block-stream stage
+  unsigned bphase;                   // bit s: parity of the next completion of mbar_b[s]
   unsigned tma_phase[NGRP];          // bit s: parity of the next completion of stage s
   unsigned vphase;                   // bit b: parity of the next completion of mbar_v[b]
   unsigned tphase;                   // bit b: parity of the next completion of mbar_t[b]
@@ -270,6 +280,8 @@ __device__ __forceinline__ void init_shm(Shm& sh, int cta) {
     for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_v[b], 1);
     for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_t[b], 1);
     sh.tphase = 0;
+    for (int b = 0; b < NBS; ++b) { mbar_init(&sh.mbar_b[b], 1); sh.bcnt[b] = 0; }
+    sh.bphase = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -722,6 +734,147 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
   __syncthreads();
 }
 
+// ---------------------------------------------------- block CSR stream (a1, a2)
+// For matrices whose rows are short (≤ BS_MAXROW nonzeros: the stencils), the
+// CTA's rows are cut (on the host) into stages of ≤ BS_BYTES of row_ptr,
+// per-row operand (Jacobi), col and val slices — four large bulk copies per
+// stage (the per-warp 32-row chunks of csr_stream cost four ≤ 1 KB copies
+// each, and bulk copies are paced by the TMA engine at ~20–40 ns per copy:
+// tools/tma_bench.cu).  All 16 warps consume a stage, each a contiguous
+// sixteenth of its rows, L lanes per row; the warp that finishes a stage last
+// (shared counter) issues the copies of the stage NBS ahead into its slot.
+template <class AT, int L, class RT, class Gather, class Pre, class Epi>
+__device__ void csr_block_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __restrict__ vals,
+                                 const RT* __restrict__ rowv, Gather gat, Pre pre, Epi epi) {
+  using Ops = AccOps<AT>;
+  using PT = decltype(pre(0, (RT)0));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int s0 = d.stage_off[sh.cta], ns = d.stage_off[sh.cta + 1] - 1 - s0;
+  const int gro = (int)d.row_base;
+  constexpr int GB = 8;
+  unsigned ph = sh.bphase;
+  struct Geo { int rb, rows, ea, o_rv, o_ci, o_va; unsigned b_rp, b_rv, b_ci, b_va; };
+  auto geo = [&](int k) {
+    const int2 e = d.stages[s0 + k], f = d.stages[s0 + k + 1];
+    Geo g;
+    g.rb = e.x;
+    g.rows = f.x - e.x;
+    g.ea = e.y & ~3;
+    const int eb = (f.y + 3) & ~3;
+    g.b_rp = (unsigned)(((g.rows + 1 + 3) & ~3) * 4);
+    g.b_rv = (unsigned)((g.rows * (int)sizeof(RT) + 15) & ~15);
+    g.b_ci = (unsigned)((eb - g.ea) * 4);
+    g.b_va = (unsigned)((eb - g.ea) * (int)sizeof(AT));
+    g.o_rv = (int)g.b_rp;
+    g.o_ci = g.o_rv + (int)g.b_rv;
+    g.o_va = g.o_ci + (int)g.b_ci;
+    return g;
+  };
+  auto issue = [&](int k) {  // one thread
+    const Geo g = geo(k);
+    const int slot = k % NBS;
+    char* st = s_stage + slot * BS_BYTES;
+    unsigned long long* bar = &sh.mbar_b[slot];
+    mbar_expect_tx(bar, g.b_rp + g.b_rv + g.b_ci + g.b_va);
+    tma_load_1d(st, d.rp + g.rb, g.b_rp, bar);
+    tma_load_1d(st + g.o_rv, rowv + g.rb, g.b_rv, bar);
+    if (g.b_ci) {
+      tma_load_1d(st + g.o_ci, d.ci + g.ea, g.b_ci, bar);
+      tma_load_1d(st + g.o_va, vals + g.ea, g.b_va, bar);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NBS && k < ns; ++k) issue(k);
+  for (int k = 0; k < ns; ++k) {
+    const int slot = k % NBS;
+    {
+      const unsigned par = (ph >> slot) & 1u;
+      ph ^= (1u << slot);
+      if (!mbar_try_wait(&sh.mbar_b[slot], par)) {
+        const unsigned long long t0 = globaltimer();
+        while (!mbar_try_wait(&sh.mbar_b[slot], par))
+          if ((long long)(globaltimer() - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); break; }
+      }
+    }
+    const Geo g = geo(k);
+    const char* st = s_stage + slot * BS_BYTES;
+    const int* srp = reinterpret_cast<const int*>(st);
+    const RT* srv = reinterpret_cast<const RT*>(st + g.o_rv);
+    const int* sci = reinterpret_cast<const int*>(st + g.o_ci);
+    const AT* sa = reinterpret_cast<const AT*>(st + g.o_va);
+    const int wa = (warp * g.rows) / NW, wb = ((warp + 1) * g.rows) / NW;
+    const int sub = lane / L, ln = lane & (L - 1);
+    constexpr int RPP = 32 / L;  // rows per pass of the warp
+    // two passes' rows at once per lane: both rows' gathers are in flight together
+    for (int r0 = wa; r0 < wb; r0 += 2 * RPP) {
+      int r[2], p[2], q[2];
+      bool act[2];
+      PT pv[2];
+      AT acc[2], dg[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        r[t] = r0 + sub + t * RPP;
+        act[t] = r[t] < wb;
+        pv[t] = PT{};
+        if (act[t] && ln == 0) pv[t] = pre(g.rb + r[t], srv[r[t]]);
+        p[t] = act[t] ? srp[r[t]] - g.ea + ln : 0;
+        q[t] = act[t] ? srp[r[t] + 1] - g.ea : 0;
+        acc[t] = (AT)0;
+        dg[t] = (AT)0;
+      }
+      while (p[0] < q[0] || p[1] < q[1]) {
+        AT gv[2][GB], av[2][GB];
+        int cc[2][GB];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int u = 0; u < GB; ++u) {
+            const int e = p[t] + u * L;
+            const bool ok = e < q[t];
+            cc[t][u] = ok ? sci[e] : -1;
+            gv[t][u] = ok ? gat(cc[t][u]) : (AT)0;
+            av[t][u] = ok ? sa[e] : (AT)0;
+          }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+#pragma unroll
+          for (int u = 0; u < GB; ++u) {
+            if (p[t] + u * L < q[t]) acc[t] = Ops::add(acc[t], Ops::mul(av[t][u], gv[t][u]));
+            if (cc[t][u] == g.rb + r[t] + gro) dg[t] = gv[t][u];
+          }
+          p[t] += GB * L;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) {
+          acc[t] = Ops::add(acc[t], __shfl_xor_sync(0xffffffffu, acc[t], o));
+          dg[t] += __shfl_xor_sync(0xffffffffu, dg[t], o);
+        }
+        if (act[t] && ln == 0) epi(g.rb + r[t], acc[t], pv[t], dg[t]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {  // the last warp done with stage k refills its slot
+      if (atomicAdd(&sh.bcnt[slot], 1) == NW - 1) {
+        sh.bcnt[slot] = 0;
+        if (k + NBS < ns) issue(k + NBS);
+      }
+    }
+  }
+  if (threadIdx.x == 0) sh.bphase = ph;  // every thread read it at entry, before the barrier below
+  fence_proxy_async_global();
+  __syncthreads();
+}
+
+template <class AT, int L, class RT, class Gather, class Pre, class Epi>
+__device__ __forceinline__ void csr_any_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __restrict__ vals,
+                                               const RT* __restrict__ rowv, Gather gat, Pre pre, Epi epi) {
+  if (d.block_stream) csr_block_stream<AT, L>(d, sh, s_stage, vals, rowv, gat, pre, epi);
+  else csr_stream<AT, L>(d, sh, s_stage, vals, rowv, gat, pre, epi);
+}
+
 // ------------------------------------------------------------------ a1
 // Alg. 1 lines 86–90: z = b − A64 x in fp64, then
 // r = RN_W(dinv_W · RN_W(z)) (reading R10).  fp64 row sums.
@@ -744,26 +897,28 @@ __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict_
     r_out[row] = ri;
     rr += (double)ri * (double)ri;
   };
-  csr_stream<double, L>(d, sh, s_stage, d.a64, dinv, gat, pre, epi);
+  csr_any_stream<double, L>(d, sh, s_stage, d.a64, dinv, gat, pre, epi);
 }
 
 // ------------------------------------------------------------------ a2
-// Alg. 1: w = RN_W(dinv_W ∘ (A_W v_j)), with v_j = RN_W(src · inv)
-// formed on the fly from the unnormalised previous vector (line 105 fused
-// into the gather: identical bits to normalising first).  The epilogue also
-// stores the CTA's own rows of v_j into V[:, j−1].
+// Alg. 1: w = RN_W(dinv_W ∘ (A_W v_j)), with v_j = RN_W(src · RN_W(inv))
+// (reading R21: a working-precision scal by the rounded reciprocal) formed on
+// the fly from the unnormalised previous vector (line 105 fused into the
+// gather: identical bits to normalising first).  The epilogue also stores the
+// CTA's own rows of v_j into V[:, j−1].
 template <class W, int L>
 __device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
                            W* __restrict__ dst, W* __restrict__ V, int vc) {
   const W* dinv = (const W*)d.dinvW;
   const W* __restrict__ srcg = src - d.row_base;  // global-index view (CSR columns are global)
-  auto gat = [&](int col) -> W { return RN<W>((double)srcg[col] * inv); };
+  const W invW = RN<W>(inv);
+  auto gat = [&](int col) -> W { return mulw(srcg[col], invW); };
   auto pre = [&](int, W di) -> W { return di; };
   auto epi = [&](int row, W acc, W di, W vj) {
     dst[row] = mulw(di, acc);
     if (V) *v_at(d, V, row, vc) = vj;  // v_j at the diagonal = RN_W(src_row · inv), gathered above
   };
-  csr_stream<W, L>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, epi);
+  csr_any_stream<W, L>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, epi);
 }
 
 // ------------------------------------------------------------------ a3
@@ -1547,7 +1702,7 @@ __global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int ite
       auto gat = [&](int) -> W { return (W)1; };
       auto pre = [&](int, W di) -> W { return di; };
       auto epi = [&](int row, W a, W di, W) { w[row] = mulw(di, a); };
-      csr_stream<W, 1>(d, sh, s_tiles, (const W*)d.aW, dinv, gat, pre, epi);
+      csr_any_stream<W, 1>(d, sh, s_tiles, (const W*)d.aW, dinv, gat, pre, epi);
     } else if (what == 7) {  // full SpMV phase (gathers from V column 0), L = 1
       spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, (W*)nullptr, 0);
     } else if (what == 8) {  // ... plus the fused V-column write (as in the solve)
