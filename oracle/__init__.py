@@ -73,6 +73,9 @@ def lib():
         L.oracle_gmres_solve.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, dbl, i32, i32, dbl, i32, i32,
                                          vp, vp, ctypes.c_int32, vp, ctypes.c_int32]
         L.oracle_gmres_solve.restype = i32
+        L.oracle_gmres_solve_policy.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, dbl, i32, i32, dbl, i32, i32,
+                                                vp, vp, ctypes.c_int32, vp, ctypes.c_int32, i32, dbl, dbl]
+        L.oracle_gmres_solve_policy.restype = i32
         _lib = L
     return _lib
 
@@ -258,19 +261,23 @@ class SolveResult:
     final_relres: float
 
 
+THRESHOLD, TWOSTAGE, STALL = 0, 1, 2   # restart policies (oracle.h; R6, R22)
+
+
 def solve(A, b, x0=None, m=30, tol=1e-10, ortho=CGSR, prec=MIXED, delta=None, max_cycles=10000, flags=0,
-          inner_cap=200000):
+          inner_cap=200000, policy=THRESHOLD, stall_factor=1.001, stall_frac=0.05):
     if delta is None:
-        delta = 1e-6 if prec == MIXED else 0.0
+        delta = 1e-6 if (prec == MIXED and policy != STALL) else 0.0
     n = A.n
     x = np.zeros(n)
     hist = np.zeros(max_cycles + 2)
     inner = np.zeros(inner_cap)
     res = _Result()
     x0c = None if x0 is None else _c(x0, np.float64)
-    rc = lib().oracle_gmres_solve(n, _p(A.row_ptr), _p(A.col), _p(_c(A.val, np.float64)), _p(_c(b, np.float64)),
-                                  _p(x0c), _p(x), m, tol, ortho, prec, delta, max_cycles, flags,
-                                  ctypes.byref(res), _p(hist), hist.size, _p(inner), inner.size)
+    rc = lib().oracle_gmres_solve_policy(n, _p(A.row_ptr), _p(A.col), _p(_c(A.val, np.float64)),
+                                         _p(_c(b, np.float64)), _p(x0c), _p(x), m, tol, ortho, prec, delta,
+                                         max_cycles, flags, ctypes.byref(res), _p(hist), hist.size, _p(inner),
+                                         inner.size, int(policy), float(stall_factor), float(stall_frac))
     if rc < 0:
         raise RuntimeError(f"oracle_gmres_solve error {rc}")
     return SolveResult(rc, x, res.cycles, res.inner_iters, hist[:min(res.history_len, hist.size)].copy(),

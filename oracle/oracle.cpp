@@ -283,10 +283,16 @@ void oracle_xupdate(int prec, int64_t n, int J, const void* V, int64_t ldv, cons
 namespace {
 
 // One Arnoldi cycle: Alg. 1 lines 92–141.
+// Restart conditions (reading R6 + R22): j = jmax, lucky breakdown,
+// |s_{j+1}| ≤ thr, or — with stall_w > 0 — stall: the Arnoldi residual improved
+// by less than a factor stall_factor over the last stall_w inner iterations
+// (1.001 over 5 % of the restart length).
 template <class W>
 int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* ci, const W* aW, const W* dinvW,
             const W* r, int m, double thr, W* V, int64_t ldv, double* Hbar, double* R, double* s, int32_t* Jout,
-            int32_t* bd_out, double* inner_hist) {
+            int32_t* bd_out, double* inner_hist, int jmax = 0, int stall_w = 0, double stall_factor = 1.0) {
+  if (jmax <= 0 || jmax > m) jmax = m;
+  std::vector<double> sabs_hist(m + 1);
   const bool acc32 = (flags & ORACLE_F_ACC32) != 0;
   const int passes = (flags & ORACLE_F_CGS1) ? 1 : 2;
   const int64_t ldh = m + 1;
@@ -297,6 +303,7 @@ int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* c
   if (!(beta > 0.0) || !std::isfinite(beta)) return ORACLE_ENONFINITE;
   for (int i = 0; i <= m; ++i) s[i] = 0.0;
   s[0] = beta;
+  sabs_hist[0] = beta;
   scale<W>(n, r, 1.0 / beta, V);
   int J = 0, breakdown = 0;
   for (int j = 1; j <= m; ++j) {  // lines 98–99
@@ -314,8 +321,10 @@ int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* c
     double sabs = oracle_hess_step(j, h.data(), cs.data(), sn.data(), s);  // lines 108–140
     for (int i = 0; i <= j; ++i) R[(int64_t)(j - 1) * ldh + i] = h[i];
     if (inner_hist) inner_hist[j - 1] = sabs / beta;
+    sabs_hist[j] = sabs;
     J = j;
-    if (j == m || breakdown || sabs <= thr) break;  // restart condition (reading R6)
+    const bool stall = stall_w > 0 && j >= stall_w && sabs * stall_factor > sabs_hist[j - stall_w];
+    if (j == jmax || breakdown || sabs <= thr || stall) break;  // restart condition (readings R6, R22)
   }
   *Jout = J;
   *bd_out = breakdown;
@@ -340,7 +349,8 @@ namespace {
 template <class W>
 int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, const double* b, const double* x0,
           double* x, int m, double tol, int ortho, double delta, int max_cycles, int flags, oracle_result* res,
-          double* history, int32_t history_cap, double* inner, int32_t inner_cap) {
+          double* history, int32_t history_cap, double* inner, int32_t inner_cap, int policy = 0,
+          double stall_factor = 1.001, double stall_frac = 0.05) {
   const bool mixed = sizeof(W) == 4;
   const bool resid32 = (flags & ORACLE_F_RESID32) != 0;
   const bool update32 = (flags & ORACLE_F_UPDATE32) != 0;
@@ -373,7 +383,8 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
   const int64_t ldv = n;
   std::vector<W> V((size_t)n * (m + 1)), r(n);
   std::vector<double> Hbar((size_t)(m + 1) * m), R((size_t)(m + 1) * m), s(m + 1), y(m), ih(m);
-  int k = 0, total_inner = 0;
+  int k = 0, total_inner = 0, J1 = 0;
+  const int stall_w = policy == ORACLE_POLICY_STALL ? std::max(1, (int)std::ceil(stall_frac * m)) : 0;
   for (;;) {
     // line 86: z_k ← b − A x_k (fp64); line 90: r_k ← M⁻¹ z_k
     // in W after casting the residual (reading R10).
@@ -404,11 +415,15 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
     // restart condition threshold (reading R6): |s_{j+1}| ≤ β·max(tol‖b‖/‖z_k‖, δ)
     double beta = std::sqrt(dot<W>(n, r.data(), r.data(), (flags & ORACLE_F_ACC32) != 0));
     double need = tol * nb / znorm;
-    double thr = beta * std::fmax(need, delta);
+    // two-stage policy (reading R22): after the first cycle,
+    // restart at the first cycle's iteration count instead of the δ test
+    const bool repeat = policy == ORACLE_POLICY_TWOSTAGE && k > 0;
+    double thr = beta * std::fmax(need, repeat ? 0.0 : delta);
     int32_t J = 0, bd = 0;
-    int rc = arnoldi<W>(ortho, flags, n, rp, ci, aW.data(), dinvW.data(),
-                        r.data(), m, thr, V.data(), ldv, Hbar.data(), R.data(), s.data(), &J, &bd, ih.data());
+    int rc = arnoldi<W>(ortho, flags, n, rp, ci, aW.data(), dinvW.data(), r.data(), m, thr, V.data(), ldv,
+                        Hbar.data(), R.data(), s.data(), &J, &bd, ih.data(), repeat ? J1 : m, stall_w, stall_factor);
     if (rc != 0) return rc;
+    if (k == 0) J1 = J;
     for (int t = 0; t < J; ++t) {
       if (res->inner_len < inner_cap) inner[res->inner_len] = ih[t];
       res->inner_len++;
@@ -423,10 +438,26 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
 
 }  // namespace
 
+extern "C" int oracle_gmres_solve_policy(int64_t n, const int32_t* rp, const int32_t* ci, const double* a,
+                                         const double* b, const double* x0, double* x, int m, double tol, int ortho,
+                                         int prec, double delta, int max_cycles, int flags, oracle_result* res,
+                                         double* history, int32_t history_cap, double* inner, int32_t inner_cap,
+                                         int policy, double stall_factor, double stall_frac);
+
 extern "C" int oracle_gmres_solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, const double* b,
                                   const double* x0, double* x, int m, double tol, int ortho, int prec, double delta,
                                   int max_cycles, int flags, oracle_result* res, double* history,
                                   int32_t history_cap, double* inner, int32_t inner_cap) {
+  return oracle_gmres_solve_policy(n, rp, ci, a, b, x0, x, m, tol, ortho, prec, delta, max_cycles, flags, res,
+                                   history, history_cap, inner, inner_cap, ORACLE_POLICY_THRESHOLD, 1.001, 0.05);
+}
+
+extern "C" int oracle_gmres_solve_policy(int64_t n, const int32_t* rp, const int32_t* ci, const double* a,
+                                         const double* b, const double* x0, double* x, int m, double tol, int ortho,
+                                         int prec, double delta, int max_cycles, int flags, oracle_result* res,
+                                         double* history, int32_t history_cap, double* inner, int32_t inner_cap,
+                                         int policy, double stall_factor, double stall_frac) {
+  if (policy < 0 || policy > 2 || !(stall_factor >= 1.0) || !(stall_frac > 0.0)) return ORACLE_EINVAL;
   if (n < 1 || m < 1 || !(tol > 0.0) || !(delta >= 0.0) || max_cycles < 0) return ORACLE_EINVAL;
   if (rp[0] != 0) return ORACLE_EBADCSR;
   for (int64_t i = 0; i < n; ++i) {
@@ -438,7 +469,7 @@ extern "C" int oracle_gmres_solve(int64_t n, const int32_t* rp, const int32_t* c
   }
   if (prec == ORACLE_MIXED)
     return solve<float>(n, rp, ci, a, b, x0, x, m, tol, ortho, delta, max_cycles, flags, res, history, history_cap,
-                        inner, inner_cap);
+                        inner, inner_cap, policy, stall_factor, stall_frac);
   return solve<double>(n, rp, ci, a, b, x0, x, m, tol, ortho, delta, max_cycles, flags, res, history, history_cap,
-                       inner, inner_cap);
+                       inner, inner_cap, policy, stall_factor, stall_frac);
 }

@@ -70,12 +70,25 @@ int oracle_arnoldi(int prec, int ortho, int flags, int64_t n, const int32_t* rp,
                    void* V, int64_t ldv, double* Hbar, double* R, double* s, int32_t* J, int32_t* breakdown,
                    double* inner_hist);
 
+/* Restart policies (readings R6, R22):
+ * THRESHOLD  restart at j = m or |s_{j+1}| ≤ β·max(tol‖b‖/‖z‖, δ);
+ * TWOSTAGE   the first cycle as THRESHOLD, later cycles at the first cycle's
+ *            iteration count J1;
+ * STALL      THRESHOLD plus: restart when |s_{j+1}| improved by less than a factor
+ *            stall_factor over the last ⌈stall_frac·m⌉ inner iterations
+ *            (SURVEY §8 f4). */
+enum { ORACLE_POLICY_THRESHOLD = 0, ORACLE_POLICY_TWOSTAGE = 1, ORACLE_POLICY_STALL = 2 };
+
 /* The whole restarted solve (Alg. 1).  x0 may be NULL (= 0).  history[k] =
  * ‖b − A x_k‖/‖b‖, k = 0..cycles; inner[t] = |s_{j+1}|/β per inner step. */
 int oracle_gmres_solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, const double* b,
                        const double* x0, double* x, int m, double tol, int ortho, int prec, double delta,
                        int max_cycles, int flags, oracle_result* res, double* history, int32_t history_cap,
                        double* inner, int32_t inner_cap);
+int oracle_gmres_solve_policy(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, const double* b,
+                              const double* x0, double* x, int m, double tol, int ortho, int prec, double delta,
+                              int max_cycles, int flags, oracle_result* res, double* history, int32_t history_cap,
+                              double* inner, int32_t inner_cap, int policy, double stall_factor, double stall_frac);
 
 #ifdef __cplusplus
 }

@@ -383,3 +383,57 @@ def test_single_cgs_pass_still_converges_in_mixed(c1):
     # the correction variables alone in fp32 still converge: fp32 accumulators too
     r = O.solve(c1.A, c1.b, m=30, ortho=O.MGS, prec=O.MIXED, flags=O.F_ACC32)
     assert r.status == O.OK and r.final_relres <= 1e-10
+
+
+# ---------------------------------------------------------------- restart policies (reading R22)
+def _cycle_lengths(inner):
+    """Cycle lengths from the per-inner |s_{j+1}|/β history: |s| is non-increasing within a
+    cycle (Givens), so every increase marks a restart."""
+    J, c = [], 0
+    for t in range(len(inner)):
+        if t > 0 and inner[t] > inner[t - 1] * (1 + 1e-12):
+            J.append(c)
+            c = 0
+        c += 1
+    J.append(c)
+    return J
+
+
+def test_twostage_restart_repeats_first_cycle_length():
+    """f1: first restart on an Arnoldi improvement δ, then every cycle restarts
+    at the first cycle's iteration count; the last cycle may stop earlier (converged)."""
+    P = inputs.make("C2", 24)
+    delta = 1e-3
+    for ortho in (O.MGS, O.CGSR):
+        r = O.solve(P.A, P.b, m=150, ortho=ortho, prec=O.MIXED, policy=O.TWOSTAGE, delta=delta)
+        assert r.status == O.OK and r.final_relres <= 1e-10
+        J = _cycle_lengths(r.inner)
+        assert len(J) == r.cycles and sum(J) == r.inner_iters
+        J1 = J[0]
+        assert J1 < 150 and all(j == J1 for j in J[1:-1]) and J[-1] <= J1
+        # the first cycle ended on the δ rule: |s_{J1+1}|/β ≤ δ < |s_{J1}|/β
+        assert r.inner[J1 - 1] <= delta < r.inner[J1 - 2]
+        # against the threshold policy, which keeps restarting on δ
+        r0 = O.solve(P.A, P.b, m=150, ortho=ortho, prec=O.MIXED, policy=O.THRESHOLD, delta=delta)
+        assert _cycle_lengths(r0.inner)[0] == J1 and _cycle_lengths(r0.inner)[1] != J1
+
+
+def test_stall_restart_fires_exactly_at_the_first_stall():
+    """f4: restart when |s| improves by less than ×1.001 over the
+    last ⌈5 % · m⌉ inner iterations — checked against the recorded |s| history."""
+    P = inputs.make("C2", 24)
+    m, factor = 150, 1.001
+    w = math.ceil(0.05 * m)
+    r = O.solve(P.A, P.b, m=m, ortho=O.MGS, prec=O.MIXED, policy=O.STALL)
+    assert r.status == O.OK and r.final_relres <= 1e-10
+    J = _cycle_lengths(r.inner)
+    first = np.concatenate([[1.0], r.inner[:J[0]]])   # |s_1|/β = 1, then |s_{j+1}|/β
+    stall = [j for j in range(w, len(first)) if first[j] * factor > first[j - w]]
+    assert J[0] < m and stall and stall[0] == J[0]      # MGS stagnates: the stall ends the cycle
+    # without the stall test the same cycle runs to m (MGS's Arnoldi residual stagnates)
+    r0 = O.solve(P.A, P.b, m=m, ortho=O.MGS, prec=O.MIXED, policy=O.THRESHOLD, delta=0.0)
+    assert _cycle_lengths(r0.inner)[0] == m
+    # CGSR: the stall is not visible in the Arnoldi residual (PAPER.md:366-367)
+    rc = O.solve(P.A, P.b, m=m, ortho=O.CGSR, prec=O.MIXED, policy=O.STALL)
+    rc0 = O.solve(P.A, P.b, m=m, ortho=O.CGSR, prec=O.MIXED, policy=O.THRESHOLD, delta=0.0)
+    assert _cycle_lengths(rc.inner) == _cycle_lengths(rc0.inner)
