@@ -69,6 +69,14 @@ typedef struct {
   int32_t ctas_per_sm;    /* 0 = auto (occupancy)                                       */
   int32_t profile;        /* != 0: grid barrier after each phase for clean phase timers */
   int32_t tune;           /* developer A/B switches; 0 = production defaults            */
+  int32_t restart_policy; /* 0 THRESHOLD: restart at j = m or |s_{j+1}| ≤ β·max(tol‖b‖/‖z‖, δ)
+                             (PAPER.md:257-264); 1 TWOSTAGE: the first cycle as THRESHOLD,
+                             later cycles at the first cycle's iteration count (PAPER.md:
+                             251-255, 448); 2 STALL: THRESHOLD plus a restart when |s| improved
+                             by less than stall_factor over the last ⌈stall_frac·m⌉ inner
+                             iterations (δ defaults to 0)          */
+  double stall_factor;    /* ≤ 0 → 1.001                                */
+  double stall_frac;      /* ≤ 0 → 0.05                                */
 } gmres_opts;
 
 /* Create a solver context on the current CUDA device: validates the CSR on the

@@ -787,8 +787,15 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   if (ortho != GMRES_MGS && ortho != GMRES_CGSR) return fail(ctx, GMRES_EINVAL, "ortho must be 0 (MGS) or 1 (CGSR)");
   if (int rc = check_prec(ctx, precision)) return rc;
   if (ctx->dist() && !ctx->linked) return fail(ctx, GMRES_EINVAL, "row-partitioned context not linked to its peers");
-  double delta = (opts && opts->delta >= 0.0) ? opts->delta : (precision == GMRES_MIXED ? 1e-6 : 0.0);
+  const int policy = opts ? opts->restart_policy : 0;
+  if (policy < 0 || policy > 2) return fail(ctx, GMRES_EINVAL, "restart_policy must be 0, 1 or 2");
+  double delta = (opts && opts->delta >= 0.0) ? opts->delta
+                                              : (precision == GMRES_MIXED && policy != 2 ? 1e-6 : 0.0);
   if (!std::isfinite(delta)) return fail(ctx, GMRES_EINVAL, "delta must be finite");
+  const double stall_factor = (opts && opts->stall_factor > 0.0) ? opts->stall_factor : 1.001;
+  const double stall_frac = (opts && opts->stall_frac > 0.0) ? opts->stall_frac : 0.05;
+  if (!(stall_factor >= 1.0) || !std::isfinite(stall_factor) || !(stall_frac <= 1.0))
+    return fail(ctx, GMRES_EINVAL, "stall_factor must be >= 1 and stall_frac in (0, 1]");
   const int max_cycles = (opts && opts->max_cycles > 0) ? opts->max_cycles : 10000;
   P.rec_inner = opts && opts->record_inner;
   int L = (opts && opts->lanes_per_row) ? opts->lanes_per_row : auto_lanes(ctx->n, ctx->nnz);
@@ -859,6 +866,9 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   d.tol = tol;
   d.delta = delta;
   d.max_cycles = max_cycles;
+  d.policy = policy;
+  d.stall_w = policy == 2 ? std::max(1, (int)std::ceil(stall_frac * m)) : 0;
+  d.stall_factor = stall_factor;
   d.inner_cap = inner_cap_dev;
   d.profile = (opts && opts->profile) ? 1 : 0;
   d.tile_bytes = tile_bytes;

@@ -126,6 +126,9 @@ struct Dev {
   const int* chunk_off; // G+1 offsets into chunks (CTA g: [off[g], off[g+1]-1) + sentinel)
   double tol, delta;
   int max_cycles;
+  int policy;           // restart policy (reading R22): 0 threshold, 1 two-stage, 2 stall
+  int stall_w;          // stall window (inner iterations), policy 2
+  double stall_factor;  // stall improvement factor, policy 2
   double* history; int hist_cap;
   int* cycle_J;         // [hist_cap] inner iterations of every cycle
   double* inner_hist; int inner_cap;
@@ -1458,7 +1461,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (lead) { const unsigned long long t = globaltimer(); d.prof[ph] += t - tprev; tprev = t; }
   };
 
-  int k = 0, total_inner = 0, inner_len = 0, status = ST_OK;
+  int k = 0, total_inner = 0, inner_len = 0, status = ST_OK, J1 = 0;
   // (every rank reads its own flag: the cast overflow check is the same on all
   // ranks only if the caller built A32 on all of them; ranks agree on it via
   // the residual all-reduce below, which carries the error bits)
@@ -1505,10 +1508,15 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (k >= d.max_cycles) { status = ST_NOT_CONVERGED; break; }
     const double beta = sqrt(RR);
     if (!(beta > 0.0) || !isfinite(beta)) { status = ST_ENONFINITE; break; }
-    const double thr = beta * fmax(d.tol * nb / sqrt(ZZ), d.delta);
+    // restart threshold (readings R6, R22): the two-stage policy drops δ after
+    // the first cycle and restarts at the first cycle's iteration count J1
+    const bool repeat = d.policy == 1 && k > 0;
+    const double thr = beta * fmax(d.tol * nb / sqrt(ZZ), repeat ? 0.0 : d.delta);
+    const int jmax = repeat ? min(d.m, J1) : d.m;
     if (threadIdx.x == 0) {
       for (int i = 0; i <= d.m; ++i) s_s[i] = 0.0;
       s_s[0] = beta;
+      s_rhs[0] = beta;  // |s| history of the cycle (stall policy; s_rhs is free until the back-solve)
     }
     double inv = 1.0 / beta;
     W* src = wb0;
@@ -1540,7 +1548,9 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
           for (int i = 0; i <= j; ++i) d.R[(size_t)(j - 1) * (d.m + 1) + i] = s_h[i];
           if (inner_len < d.inner_cap) d.inner_hist[inner_len] = sabs / beta;
         }
-        sh.flag = (j == d.m) || (hn == 0.0) || (sabs <= thr) || !isfinite(hn);
+        s_rhs[j] = sabs;
+        const bool stall = d.stall_w > 0 && j >= d.stall_w && sabs * d.stall_factor > s_rhs[j - d.stall_w];
+        sh.flag = (j == jmax) || (hn == 0.0) || (sabs <= thr) || stall || !isfinite(hn);
       }
       __syncthreads();
       inner_len++;
@@ -1553,6 +1563,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     }
     if (fail) { if (status == ST_OK) status = ST_ETIMEOUT; break; }
     total_inner += J;
+    if (k == 0) J1 = J;
     if (lead && k < d.hist_cap) d.cycle_J[k] = J;
     // ------------ y = R⁻¹ s, x ← x + V_J y  (lines 143–147)
     if (cta == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);

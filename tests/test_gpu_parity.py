@@ -362,3 +362,48 @@ def test_basis_matches_oracle_first_cycle(ortho, prec):
     loss = np.abs(np.eye(J) - V.T @ V).max()
     loss_o = np.abs(np.eye(J) - Vo.T @ Vo).max()
     assert loss <= 10 * loss_o + (1e-13 if prec == G.FP64 else 1e-6), (loss, loss_o)
+
+
+# ------------------------------------------------------------------ restart policies (§8 f1, f4; reading R22)
+def _cycle_lengths(inner):
+    J, c = [], 0
+    for t in range(len(inner)):
+        if t > 0 and inner[t] > inner[t - 1] * (1 + 1e-12):
+            J.append(c)
+            c = 0
+        c += 1
+    J.append(c)
+    return J
+
+
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+def test_twostage_policy_matches_oracle(ortho):
+    P = inputs.make("C2", 24)
+    S = G.Solver.from_csr(P.A)
+    r = S.solve(P.b, m=150, ortho=ortho, precision=G.MIXED, delta=1e-3, policy=G.TWOSTAGE)
+    ref = O.solve(P.A, P.b, m=150, ortho=ortho, prec=O.MIXED, delta=1e-3, policy=O.TWOSTAGE)
+    assert r.status == 0 and check_solution(P.A, P.b, r.x) <= 1e-10
+    Jo = _cycle_lengths(ref.inner)
+    J = list(r.cycle_iters)
+    assert J[0] == Jo[0] and all(j == J[0] for j in J[1:-1]) and J[-1] <= J[0]
+    assert abs(r.cycles - ref.cycles) <= max(1, 0.1 * ref.cycles)
+
+
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+def test_stall_policy_matches_oracle(ortho):
+    P = inputs.make("C2", 24)
+    S = G.Solver.from_csr(P.A)
+    m = 150
+    r = S.solve(P.b, m=m, ortho=ortho, precision=G.MIXED, policy=G.STALL, record_inner=True)
+    ref = O.solve(P.A, P.b, m=m, ortho=ortho, prec=O.MIXED, policy=O.STALL)
+    assert r.status == 0 and check_solution(P.A, P.b, r.x) <= 1e-10
+    J, Jo = list(r.cycle_iters), _cycle_lengths(ref.inner)
+    assert abs(J[0] - Jo[0]) <= 3, (J, Jo)
+    # the device took its exit at the first stall of its own |s| history
+    w = math.ceil(0.05 * m)
+    first = np.concatenate([[1.0], r.inner[:J[0]]])
+    stall = [j for j in range(w, len(first)) if first[j] * 1.001 > first[j - w]]
+    if J[0] < m and not stall:   # exit by convergence (need), as for CGSR
+        assert first[-1] <= 1e-10 * 10
+    elif stall:
+        assert stall[0] == J[0]
