@@ -78,6 +78,37 @@ __global__ void __launch_bounds__(NT, 1) kern(Args a) {
         double s = 0; for (int w = 0; w < (G + 31) / 32; ++w) s += red2[w];
         acc_all += s;
       }
+    } else if (a.variant >= 10) {
+      // counter + partial load with the arrivals spread over NC = variant-10 counters
+      // (256 B apart: different L2 slices); warp 0 lane c polls counter c
+      const int NC = a.variant - 10;
+      v = warp_sum(v);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      double* P = a.parts + (size_t)(it & 1) * G;
+      if (warp == 0) {
+        if (lane == 0) {
+          double s = 0; for (int w = 0; w < NW; ++w) s += red[w];
+          P[g] = s;
+          red_rel(a.ctr + (size_t)(g % NC) * 32, 1);
+        }
+        epoch += (lane == 0);
+        const unsigned long long ep = __shfl_sync(0xffffffffu, epoch, 0);
+        // counter c receives the arrivals of CTAs g ≡ c (mod NC)
+        const unsigned long long want = lane < NC ? ep * (unsigned long long)((G - lane + NC - 1) / NC) : 0ull;
+        bool done = false;
+        while (!done) {
+          const unsigned long long cv = lane < NC ? ld_acq(a.ctr + (size_t)lane * 32) : 0ull;
+          done = __all_sync(0xffffffffu, cv >= want);
+        }
+      }
+      __syncthreads();
+      double x = 0.0;
+      if (threadIdx.x < G) x = __ldcg(P + threadIdx.x);
+      if (warp < (G + 31) / 32) { x = warp_sum(x); if (lane == 0) red2[warp] = x; }
+      __syncthreads();
+      double s = 0; for (int w = 0; w < (G + 31) / 32; ++w) s += red2[w];
+      acc_all += s;
     } else {
       // sentinel slots: 3: st.release push, relaxed poll, slot stride a.stride (doubles)
       //                 4: st.relaxed push
@@ -129,7 +160,7 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int G = sms, iters = 2000;
   unsigned long long *ctr, *out; double *slots, *parts;
-  cudaMalloc(&ctr, 8); cudaMalloc(&out, 16);
+  cudaMalloc(&ctr, 8 * 32 * 32); cudaMalloc(&out, 16);
   const int maxstride = 32;
   cudaMalloc(&slots, sizeof(double) * 3 * G * maxstride);
   cudaMalloc(&parts, sizeof(double) * 2 * G);
@@ -145,10 +176,15 @@ int main() {
     {5, 1, "slots release push + acquire fence, stride 8B"},
     {6, 1, "slots release push, warp-0 poll, stride 8B"},
     {6, 32, "slots release push, warp-0 poll, stride 256B"},
+    {11, 1, "counter x1 (warp-0 poll) + partial load"},
+    {12, 1, "counters x2 + partial load"},
+    {14, 1, "counters x4 + partial load"},
+    {18, 1, "counters x8 + partial load"},
+    {26, 1, "counters x16 + partial load"},
   };
   for (auto& v : vs) {
     for (int rep = 0; rep < 2; ++rep) {
-      cudaMemset(ctr, 0, 8);
+      cudaMemset(ctr, 0, 8 * 32 * 32);
       fill<<<64, 256>>>((unsigned long long*)slots, (size_t)3 * G * maxstride, SENT);
       Args a{v.v, iters, G, v.stride, ctr, slots, parts, out};
       void* args[] = {&a};
