@@ -76,6 +76,10 @@ def lib():
         L.oracle_gmres_solve_policy.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, dbl, i32, i32, dbl, i32, i32,
                                                 vp, vp, ctypes.c_int32, vp, ctypes.c_int32, i32, dbl, dbl]
         L.oracle_gmres_solve_policy.restype = i32
+        L.oracle_gmres_solve_orth.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, dbl, i32, i32, dbl, i32, i32,
+                                              vp, vp, ctypes.c_int32, vp, ctypes.c_int32, i32, dbl, dbl, i32, dbl,
+                                              vp, ctypes.c_int32]
+        L.oracle_gmres_solve_orth.restype = i32
         _lib = L
     return _lib
 
@@ -261,11 +265,11 @@ class SolveResult:
     final_relres: float
 
 
-THRESHOLD, TWOSTAGE, STALL = 0, 1, 2   # restart policies (oracle.h; R6, R22)
+THRESHOLD, TWOSTAGE, STALL, ORTHLOSS = 0, 1, 2, 3   # restart policies (oracle.h; R6, R22, R23)
 
 
 def solve(A, b, x0=None, m=30, tol=1e-10, ortho=CGSR, prec=MIXED, delta=None, max_cycles=10000, flags=0,
-          inner_cap=200000, policy=THRESHOLD, stall_factor=1.001, stall_frac=0.05):
+          inner_cap=200000, policy=THRESHOLD, stall_factor=1.001, stall_frac=0.05, orth_kind=0, orth_thresh=1.0):
     if delta is None:
         delta = 1e-6 if (prec == MIXED and policy != STALL) else 0.0
     n = A.n
@@ -274,11 +278,15 @@ def solve(A, b, x0=None, m=30, tol=1e-10, ortho=CGSR, prec=MIXED, delta=None, ma
     inner = np.zeros(inner_cap)
     res = _Result()
     x0c = None if x0 is None else _c(x0, np.float64)
-    rc = lib().oracle_gmres_solve_policy(n, _p(A.row_ptr), _p(A.col), _p(_c(A.val, np.float64)),
-                                         _p(_c(b, np.float64)), _p(x0c), _p(x), m, tol, ortho, prec, delta,
-                                         max_cycles, flags, ctypes.byref(res), _p(hist), hist.size, _p(inner),
-                                         inner.size, int(policy), float(stall_factor), float(stall_frac))
+    orth = np.zeros(inner_cap)
+    rc = lib().oracle_gmres_solve_orth(n, _p(A.row_ptr), _p(A.col), _p(_c(A.val, np.float64)),
+                                       _p(_c(b, np.float64)), _p(x0c), _p(x), m, tol, ortho, prec, delta,
+                                       max_cycles, flags, ctypes.byref(res), _p(hist), hist.size, _p(inner),
+                                       inner.size, int(policy), float(stall_factor), float(stall_frac),
+                                       int(orth_kind), float(orth_thresh), _p(orth), orth.size)
     if rc < 0:
         raise RuntimeError(f"oracle_gmres_solve error {rc}")
-    return SolveResult(rc, x, res.cycles, res.inner_iters, hist[:min(res.history_len, hist.size)].copy(),
-                       inner[:min(res.inner_len, inner.size)].copy(), res.final_relres)
+    out = SolveResult(rc, x, res.cycles, res.inner_iters, hist[:min(res.history_len, hist.size)].copy(),
+                      inner[:min(res.inner_len, inner.size)].copy(), res.final_relres)
+    out.orth = orth[:min(res.inner_len, orth.size)].copy() if policy == ORTHLOSS else None
+    return out

@@ -287,12 +287,55 @@ namespace {
 // |s_{j+1}| ≤ thr, or — with stall_w > 0 — stall: the Arnoldi residual improved
 // by less than a factor stall_factor over the last stall_w inner iterations
 // (1.001 over 5 % of the restart length).
+// Orthogonality-loss monitor (reading R23): U_k = strict upper
+// part of V_kᵀV_k, S_k = (I + U_k)⁻¹ U_k, built one column per inner iteration:
+// the new column of U is u_i = v_i·v_{k+1} (i ≤ k) and the new column of S is
+// (I + U_k)⁻¹ u (unit upper-triangular back-substitution; S's leading block does
+// not change).  ‖S‖_F accumulates over columns; ‖S‖₂ is estimated by 10 power
+// iterations on SᵀS from x = (1,…,1)/√k.
+struct OrthMonitor {
+  int kind = 0;          // 0 Frobenius, 1 spectral (10 power iterations)
+  double thresh = 1.0;   // restart when the norm reaches it
+  int m = 0;
+  std::vector<double> U, S;  // column-major (m+1)×(m+1)
+  double fro2 = 0.0;
+  void init(int m_) { m = m_; U.assign((size_t)(m + 1) * (m + 1), 0.0); S.assign(U.size(), 0.0); fro2 = 0.0; }
+  double& u(int i, int l) { return U[(size_t)l * (m + 1) + i]; }
+  double& sm(int i, int l) { return S[(size_t)l * (m + 1) + i]; }
+  // append column l (0-based: basis vectors 0..l−1 against vector l); returns the norm estimate
+  double append(int l, const double* ucol) {
+    for (int i = 0; i < l; ++i) u(i, l) = ucol[i];
+    for (int i = l - 1; i >= 0; --i) {  // (I + U_l) s = u, U_l = leading l×l block
+      double t = ucol[i];
+      for (int q = i + 1; q < l; ++q) t -= u(i, q) * sm(q, l);
+      sm(i, l) = t;
+    }
+    for (int i = 0; i < l; ++i) fro2 += sm(i, l) * sm(i, l);
+    if (kind == 0) return std::sqrt(fro2);
+    const int k = l + 1;  // S is k×k (columns 0..l)
+    std::vector<double> x(k, 1.0 / std::sqrt((double)k)), y(k);
+    for (int it = 0; it < 10; ++it) {
+      for (int i = 0; i < k; ++i) { double t = 0.0; for (int q = i + 1; q < k; ++q) t += sm(i, q) * x[q]; y[i] = t; }
+      double nx = 0.0;
+      for (int q = 0; q < k; ++q) { double t = 0.0; for (int i = 0; i < q; ++i) t += sm(i, q) * y[i]; x[q] = t; nx += t * t; }
+      nx = std::sqrt(nx);
+      if (nx == 0.0) return 0.0;
+      for (int q = 0; q < k; ++q) x[q] /= nx;
+    }
+    double ny = 0.0;
+    for (int i = 0; i < k; ++i) { double t = 0.0; for (int q = i + 1; q < k; ++q) t += sm(i, q) * x[q]; ny += t * t; }
+    return std::sqrt(ny);
+  }
+};
+
 template <class W>
 int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* ci, const W* aW, const W* dinvW,
             const W* r, int m, double thr, W* V, int64_t ldv, double* Hbar, double* R, double* s, int32_t* Jout,
-            int32_t* bd_out, double* inner_hist, int jmax = 0, int stall_w = 0, double stall_factor = 1.0) {
+            int32_t* bd_out, double* inner_hist, int jmax = 0, int stall_w = 0, double stall_factor = 1.0,
+            OrthMonitor* mon = nullptr, double* mon_hist = nullptr) {
   if (jmax <= 0 || jmax > m) jmax = m;
-  std::vector<double> sabs_hist(m + 1);
+  std::vector<double> sabs_hist(m + 1), ucol(mon ? m + 1 : 0);
+  if (mon) mon->init(m);
   const bool acc32 = (flags & ORACLE_F_ACC32) != 0;
   const int passes = (flags & ORACLE_F_CGS1) ? 1 : 2;
   const int64_t ldh = m + 1;
@@ -324,7 +367,15 @@ int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* c
     sabs_hist[j] = sabs;
     J = j;
     const bool stall = stall_w > 0 && j >= stall_w && sabs * stall_factor > sabs_hist[j - stall_w];
-    if (j == jmax || breakdown || sabs <= thr || stall) break;  // restart condition (readings R6, R22)
+    bool orth = false;
+    if (mon && !breakdown) {  // column j of U: v_i · v_{j+1}, i = 1..j (fp64 accumulation)
+      const W* vn = V + (int64_t)j * ldv;
+      for (int i = 0; i < j; ++i) ucol[i] = dot<W>(n, V + (int64_t)i * ldv, vn, false);
+      const double sn = mon->append(j, ucol.data());
+      if (mon_hist) mon_hist[j - 1] = sn;
+      orth = sn >= mon->thresh;
+    }
+    if (j == jmax || breakdown || sabs <= thr || stall || orth) break;  // restart (readings R6, R22, R23)
   }
   *Jout = J;
   *bd_out = breakdown;
@@ -350,7 +401,8 @@ template <class W>
 int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, const double* b, const double* x0,
           double* x, int m, double tol, int ortho, double delta, int max_cycles, int flags, oracle_result* res,
           double* history, int32_t history_cap, double* inner, int32_t inner_cap, int policy = 0,
-          double stall_factor = 1.001, double stall_frac = 0.05) {
+          double stall_factor = 1.001, double stall_frac = 0.05, int orth_kind = 0, double orth_thresh = 1.0,
+          double* orth_hist = nullptr, int32_t orth_cap = 0) {
   const bool mixed = sizeof(W) == 4;
   const bool resid32 = (flags & ORACLE_F_RESID32) != 0;
   const bool update32 = (flags & ORACLE_F_UPDATE32) != 0;
@@ -385,6 +437,10 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
   std::vector<double> Hbar((size_t)(m + 1) * m), R((size_t)(m + 1) * m), s(m + 1), y(m), ih(m);
   int k = 0, total_inner = 0, J1 = 0;
   const int stall_w = policy == ORACLE_POLICY_STALL ? std::max(1, (int)std::ceil(stall_frac * m)) : 0;
+  OrthMonitor mon;
+  mon.kind = orth_kind;
+  mon.thresh = orth_thresh;
+  std::vector<double> mh(m);
   for (;;) {
     // line 86: z_k ← b − A x_k (fp64); line 90: r_k ← M⁻¹ z_k
     // in W after casting the residual (reading R10).
@@ -421,8 +477,12 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
     double thr = beta * std::fmax(need, repeat ? 0.0 : delta);
     int32_t J = 0, bd = 0;
     int rc = arnoldi<W>(ortho, flags, n, rp, ci, aW.data(), dinvW.data(), r.data(), m, thr, V.data(), ldv,
-                        Hbar.data(), R.data(), s.data(), &J, &bd, ih.data(), repeat ? J1 : m, stall_w, stall_factor);
+                        Hbar.data(), R.data(), s.data(), &J, &bd, ih.data(), repeat ? J1 : m, stall_w, stall_factor,
+                        policy == ORACLE_POLICY_ORTHLOSS ? &mon : nullptr, mh.data());
     if (rc != 0) return rc;
+    if (policy == ORACLE_POLICY_ORTHLOSS && orth_hist)
+      for (int t = 0; t < J; ++t)
+        if (res->inner_len + t < orth_cap) orth_hist[res->inner_len + t] = mh[t];
     if (k == 0) J1 = J;
     for (int t = 0; t < J; ++t) {
       if (res->inner_len < inner_cap) inner[res->inner_len] = ih[t];
@@ -457,7 +517,18 @@ extern "C" int oracle_gmres_solve_policy(int64_t n, const int32_t* rp, const int
                                          int prec, double delta, int max_cycles, int flags, oracle_result* res,
                                          double* history, int32_t history_cap, double* inner, int32_t inner_cap,
                                          int policy, double stall_factor, double stall_frac) {
-  if (policy < 0 || policy > 2 || !(stall_factor >= 1.0) || !(stall_frac > 0.0)) return ORACLE_EINVAL;
+  return oracle_gmres_solve_orth(n, rp, ci, a, b, x0, x, m, tol, ortho, prec, delta, max_cycles, flags, res, history,
+                                 history_cap, inner, inner_cap, policy, stall_factor, stall_frac, 0, 1.0, nullptr, 0);
+}
+
+extern "C" int oracle_gmres_solve_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double* a,
+                                       const double* b, const double* x0, double* x, int m, double tol, int ortho,
+                                       int prec, double delta, int max_cycles, int flags, oracle_result* res,
+                                       double* history, int32_t history_cap, double* inner, int32_t inner_cap,
+                                       int policy, double stall_factor, double stall_frac, int orth_kind,
+                                       double orth_thresh, double* orth_hist, int32_t orth_cap) {
+  if (policy < 0 || policy > 3 || !(stall_factor >= 1.0) || !(stall_frac > 0.0)) return ORACLE_EINVAL;
+  if (orth_kind < 0 || orth_kind > 1 || !(orth_thresh > 0.0)) return ORACLE_EINVAL;
   if (n < 1 || m < 1 || !(tol > 0.0) || !(delta >= 0.0) || max_cycles < 0) return ORACLE_EINVAL;
   if (rp[0] != 0) return ORACLE_EBADCSR;
   for (int64_t i = 0; i < n; ++i) {
@@ -469,7 +540,9 @@ extern "C" int oracle_gmres_solve_policy(int64_t n, const int32_t* rp, const int
   }
   if (prec == ORACLE_MIXED)
     return solve<float>(n, rp, ci, a, b, x0, x, m, tol, ortho, delta, max_cycles, flags, res, history, history_cap,
-                        inner, inner_cap, policy, stall_factor, stall_frac);
+                        inner, inner_cap, policy, stall_factor, stall_frac, orth_kind, orth_thresh, orth_hist,
+                        orth_cap);
   return solve<double>(n, rp, ci, a, b, x0, x, m, tol, ortho, delta, max_cycles, flags, res, history, history_cap,
-                       inner, inner_cap, policy, stall_factor, stall_frac);
+                       inner, inner_cap, policy, stall_factor, stall_frac, orth_kind, orth_thresh, orth_hist,
+                       orth_cap);
 }

@@ -77,7 +77,11 @@ int oracle_arnoldi(int prec, int ortho, int flags, int64_t n, const int32_t* rp,
  * STALL      THRESHOLD plus: restart when |s_{j+1}| improved by less than a factor
  *            stall_factor over the last ⌈stall_frac·m⌉ inner iterations
  *            (SURVEY §8 f4). */
-enum { ORACLE_POLICY_THRESHOLD = 0, ORACLE_POLICY_TWOSTAGE = 1, ORACLE_POLICY_STALL = 2 };
+enum { ORACLE_POLICY_THRESHOLD = 0, ORACLE_POLICY_TWOSTAGE = 1, ORACLE_POLICY_STALL = 2, ORACLE_POLICY_ORTHLOSS = 3 };
+/* ORTHLOSS   THRESHOLD plus a restart when ‖S_k‖ ≥ orth_thresh, S_k = (I+U_k)⁻¹U_k,
+ *            U_k = strict upper part of V_kᵀV_k (SURVEY §8
+ *            f3); ‖·‖ = Frobenius (orth_kind 0) or spectral by 10 power iterations (1);
+ *            orth_hist[t] = the norm after inner step t. */
 
 /* The whole restarted solve (Alg. 1).  x0 may be NULL (= 0).  history[k] =
  * ‖b − A x_k‖/‖b‖, k = 0..cycles; inner[t] = |s_{j+1}|/β per inner step. */
@@ -89,6 +93,11 @@ int oracle_gmres_solve_policy(int64_t n, const int32_t* rp, const int32_t* ci, c
                               const double* x0, double* x, int m, double tol, int ortho, int prec, double delta,
                               int max_cycles, int flags, oracle_result* res, double* history, int32_t history_cap,
                               double* inner, int32_t inner_cap, int policy, double stall_factor, double stall_frac);
+int oracle_gmres_solve_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, const double* b,
+                            const double* x0, double* x, int m, double tol, int ortho, int prec, double delta,
+                            int max_cycles, int flags, oracle_result* res, double* history, int32_t history_cap,
+                            double* inner, int32_t inner_cap, int policy, double stall_factor, double stall_frac,
+                            int orth_kind, double orth_thresh, double* orth_hist, int32_t orth_cap);
 
 #ifdef __cplusplus
 }

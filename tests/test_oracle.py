@@ -437,3 +437,37 @@ def test_stall_restart_fires_exactly_at_the_first_stall():
     rc = O.solve(P.A, P.b, m=m, ortho=O.CGSR, prec=O.MIXED, policy=O.STALL)
     rc0 = O.solve(P.A, P.b, m=m, ortho=O.CGSR, prec=O.MIXED, policy=O.THRESHOLD, delta=0.0)
     assert _cycle_lengths(rc.inner) == _cycle_lengths(rc0.inner)
+
+
+def test_orthloss_monitor_matches_dense_definition():
+    """f3: the incremental S_k = (I+U_k)⁻¹U_k of the monitor equals the
+    dense definition from the cycle's basis; ‖S‖_F exactly, ‖S‖₂ by 10 power iterations from
+    below; Frobenius ≥ spectral; the cycle ends at the first step whose norm reaches the
+    threshold (reading R23)."""
+    P = inputs.make("C2", 16)
+    m = 60
+    for kind in (0, 1):
+        r = O.solve(P.A, P.b, m=m, ortho=O.MGS, prec=O.MIXED, policy=O.ORTHLOSS, orth_kind=kind,
+                    orth_thresh=10.0, delta=0.0, max_cycles=1)
+        aW, dW = O.working_copy(P.A, O.MIXED)
+        r0 = O.resid(O.MIXED, P.A, P.b, np.zeros(P.A.n), dW)[1]
+        cyc = O.arnoldi(O.MIXED, O.MGS, P.A, r0, m, 0.0)
+        V = cyc.V.astype(np.float64)                       # n × (J+1)
+        J = len(r.orth)
+        assert J == cyc.J
+        for j in (1, 5, 20, J - 1):                        # monitor value after inner step j
+            k = j + 1
+            U = np.triu(V[:, :k].T @ V[:, :k], 1)
+            S = np.linalg.solve(np.eye(k) + U, U)
+            fro, two = np.linalg.norm(S), np.linalg.norm(S, 2)
+            if kind == 0:
+                assert r.orth[j - 1] == pytest.approx(fro, rel=1e-9, abs=1e-13)
+            else:
+                assert r.orth[j - 1] <= two * (1 + 1e-9) + 1e-13
+                assert r.orth[j - 1] >= 0.5 * two - 1e-13
+            assert two <= 1 + 1e-9 and fro >= two - 1e-12
+    # the trigger: first step whose Frobenius norm reaches the threshold
+    r = O.solve(P.A, P.b, m=m, ortho=O.MGS, prec=O.MIXED, policy=O.ORTHLOSS, orth_thresh=0.05, delta=0.0,
+                max_cycles=1)
+    hit = np.nonzero(r.orth >= 0.05)[0]
+    assert hit.size and len(r.orth) == hit[0] + 1 < m
