@@ -77,6 +77,10 @@ typedef struct {
                              iterations (δ defaults to 0)          */
   double stall_factor;    /* ≤ 0 → 1.001                                */
   double stall_frac;      /* ≤ 0 → 0.05                                */
+  double orth_thresh;     /* restart_policy 3 ORTHLOSS: THRESHOLD plus a restart when
+                             ‖S_k‖_F ≥ orth_thresh, S_k = (I+U_k)⁻¹U_k, U_k = strict upper
+                             part of V_kᵀV_k; ≤ 0 → 1.0.  Adds
+                             one pass over the basis per inner iteration               */
 } gmres_opts;
 
 /* Create a solver context on the current CUDA device: validates the CSR on the

@@ -51,6 +51,7 @@ struct gmres_ctx {
   unsigned long long* d_ctr = nullptr;  // arrival counter
   size_t slots_count = 0;
   double* d_R = nullptr;
+  double* d_umat = nullptr;  // orthogonality monitor U (policy 3)
   double* d_y = nullptr;
   int* d_flags = nullptr;  // [0] abort [1] err [2] scratch
   int* d_out_int = nullptr;
@@ -216,6 +217,12 @@ void* pick_solve(int prec, int L) {
     case 16: return solve_kernel_ptr<double, 16>();
     default: return solve_kernel_ptr<double, 32>();
   }
+}
+
+// orthogonality-monitor launches (restart policy 3): L ∈ {1, 4}
+void* pick_solve_monitor(int prec, int L) {
+  if (prec == GMRES_MIXED) return L == 1 ? (void*)&solve_kernel<float, 1, false, true> : (void*)&solve_kernel<float, 4, false, true>;
+  return L == 1 ? (void*)&solve_kernel<double, 1, false, true> : (void*)&solve_kernel<double, 4, false, true>;
 }
 
 // virtual-rank launches (several row blocks on one device): L ∈ {1, 4}
@@ -468,6 +475,7 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   const size_t octr = take(sizeof(unsigned long long) * 4);
   const size_t oR = take(sizeof(double) * kmax * m);
   const size_t oy = take(sizeof(double) * kmax);
+  const size_t oum = take(sizeof(double) * (m + 1) * (m + 1));
   const size_t ofl = take(sizeof(int) * 8);
   const size_t ooi = take(sizeof(int) * 8);
   const size_t ood = take(sizeof(double) * 4);
@@ -487,6 +495,7 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   ctx->d_ctr = (unsigned long long*)(ctx->d_ws + octr);
   ctx->d_R = (double*)(ctx->d_ws + oR);
   ctx->d_y = (double*)(ctx->d_ws + oy);
+  ctx->d_umat = (double*)(ctx->d_ws + oum);
   ctx->d_flags = (int*)(ctx->d_ws + ofl);
   ctx->d_out_int = (int*)(ctx->d_ws + ooi);
   ctx->d_out_dbl = (double*)(ctx->d_ws + ood);
@@ -788,7 +797,8 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   if (int rc = check_prec(ctx, precision)) return rc;
   if (ctx->dist() && !ctx->linked) return fail(ctx, GMRES_EINVAL, "row-partitioned context not linked to its peers");
   const int policy = opts ? opts->restart_policy : 0;
-  if (policy < 0 || policy > 2) return fail(ctx, GMRES_EINVAL, "restart_policy must be 0, 1 or 2");
+  if (policy < 0 || policy > 3) return fail(ctx, GMRES_EINVAL, "restart_policy must be 0, 1, 2 or 3");
+  const double orth_thresh = (opts && opts->orth_thresh > 0.0) ? opts->orth_thresh : 1.0;
   double delta = (opts && opts->delta >= 0.0) ? opts->delta
                                               : (precision == GMRES_MIXED && policy != 2 ? 1e-6 : 0.0);
   if (!std::isfinite(delta)) return fail(ctx, GMRES_EINVAL, "delta must be finite");
@@ -801,12 +811,14 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   int L = (opts && opts->lanes_per_row) ? opts->lanes_per_row : auto_lanes(ctx->n, ctx->nnz);
   if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16 && L != 32)
     return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 1/2/4/8/16/32");
-  if (virt && L != 1) L = 4;
+  if ((virt || policy == 3) && L != 1) L = 4;
   P.st = stream ? (cudaStream_t)stream : ctx->stream;
   P.prec = precision;
   const cudaStream_t st = P.st;
 
-  const void* kern = virt ? pick_solve_virtual(precision, L) : pick_solve(precision, L);
+  const void* kern = virt ? pick_solve_virtual(precision, L)
+                           : policy == 3 ? pick_solve_monitor(precision, L) : pick_solve(precision, L);
+  if (virt && policy == 3) return fail(ctx, GMRES_EINVAL, "restart_policy 3 is not available for virtual ranks");
   int tile_bytes = tile_bytes_for(m);
   size_t smem = smem_bytes(m, tile_bytes);
   int G = 0;
@@ -869,6 +881,8 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   d.policy = policy;
   d.stall_w = policy == 2 ? std::max(1, (int)std::ceil(stall_frac * m)) : 0;
   d.stall_factor = stall_factor;
+  d.orth_thresh = orth_thresh;
+  d.Umat = ctx->d_umat;
   d.inner_cap = inner_cap_dev;
   d.profile = (opts && opts->profile) ? 1 : 0;
   d.tile_bytes = tile_bytes;

@@ -126,7 +126,9 @@ struct Dev {
   const int* chunk_off; // G+1 offsets into chunks (CTA g: [off[g], off[g+1]-1) + sentinel)
   double tol, delta;
   int max_cycles;
-  int policy;           // restart policy (reading R22): 0 threshold, 1 two-stage, 2 stall
+  int policy;           // restart policy (readings R22, R23): 0 threshold, 1 two-stage, 2 stall, 3 orth. loss
+  double orth_thresh;   // policy 3: restart when ‖S_k‖_F ≥ orth_thresh
+  double* Umat;         // policy 3: strict upper part of V_kᵀV_k, (m+1)×(m+1) column-major (CTA 0 writes)
   int stall_w;          // stall window (inner iterations), policy 2
   double stall_factor;  // stall improvement factor, policy 2
   double* history; int hist_cap;
@@ -1371,18 +1373,44 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   return true;
 }
 
+// ‖w‖² all-reduce that ends the orthogonalisation.  With the orthogonality
+// monitor (policy 3, reading R23) the dots V_jᵀw of the final w are formed in an
+// extra pass over V_j and all-reduced TOGETHER with ‖w‖² (one reduction of j+1
+// values); s_y[i] = (v_i·w)/‖w‖ = the new column of U (v_{j+1} = w/‖w‖).
+// (MON: compiled only into the monitor's own kernel instantiation — the default
+// kernel sits at the 128-register limit, tools/regcheck.sh)
+template <class W, bool MON>
+__device__ __forceinline__ bool final_norm(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
+                                           W* w, double nn, double* s_part, double* s_out, double* s_tmp,
+                                           W* s_coefW, double* s_y, char* s_tiles, double& NN) {
+  halo_push(d, sh, (const W*)w, wbuf_index(d, w));
+  if (!MON || d.policy != 3) return allreduce1(d, sh, nn, true, NN);
+  fence_proxy_async_global();  // w's generic stores are read by the pass's bulk copies
+  __syncthreads();
+  double dummy = 0.0;
+  rowtile_pass<W, 1>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, dummy);
+  combine_acc(d, s_tmp, j, s_part);
+  double p[1] = {nn};
+  block_sum<1>(p, sh, s_part + j);
+  if (!grid_allreduce(d, sh, s_part, j + 1, s_out, s_tmp)) return false;
+  NN = s_out[j];
+  const double inv = NN > 0.0 ? 1.0 / sqrt(NN) : 0.0;
+  for (int i = threadIdx.x; i < j; i += NT) s_y[i] = s_out[i] * inv;
+  __syncthreads();
+  return true;
+}
+
 // Orthogonalisation of w (own rows) against V[:, 0..j) and its norm: MGS
 // or CGSR (two passes).  s_h[0..j) gets
 // h_{1..j, j}; returns ‖w‖² through NN.
-template <class W>
+template <class W, bool MON = false>
 __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
                             double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
                             char* s_tiles, double& NN) {
   if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4)) {
     double nn = 0.0;
     if (!mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
-    halo_push(d, sh, (const W*)w, wbuf_index(d, w));
-    return allreduce1(d, sh, nn, true, NN);
+    return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
   }
   if (d.ortho == 0) {
     W hprev = (W)0;
@@ -1401,8 +1429,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
       hprev = RN<W>(h);
     }
     const double acc = mgs_sweep<W>(r0, r1, w, V + (long long)(j - 1) * ldv, hprev, nullptr);
-    halo_push(d, sh, (const W*)w, wbuf_index(d, w));
-    return allreduce1(d, sh, acc, true, NN);
+    return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, acc, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
   }
   double nn = 0.0;
   const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
@@ -1435,11 +1462,31 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   __syncthreads();
   nn = 0.0;
   rowtile_pass<W, 3>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
-  halo_push(d, sh, (const W*)w, wbuf_index(d, w));
   sub(4);
-  if (!allreduce1(d, sh, nn, true, NN)) return false;
+  if (!final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN))
+    return false;
   sub(5);
   return true;
+}
+
+// Orthogonality monitor (policy 3, reading R23): u = s_y[0..l) is the new
+// column l of U (CTA 0 stores it); s = (I + U_l)⁻¹ u by column-oriented unit
+// upper back-substitution with U's earlier columns from global memory; returns
+// ‖s‖² (the new column's share of ‖S‖_F²), identical in every CTA.
+__device__ __forceinline__ double orth_column(double* Umat, int ldu, int l, bool store, double* s_y, Shm& sh,
+                                           double* s_part) {
+  if (store)
+    for (int i = threadIdx.x; i < l; i += NT) Umat[(size_t)l * ldu + i] = s_y[i];
+  for (int q = l - 1; q >= 0; --q) {
+    __syncthreads();
+    const double sq = s_y[q];
+    for (int i = threadIdx.x; i < q; i += NT) s_y[i] = __dsub_rn(s_y[i], __dmul_rn(__ldcg(Umat + (size_t)q * ldu + i), sq));
+  }
+  __syncthreads();
+  double f[1] = {0.0};
+  for (int i = threadIdx.x; i < l; i += NT) f[0] += s_y[i] * s_y[i];
+  block_sum<1>(f, sh, s_part);
+  return s_part[0];
 }
 
 // ---------------------------------------------------------- the solve
@@ -1455,7 +1502,7 @@ struct DevSet {
   int nv;  // ranks in this launch (1 = one rank per process/GPU)
 };
 
-template <class W, int L, bool VR>
+template <class W, int L, bool VR, bool MON = false>
 __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ DevSet ds) {
   // (VR = false: a static index keeps every field of d a constant-bank operand)
   const int vr = VR ? (int)blockIdx.x / ds.G : 0;
@@ -1540,6 +1587,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     W* src = wb0;
     W* dst = wb1;
     int J = 0;
+    double mon_fro2 = 0.0;  // orthogonality monitor: ‖S‖_F² of this cycle (policy 3)
     bool fail = false;
     for (int j = 1; j <= d.m; ++j) {
       // ------------ w = M⁻¹ A v_j, v_j (own rows) → V   (lines 100, 105)
@@ -1552,11 +1600,15 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       tick(PH_SPMV);
       // ------------ orthogonalise (line 101) and ‖w‖ (line 104)
       double NN;
-      if (!ortho_phase<W>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) {
+      if (!ortho_phase<W, MON>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) {
         fail = true;
         break;
       }
       tick(PH_ORTHO);
+      // ------------ orthogonality monitor (policy 3, reading R23): the new column
+      // of S_k = (I+U_k)⁻¹U_k by unit upper back-substitution, ‖S‖_F² accumulated
+      if (MON && d.policy == 3 && NN > 0.0) mon_fro2 += orth_column(d.Umat, d.m + 1, j, cta == 0, s_y, sh, s_part);
+      const bool orth = MON && d.policy == 3 && sqrt(mon_fro2) >= d.orth_thresh;
       // ------------ h_{j+1,j}, Givens, exit test (lines 104, 108–140, 98)
       const double hn = sqrt(NN);
       if (threadIdx.x == 0) {
@@ -1568,7 +1620,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
         }
         s_rhs[j] = sabs;
         const bool stall = d.stall_w > 0 && j >= d.stall_w && sabs * d.stall_factor > s_rhs[j - d.stall_w];
-        sh.flag = (j == jmax) || (hn == 0.0) || (sabs <= thr) || stall || !isfinite(hn);
+        sh.flag = (j == jmax) || (hn == 0.0) || (sabs <= thr) || stall || orth || !isfinite(hn);
       }
       __syncthreads();
       inner_len++;
