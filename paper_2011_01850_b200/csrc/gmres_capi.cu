@@ -42,6 +42,8 @@ struct gmres_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
   // workspace
   int ws_m = -1, ws_prec = -1, ws_G = 0;
+  int ws_v_tb = -1;       // basis layout (block height, 0 = column-major) the workspace V last held
+  size_t ws_v_bytes = 0;
   char* d_ws = nullptr;
   size_t ws_bytes = 0;
   void* d_V = nullptr;
@@ -266,12 +268,17 @@ void* pick_kernel(int prec, int kind, int L) {
 int kmax_for(int m) { return std::max(m + 1, 8); }
 
 // shared staging region: two CSR chunk stages, or two V tiles of ≥ 32 rows
-int tile_bytes_for(int m) { return std::max(TILE_BYTES, 2 * (m + 2) * ROWALIGN * 8); }
+constexpr size_t kMaxDynSmem = 227 * 1024;
+// staging region: all the shared memory the fixed arrays (kmax-sized) and the
+// static control block leave, at least the block stream's ring (TILE_BYTES)
+int tile_bytes_for(int m) {
+  const size_t fixed = SmemLayout(std::max(m + 1, 8), 0).total + 4096;  // + static Shm and slack
+  const size_t avail = (kMaxDynSmem - fixed) & ~size_t(127);
+  return (int)std::max<size_t>(TILE_BYTES, avail);
+}
 size_t smem_bytes(int m, int tile_bytes = 0) {
   return SmemLayout(kmax_for(m), tile_bytes ? tile_bytes : tile_bytes_for(m)).total;
 }
-constexpr size_t kMaxDynSmem = 227 * 1024;
-
 struct OccKey { const void* k; size_t smem; };
 thread_local std::vector<std::pair<OccKey, int>> g_occ;  // (kernel, smem) → blocks per SM
 
@@ -488,6 +495,8 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   CK(cudaMemsetAsync(ctx->d_ws, 0, off, ctx->stream));
   ctx->ws_bytes = off;
   ctx->d_V = ctx->d_ws + oV;
+  ctx->ws_v_bytes = ow0 - oV;
+  ctx->ws_v_tb = -1;
   ctx->d_w0 = ctx->d_ws + ow0;
   ctx->d_w1 = ctx->d_ws + ow1;
   ctx->d_slots = (double*)(ctx->d_ws + oP);
@@ -819,7 +828,9 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   const void* kern = virt ? pick_solve_virtual(precision, L)
                            : policy == 3 ? pick_solve_monitor(precision, L) : pick_solve(precision, L);
   if (virt && policy == 3) return fail(ctx, GMRES_EINVAL, "restart_policy 3 is not available for virtual ranks");
-  int tile_bytes = tile_bytes_for(m);
+  // CGSR's row tiles take all the shared memory left; MGS needs only the CSR
+  // stream's ring (more L1 for the non-resident sweep's loads)
+  int tile_bytes = ortho == GMRES_CGSR ? tile_bytes_for(m) : TILE_BYTES;
   size_t smem = smem_bytes(m, tile_bytes);
   int G = 0;
   if (int rc = grid_for(ctx, kern, smem, opts ? opts->ctas_per_sm : 0, &G)) return rc;
@@ -854,6 +865,14 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   if (int rc = ensure_ws(ctx, m, precision, G, hist_cap_dev, inner_cap_dev)) return rc;
 
   CK(cudaEventRecord(ctx->ev0, st));
+  // The padding rows (n ≤ row < nvec) of V must read as zero (the passes run over
+  // whole row blocks; zero padding keeps w's padding zero).  MGS (column-major)
+  // and CGSR (row-blocked) solves share the workspace, and one layout's padding
+  // aliases the other's data: clear V whenever the layout changes.
+  if (ctx->ws_v_tb != vl.tb) {
+    CK(cudaMemsetAsync(ctx->d_V, 0, ctx->ws_v_bytes, st));
+    ctx->ws_v_tb = vl.tb;
+  }
   if (ctx->dist()) {  // the arrival counter stays monotonic (epoch base): only the flags reset
     CK(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * 8, st));
   } else if (int rc = reset_flags(ctx, st)) {
@@ -1321,6 +1340,7 @@ int comp_setup(gmres_ctx* ctx, int prec, int m_req, int kind, int L, const void*
 }
 // pack the caller's column-major V into the workspace V in row-blocked layout
 int pack_blocked(gmres_ctx* ctx, int prec, const void* d_V, int64_t ldv, int ncols, const VLayout& vl) {
+  ctx->ws_v_tb = -1;  // the workspace V now holds packed data: clear it before the next solve
   const long long nvalid = std::min<long long>(ldv, ctx->n);
   if (prec == GMRES_MIXED)
     pack_vblocked_kernel<float><<<ctx->sms * 4, 256, 0, ctx->stream>>>((const float*)d_V, ldv, ncols, ctx->nvec, nvalid,
