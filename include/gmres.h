@@ -116,6 +116,17 @@ int gmres_get_cycle_iters(gmres_ctx* ctx, int32_t* buf, int32_t cap, int32_t* le
  * over CTAs of the CTA's own SpMV time.  Returns the count written. */
 int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap);
 
+/* Launch plan of the last solve (host-side choices, for tests and tuning):
+ * [0] CTAs, [1] SpMV lanes per row, [2] MGS variant (0 global sweep,
+ * 1 whole-vector TMA ring, 2 chunk ring with w partly in shared memory),
+ * [3] ring depth (vectors for 1, 8 KB chunk slots for 2), [4] chunks of w in
+ * shared memory (variant 2), [5] staging bytes, [6] dynamic shared memory per
+ * CTA, [7] block CSR stream (0/1), [8] CGSR row-tile height (0: column-major
+ * basis).  buf is host memory of cap ≥ 0 entries; returns the count written
+ * (≤ GMRES_PLAN_N), or GMRES_EINVAL for a null argument. */
+#define GMRES_PLAN_N 9
+int gmres_get_plan(gmres_ctx* ctx, int32_t* buf, int32_t cap);
+
 /* Instrumentation (outside any timed region): copy columns [col0, col0+ncols)
  * of the Krylov basis V left by the last solve on ctx — the basis of its last
  * cycle, v_1..v_J in columns 0..J−1 — into d_dst (device, column-major,

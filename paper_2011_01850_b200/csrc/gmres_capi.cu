@@ -88,6 +88,7 @@ struct gmres_ctx {
   std::vector<double> inner_host;
   std::vector<int32_t> cycJ_host;
   double phase_ns[PH_N] = {0};
+  int32_t plan[GMRES_PLAN_N] = {0};  // launch plan of the last solve (gmres_get_plan)
   std::string err;
   // basis of the last solve (gmres_get_basis): layout, m, precision
   int last_m = 0, last_prec = -1;
@@ -225,6 +226,13 @@ void* pick_solve(int prec, int L) {
 void* pick_solve_monitor(int prec, int L) {
   if (prec == GMRES_MIXED) return L == 1 ? (void*)&solve_kernel<float, 1, false, true> : (void*)&solve_kernel<float, 4, false, true>;
   return L == 1 ? (void*)&solve_kernel<double, 1, false, true> : (void*)&solve_kernel<double, 4, false, true>;
+}
+
+// chunk-ring MGS launches (d.mgs_resident == 2): L ∈ {1, 4}
+void* pick_solve_chunked(int prec, int L) {
+  if (prec == GMRES_MIXED)
+    return L == 1 ? (void*)&solve_kernel<float, 1, false, false, true> : (void*)&solve_kernel<float, 4, false, false, true>;
+  return L == 1 ? (void*)&solve_kernel<double, 1, false, false, true> : (void*)&solve_kernel<double, 4, false, false, true>;
 }
 
 // virtual-rank launches (several row blocks on one device): L ∈ {1, 4}
@@ -580,6 +588,7 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.rank = 0;
   d.sys_scope = 0;
   d.mgs_nbuf = 2;
+  d.mgs_wsm = 0;
   d.R = ctx->d_R;
   d.y = ctx->d_y;
   d.abort_flag = ctx->d_flags;
@@ -838,27 +847,44 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   const VLayout vl = (opts && (opts->tune & 4096)) ? VLayout{} :
                      vlayout_for(ortho, m, precision == GMRES_MIXED ? 4 : 8, tile_bytes);
   if (int rc = ensure_partition(ctx, G, vl.tb ? vl.tb : ROWALIGN)) return rc;
-  // resident MGS (gmres_kernels.cuh mgs_resident): every CTA's rows of w in
-  // ≤ MGS_MV 16-byte registers per thread, and a ring of NB = 3 (else 2)
-  // shared buffers of one basis-vector row block for the TMA stream
-  int mgs_resident = 0, mgs_nbuf = 2;
-  {
+  // resident MGS: every CTA's rows of w on chip.  mgs_resident: w in ≤ MGS_MV
+  // 16-byte registers per thread and a ring of NB = 3 (else 2) shared buffers
+  // of one basis-vector row block; else mgs_chunked: the rest of w in shared
+  // memory and a ring of ≥ one vector's worth of MGS_CHUNK-byte slots
+  int mgs_resident = 0, mgs_nbuf = 2, mgs_wsm = 0;
+  if (ortho == GMRES_MGS) {
     const int wb = precision == GMRES_MIXED ? 4 : 8;
     const int per_vec = 16 / wb;
     const int nq = ctx->part_max_rows / per_vec;
     const int buf_bytes = ((nq + 7) & ~7) * 16;
     const int tune = opts ? opts->tune : 0;
-    for (int nb = (tune & 256) ? 2 : 3; nb >= 2 && ortho == GMRES_MGS && nq <= MGS_MV * NT && !mgs_resident; --nb) {
-      const int tb = std::max(tile_bytes, nb * buf_bytes);
-      if (smem_bytes(m, tb) > kMaxDynSmem) continue;
+    auto fits = [&](const void* k, int tb) {
       int G2 = 0;
-      if (grid_for(ctx, kern, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 >= G) {
+      return smem_bytes(m, tb) <= kMaxDynSmem &&
+             grid_for(ctx, k, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 >= G;
+    };
+    for (int nb = (tune & 256) ? 2 : 3; nb >= 2 && nq <= MGS_MV * NT && !(tune & (4 | 8192)) && !mgs_resident; --nb) {
+      const int tb = std::max(tile_bytes, nb * buf_bytes);
+      if (fits(kern, tb)) {
         mgs_resident = 1;
         mgs_nbuf = nb;
         tile_bytes = tb;
-        smem = smem_bytes(m, tb);
       }
     }
+    if (!mgs_resident && !(tune & 4) && !virt && policy != 3 && (L == 1 || L == 4)) {  // the chunk-ring kernels
+      const int nch = (nq + NT - 1) / NT;
+      const int wsm = std::max(0, nch - MGS_MV);
+      const int ns = std::min<int>(MGS_MAXSLOT, tile_bytes_for(m) / MGS_CHUNK - wsm);
+      const int tb = std::max(tile_bytes, (ns + wsm) * MGS_CHUNK);
+      if (ns >= nch && fits(pick_solve_chunked(precision, L), tb)) {
+        kern = pick_solve_chunked(precision, L);
+        mgs_resident = 2;
+        mgs_nbuf = ns;
+        mgs_wsm = wsm;
+        tile_bytes = tb;
+      }
+    }
+    if (mgs_resident) smem = smem_bytes(m, tile_bytes);
   }
   const int hist_cap_dev = max_cycles + 2;
   const int inner_cap_dev = P.rec_inner ? (int)std::min<int64_t>((int64_t)max_cycles * m, 1 << 22) : 0;
@@ -907,6 +933,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   d.tile_bytes = tile_bytes;
   d.mgs_resident = mgs_resident;
   d.mgs_nbuf = mgs_nbuf;
+  d.mgs_wsm = mgs_wsm;
   set_vlayout(d, vl);
   d.tune = opts ? opts->tune : 0;
   if (ctx->dist()) {
@@ -945,6 +972,11 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   P.G = G;
   P.smem = smem;
   P.d = d;
+  {
+    const int32_t pl[GMRES_PLAN_N] = {G, L, d.mgs_resident, d.mgs_nbuf, d.mgs_wsm, tile_bytes, (int32_t)smem,
+                                      d.block_stream, vl.tb};
+    std::copy(pl, pl + GMRES_PLAN_N, ctx->plan);
+  }
   ctx->last_m = m;
   ctx->last_prec = precision;
   ctx->last_vl = vl;
@@ -1290,6 +1322,13 @@ int gmres_get_basis(gmres_ctx* ctx, int32_t col0, int32_t ncols, void* d_dst, in
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));
   return 0;
+}
+
+int gmres_get_plan(gmres_ctx* ctx, int32_t* buf, int32_t cap) {
+  if (!ctx || !buf) return fail(ctx, GMRES_EINVAL, "null argument");
+  const int k = std::min(cap, (int32_t)GMRES_PLAN_N);
+  std::copy(ctx->plan, ctx->plan + k, buf);
+  return k;
 }
 
 int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap) {

@@ -140,8 +140,9 @@ struct Dev {
   unsigned long long* prof_cta;  // [G] per-CTA own SpMV ns (profile mode)
   int profile;          // != 0: grid barrier after every phase (clean attribution)
   int tune;             // developer A/B switches (bit 0: no L2 prefetch in MGS, bit 2: no resident MGS)
-  int mgs_resident;     // != 0: every CTA's w and v_{i-1} rows fit MGS_MV vectors per thread (resident MGS)
-  int mgs_nbuf;         // TMA ring depth of the resident MGS (2 or 3 basis-vector buffers)
+  int mgs_resident;     // 1: whole-vector ring (mgs_resident), 2: chunk ring (mgs_chunked), 0: mgs_sweep
+  int mgs_nbuf;         // ring depth: basis-vector buffers (mgs_resident) or MGS_CHUNK-byte slots (mgs_chunked)
+  int mgs_wsm;          // chunks of w kept in shared memory (after the ring) by the resident MGS
   long long timeout_ns;
 };
 
@@ -235,13 +236,14 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned 
 // per-CTA control block in static shared memory
 struct Shm {
   unsigned long long mbar[NGRP][MAXSTG];  // TMA stage barriers (per CSR-stream group)
-  unsigned long long mbar_v[3];      // TMA barriers of the resident-MGS basis buffers
+  unsigned long long mbar_v[32];     // TMA barriers of the resident MGS's ring (≤ MGS_MAXSLOT)
   unsigned long long mbar_t[3];      // TMA barriers of the row-tile passes' V tiles
   unsigned long long mbar_b[NBS];    // TMA barriers of the block stream's stages
   int bcnt[NBS];                     // warps done with a block-stream stage
   unsigned bphase;                   // bit s: parity of the next completion of mbar_b[s]
   unsigned tma_phase[NGRP];          // bit s: parity of the next completion of stage s
-  unsigned vphase;                   // bit b: parity of the next completion of mbar_v[b]
+  unsigned vphase;                   // bit b: parity of the next completion of mbar_v[b] (mgs_resident)
+  unsigned vg;                       // chunk-ring MGS: stream chunks issued so far (thread 0 writes)
   unsigned tphase;                   // bit b: parity of the next completion of mbar_t[b]
   int abort;
   int flag;
@@ -277,12 +279,13 @@ __device__ __forceinline__ void init_shm(Shm& sh, int cta) {
     sh.red_epoch = 0;
     sh.abort = 0;
     sh.flag = 0;
+    sh.vg = 0;
     sh.vphase = 0;
     for (int g = 0; g < NGRP; ++g) {
       sh.tma_phase[g] = 0;
       for (int t = 0; t < MAXSTG; ++t) mbar_init(&sh.mbar[g][t], 1);
     }
-    for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_v[b], 1);
+    for (int b = 0; b < 32; ++b) mbar_init(&sh.mbar_v[b], 1);
     for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_t[b], 1);
     sh.tphase = 0;
     for (int b = 0; b < NBS; ++b) { mbar_init(&sh.mbar_b[b], 1); sh.bcnt[b] = 0; }
@@ -1269,7 +1272,7 @@ struct SmemLayout {
 // of v_{i+NB−1} is issued into it, so the HBM reads of the next vectors overlap
 // the all-reduce and no register holds an in-flight load across it.  Same
 // operations and order per element as mgs_sweep.
-constexpr int MGS_MV = 8;  // 16-byte vectors of w per thread (registers)
+constexpr int MGS_MV = 8;  // 16-byte vectors of w per thread in registers (both resident variants)
 template <class W>
 __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
                                              W* w, double* s_h, char* s_tiles, double& NN) {
@@ -1373,6 +1376,141 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   return true;
 }
 
+// ------------------------------------------------------------------ a3 (chunk ring)
+// MGS with the CTA's rows of w on chip and the basis
+// streamed through a ring of d.mgs_nbuf chunk slots of MGS_CHUNK bytes in
+// shared memory by TMA bulk copies.  Chunk k of a CTA's row block holds the
+// 16-byte vector k·NT + t of thread t: w's chunks k < MGS_MV sit in thread
+// registers, the rest (d.mgs_wsm of them) in shared memory after the ring,
+// and a thread reads exactly its own vector of each basis chunk.  The chunks of
+// v_1, v_2, … form one stream (counter sh.vg, persistent over the kernel: the
+// parity of stream chunk g's barrier is (g / nslots) & 1) that runs as far
+// ahead as the ring allows: the slots of v_i are refilled as soon as
+// w ← RN_W(w − RN_W(h_i)·v_i) (line 155) has read them, so the reads of the
+// next vectors overlap h_i's all-reduce.  Step i: partial of h_i = w·v_i
+// (line 154), all-reduce, update with v_i.  Same operations and order per
+// element as mgs_sweep.  (Used when two whole vectors do not fit on chip:
+// the unfused update costs a pass and a barrier per step, mgs_resident.)
+constexpr int MGS_CHUNK = NT * 16;    // bytes of one ring slot = one vector of every thread
+constexpr int MGS_MAXSLOT = 32;       // ring slots (barriers in Shm)
+template <class W>
+__device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
+                                             W* w, double* s_h, char* s_tiles, double& NN) {
+  using V4 = typename VecT<W>::T;
+  constexpr int N = VecT<W>::N;
+  const int q0 = r0 / N, nq = r1 / N - q0;
+  const int nch = (nq + NT - 1) / NT;  // chunks per basis vector
+  const unsigned NS = (unsigned)d.mgs_nbuf;
+  const unsigned g0 = sh.vg;           // stream index of v_1's first chunk
+  const unsigned gend = g0 + (unsigned)(j * nch);
+  V4* sv = reinterpret_cast<V4*>(s_tiles);
+  V4* ws = sv + (size_t)NS * NT - (size_t)MGS_MV * NT;  // w's chunk k ≥ MGS_MV at ws + k·NT
+  // lanes of warp 0 issue stream chunks [lo, hi), one chunk per lane and round
+  // (warp 1 performs the all-reduce's release)
+  auto issue = [&](unsigned lo, unsigned hi) {
+    if (threadIdx.x < 32)
+      for (unsigned g = lo + (threadIdx.x & 31); g < hi; g += 32) {
+        const unsigned rel = g - g0;
+        const int c = (int)(rel / (unsigned)nch), k = (int)(rel % (unsigned)nch);
+        const unsigned bytes = (unsigned)min(NT, nq - k * NT) * 16u;
+        const unsigned s = g % NS;
+        mbar_expect_tx(&sh.mbar_v[s], bytes);
+        tma_load_1d(sv + (size_t)s * NT, V + (long long)c * ldv + r0 + (long long)k * NT * N, bytes, &sh.mbar_v[s]);
+      }
+  };
+  auto wait = [&](unsigned g) -> bool {
+    const unsigned s = g % NS, par = (g / NS) & 1u;
+    if (mbar_try_wait(&sh.mbar_v[s], par)) return true;
+    const unsigned long long t0 = globaltimer();
+    for (;;) {
+      if (mbar_try_wait(&sh.mbar_v[s], par)) return true;
+      if ((long long)(globaltimer() - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); return false; }
+    }
+  };
+  unsigned issued = min(gend, g0 + NS);
+  issue(g0, issued);
+  V4 wr[MGS_MV];
+  const V4* wg = reinterpret_cast<const V4*>(w) + q0;
+#pragma unroll
+  for (int k = 0; k < MGS_MV; ++k) {
+    const int t = threadIdx.x + k * NT;
+    if (t < nq) wr[k] = wg[t];
+  }
+  for (int t = threadIdx.x + MGS_MV * NT; t < nq; t += NT) ws[t] = wg[t];
+  const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
+  unsigned long long tp = lead ? globaltimer() : 0ull;
+  auto tick = [&](int slot) {
+    if (lead) { const unsigned long long t = globaltimer(); d.prof[slot] += t - tp; tp = t; }
+  };
+  for (int i = 1; i <= j; ++i) {
+    const unsigned gi = g0 + (unsigned)((i - 1) * nch);  // v_i's first chunk
+    const int s0 = (int)(gi % NS);  // v_i's chunks sit in slots s0, s0+1, … (mod NS; NS ≥ nch)
+    auto slot = [&](int k) -> const V4* {
+      const int s = s0 + k < (int)NS ? s0 + k : s0 + k - (int)NS;
+      return sv + (size_t)s * NT + threadIdx.x;
+    };
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < MGS_MV; ++k) {
+      if (k < nch) {
+        if (!wait(gi + k)) return false;
+        if (threadIdx.x + k * NT < nq) acc += dotv(wr[k], *slot(k));
+      }
+    }
+    for (int k = MGS_MV; k < nch; ++k) {
+      if (!wait(gi + k)) return false;
+      if (threadIdx.x + k * NT < nq) acc += dotv(ws[k * NT + threadIdx.x], *slot(k));
+    }
+    tick(9);
+    double h;
+    // refill the slots freed by step i−1's update while the reduction is in flight
+    // (a warp that issues bulk copies stalls until the TMA unit takes them)
+    auto mid = [&]() {
+      const unsigned hi = min(gend, gi + NS);
+      if (hi > issued) issue(issued, hi);
+    };
+    if (!allreduce1(d, sh, acc, false, h, mid)) return false;
+    issued = max(issued, min(gend, gi + NS));
+    if (threadIdx.x == 0) s_h[i - 1] = h;
+    const W hw = RN<W>(h);
+    auto upd = [&](V4& a, const V4& x) {
+      W* pa = reinterpret_cast<W*>(&a);
+      const W* pb = reinterpret_cast<const W*>(&x);
+#pragma unroll
+      for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hw, pb[u]));
+    };
+#pragma unroll
+    for (int k = 0; k < MGS_MV; ++k)
+      if (threadIdx.x + k * NT < nq) upd(wr[k], *slot(k));
+    for (int k = MGS_MV; k < nch; ++k)
+      if (threadIdx.x + k * NT < nq) upd(ws[k * NT + threadIdx.x], *slot(k));
+    __syncthreads();  // v_i's slots are free
+    // v_{i+1}'s chunks not in flight yet (a ring of < 2 vectors) go now, the rest in step i+1's mid()
+    const unsigned need = min(gend, gi + 2u * (unsigned)nch);
+    if (need > issued) { issue(issued, need); issued = need; }
+    tick(10);
+  }
+  // ‖w‖², w back to global for the next SpMV
+  double nn = 0.0;
+  V4* wo = reinterpret_cast<V4*>(w) + q0;
+#pragma unroll
+  for (int k = 0; k < MGS_MV; ++k) {
+    const int t = threadIdx.x + k * NT;
+    if (t < nq) {
+      nn += dotv(wr[k], wr[k]);
+      wo[t] = wr[k];
+    }
+  }
+  for (int t = threadIdx.x + MGS_MV * NT; t < nq; t += NT) {
+    const V4 a = ws[t];
+    nn += dotv(a, a);
+    wo[t] = a;
+  }
+  if (threadIdx.x == 0) sh.vg = gend;  // read by every thread at entry, before the syncs below
+  NN = nn;  // this thread's share of ‖w‖²; the caller pushes the halo and all-reduces it
+  return true;
+}
+
 // ‖w‖² all-reduce that ends the orthogonalisation.  With the orthogonality
 // monitor (policy 3, reading R23) the dots V_jᵀw of the final w are formed in an
 // extra pass over V_j and all-reduced TOGETHER with ‖w‖² (one reduction of j+1
@@ -1403,16 +1541,26 @@ __device__ __forceinline__ bool final_norm(const Dev& d, Shm& sh, int r0, int r1
 // Orthogonalisation of w (own rows) against V[:, 0..j) and its norm: MGS
 // or CGSR (two passes).  s_h[0..j) gets
 // h_{1..j, j}; returns ‖w‖² through NN.
-template <class W, bool MON = false>
+// CH: the chunk-ring kernel instantiation (mgs_chunked, launched only with
+// d.mgs_resident == 2); the default one holds mgs_resident and mgs_sweep.  Each
+// MGS variant lives in its own kernel: inlined together they raise the register
+// pressure of every phase (tools/regcheck.sh).
+template <class W, bool MON = false, bool CH = false>
 __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
                             double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
                             char* s_tiles, double& NN) {
-  if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4)) {
+  if constexpr (CH) {
+    if (d.ortho == 0) {
+      double nn = 0.0;
+      if (!mgs_chunked<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
+      return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
+    }
+  } else if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4)) {
     double nn = 0.0;
     if (!mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
     return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
   }
-  if (d.ortho == 0) {
+  if (!CH && d.ortho == 0) {
     W hprev = (W)0;
     const bool pf = !(d.tune & 1) && r1 > r0;
     const unsigned pf_bytes = (unsigned)((r1 - r0) * (int)sizeof(W));
@@ -1502,7 +1650,7 @@ struct DevSet {
   int nv;  // ranks in this launch (1 = one rank per process/GPU)
 };
 
-template <class W, int L, bool VR, bool MON = false>
+template <class W, int L, bool VR, bool MON = false, bool CH = false>
 __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ DevSet ds) {
   // (VR = false: a static index keeps every field of d a constant-bank operand)
   const int vr = VR ? (int)blockIdx.x / ds.G : 0;
@@ -1600,7 +1748,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       tick(PH_SPMV);
       // ------------ orthogonalise (line 101) and ‖w‖ (line 104)
       double NN;
-      if (!ortho_phase<W, MON>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) {
+      if (!ortho_phase<W, MON, CH>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) {
         fail = true;
         break;
       }

@@ -69,6 +69,8 @@ def load_library():
     L.gmres_get_cycle_iters.argtypes = [vp, vp, i32, ctypes.POINTER(i32)]
     L.gmres_get_cycle_iters.restype = ctypes.c_int
     L.gmres_get_phase_ns.argtypes = [vp, vp, i32]
+    L.gmres_get_plan.argtypes = [vp, vp, i32]
+    L.gmres_get_plan.restype = ctypes.c_int
     L.gmres_get_basis.argtypes = [vp, i32, i32, vp, i64]
     L.gmres_get_basis.restype = ctypes.c_int
     L.gmres_get_phase_ns.restype = ctypes.c_int
@@ -295,6 +297,17 @@ class Solver:
         out = self._finish(rc, res, hist, hl, record_inner)
         out.x = x
         return out
+
+    PLAN_KEYS = ("ctas", "lanes", "mgs_variant", "ring", "w_smem_chunks", "stage_bytes", "smem", "block_stream",
+                 "row_tile")
+
+    def plan(self) -> dict:
+        """Launch plan of the last solve (gmres_get_plan): grid, SpMV lanes, MGS variant, staging sizes."""
+        buf = np.zeros(len(self.PLAN_KEYS), np.int32)
+        k = self._lib.gmres_get_plan(self._h, _p(buf), len(buf))
+        if k < 0:
+            raise RuntimeError("gmres_get_plan failed")
+        return dict(zip(self.PLAN_KEYS, buf[:k].tolist()))
 
     def basis(self, ncols, precision, col0=0):
         """gmres_get_basis: columns of the last solve's Krylov basis as a (ncols, n) torch tensor."""

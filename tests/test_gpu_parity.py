@@ -337,6 +337,32 @@ def test_full_size(name):
     S.close()
 
 
+# ------------------------------------------------------------------ MGS variants (DESIGN.md §5 a3)
+# The global sweep, the whole-vector TMA ring and the chunk ring perform the
+# same operations in the same order per element and per thread partial
+# (reading R9), so their solves agree bit for bit; sizes are
+# picked so each ring engages (fp64 chunk ring: > 8 register vectors of w per
+# thread; the ragged grid side 109 leaves a partial last chunk).
+@pytest.mark.slow
+@pytest.mark.parametrize("prec,k,variant", [(G.MIXED, 64, 1), (G.FP64, 64, 1), (G.FP64, 109, 2), (G.MIXED, 137, 2)])
+def test_mgs_variants_agree(prec, k, variant):
+    P = inputs.make("C2", k)
+    S = G.Solver.from_csr(P.A)
+    bd = tdev(P.b)
+    xs, its = [], []
+    for tune in (0, 4):   # tune bit 2: force the global sweep
+        xd = torch.zeros_like(bd)
+        r = S.solve_device(bd, xd, m=30, ortho=G.MGS, precision=prec, max_cycles=3, tol=1e-14, tune=tune)
+        assert r.status in (0, 1), r.status_name
+        plan = S.plan()
+        assert plan["mgs_variant"] == (variant if tune == 0 else 0), plan
+        xs.append(xd.cpu().numpy())
+        its.append((r.cycles, list(r.cycle_iters), r.final_relres))
+    assert its[0] == its[1]
+    assert np.array_equal(xs[0], xs[1])
+    S.close()
+
+
 # ------------------------------------------------------------------ basis getter (C5 orthogonality report)
 @pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])   # column-major / row-blocked basis layouts
 @pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
