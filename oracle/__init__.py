@@ -27,6 +27,7 @@ _lib = None
 FP64, MIXED = 0, 1
 MGS, CGSR = 0, 1
 F_CGS1, F_RESID32, F_UPDATE32, F_ACC32 = 1, 2, 4, 8
+F_ILU0, F_ILU32 = 16, 32   # preconditioner (§8 f2, reading R24); default Jacobi
 OK, NOT_CONVERGED = 0, 1
 
 
@@ -57,6 +58,8 @@ def lib():
         L.oracle_spmv32.argtypes = [i64, vp, vp, vp, vp, vp]; L.oracle_spmv32.restype = None
         L.oracle_dinv.argtypes = [i64, vp, vp, vp, vp, vp]; L.oracle_dinv.restype = i32
         L.oracle_cast32.argtypes = [i64, vp, vp]; L.oracle_cast32.restype = i32
+        L.oracle_ilu0.argtypes = [i32, i64, vp, vp, vp, vp, vp]; L.oracle_ilu0.restype = i32
+        L.oracle_ilu0_apply.argtypes = [i32, i64, vp, vp, vp, vp, vp]; L.oracle_ilu0_apply.restype = None
         L.oracle_jacobi_spmv.argtypes = [i32, i64, vp, vp, vp, vp, vp, vp]; L.oracle_jacobi_spmv.restype = None
         L.oracle_resid.argtypes = [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]; L.oracle_resid.restype = i32
         L.oracle_dot.argtypes = [i32, i64, vp, vp]; L.oracle_dot.restype = dbl
@@ -134,6 +137,27 @@ def working_copy(A, prec):
     if prec == MIXED:
         return cast32(A.val), d.astype(np.float32)
     return _c(A.val, np.float64), d
+
+
+def ilu0(prec, A, aW=None):
+    """ILU(0) factors of A_W in W (reading R24): one array on A's
+    pattern, strict lower part = L (unit diagonal implicit), the rest = U."""
+    dt = wdtype(prec)
+    aW = working_copy(A, prec)[0] if aW is None else _c(aW, dt)
+    f = np.empty(A.nnz, dt)
+    bad = np.zeros(1, np.int64)
+    rc = lib().oracle_ilu0(prec, A.n, _p(A.row_ptr), _p(A.col), _p(aW), _p(f), _p(bad))
+    if rc != 0:
+        raise ZeroDivisionError(f"ILU(0): zero or missing pivot at row {int(bad[0])}")
+    return f
+
+
+def ilu0_apply(prec, A, f, z):
+    """U⁻¹ L⁻¹ z in W (forward, then backward substitution)."""
+    dt = wdtype(prec)
+    out = np.empty(A.n, dt)
+    lib().oracle_ilu0_apply(prec, A.n, _p(A.row_ptr), _p(A.col), _p(_c(f, dt)), _p(_c(z, dt)), _p(out))
+    return out
 
 
 def jacobi_spmv(prec, A, aW, dinvW, v):

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <vector>
 
 namespace {
@@ -51,6 +52,53 @@ void jacobi_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const W* a, co
       acc = acc + p;
     }
     w[i] = dinv[i] * acc;
+  }
+}
+
+// ILU(0) ("preconditioned with incomplete LU without fill in";
+// reading R24): IKJ elimination restricted to A's pattern, rows in natural
+// order, every operation rounded to W:
+//   for i, for k < i with a_ik in the pattern (ascending):
+//     a_ik ← a_ik / a_kk ;  a_ij ← a_ij − a_ik·a_kj  for j > k with a_ij, a_kj in the pattern.
+// The strict lower part then holds L (unit diagonal implicit), the rest U.
+template <class W>
+int64_t ilu0(int64_t n, const int32_t* rp, const int32_t* ci, W* f) {
+  std::vector<int64_t> dpos(n, -1), pos(n, -1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e)
+      if (ci[e] == i) dpos[i] = e;
+  for (int64_t i = 0; i < n; ++i) {
+    if (dpos[i] < 0) return i;
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) pos[ci[e]] = e;
+    for (int64_t e = rp[i]; e < rp[i + 1] && ci[e] < i; ++e) {
+      const int64_t k = ci[e];
+      f[e] = f[e] / f[dpos[k]];
+      for (int64_t q = dpos[k] + 1; q < rp[k + 1]; ++q)
+        if (pos[ci[q]] >= 0) f[pos[ci[q]]] = f[pos[ci[q]]] - f[e] * f[q];
+    }
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) pos[ci[e]] = -1;
+    if (f[dpos[i]] == (W)0 || !std::isfinite((double)f[dpos[i]])) return i;
+  }
+  return -1;
+}
+
+// M⁻¹ z with M = LU (Alg. 1 lines 90 and 100 with the ILU(0) preconditioner):
+// L y = z (unit lower), then U x = y, each row's sum sequential in ascending
+// column order, in W.
+template <class W>
+void ilu0_apply(int64_t n, const int32_t* rp, const int32_t* ci, const W* f, const W* z, W* out) {
+  std::vector<W> y(n);
+  for (int64_t i = 0; i < n; ++i) {
+    W t = z[i];
+    for (int64_t e = rp[i]; e < rp[i + 1] && ci[e] < i; ++e) t = t - f[e] * y[ci[e]];
+    y[i] = t;
+  }
+  for (int64_t i = n - 1; i >= 0; --i) {
+    int64_t d = rp[i];
+    while (ci[d] < i) ++d;
+    W t = y[i];
+    for (int64_t e = d + 1; e < rp[i + 1]; ++e) t = t - f[e] * out[ci[e]];
+    out[i] = t / f[d];
   }
 }
 
@@ -174,6 +222,26 @@ int oracle_cast32(int64_t cnt, const double* in, float* out) {
     out[e] = (float)in[e];
   }
   return 0;
+}
+
+int oracle_ilu0(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* aW, void* f, int64_t* bad_row) {
+  const int64_t nnz = rp[n];
+  int64_t bad;
+  if (prec == ORACLE_MIXED) {
+    std::memcpy(f, aW, sizeof(float) * nnz);
+    bad = ilu0<float>(n, rp, ci, (float*)f);
+  } else {
+    std::memcpy(f, aW, sizeof(double) * nnz);
+    bad = ilu0<double>(n, rp, ci, (double*)f);
+  }
+  if (bad_row) *bad_row = bad;
+  return bad >= 0 ? ORACLE_EZERODIAG : ORACLE_OK;
+}
+
+void oracle_ilu0_apply(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* f, const void* z,
+                       void* out) {
+  if (prec == ORACLE_MIXED) ilu0_apply<float>(n, rp, ci, (const float*)f, (const float*)z, (float*)out);
+  else ilu0_apply<double>(n, rp, ci, (const double*)f, (const double*)z, (double*)out);
 }
 
 void oracle_jacobi_spmv(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* aW,
@@ -332,7 +400,8 @@ template <class W>
 int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* ci, const W* aW, const W* dinvW,
             const W* r, int m, double thr, W* V, int64_t ldv, double* Hbar, double* R, double* s, int32_t* Jout,
             int32_t* bd_out, double* inner_hist, int jmax = 0, int stall_w = 0, double stall_factor = 1.0,
-            OrthMonitor* mon = nullptr, double* mon_hist = nullptr) {
+            OrthMonitor* mon = nullptr, double* mon_hist = nullptr,
+            const std::function<void(const W*, W*)>* ilu = nullptr) {
   if (jmax <= 0 || jmax > m) jmax = m;
   std::vector<double> sabs_hist(m + 1), ucol(mon ? m + 1 : 0);
   if (mon) mon->init(m);
@@ -351,7 +420,17 @@ int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* c
   int J = 0, breakdown = 0;
   for (int j = 1; j <= m; ++j) {  // lines 98–99
     const W* vj = V + (int64_t)(j - 1) * ldv;
-    jacobi_spmv<W>(n, rp, ci, aW, dinvW, vj, w.data());  // line 100
+    if (ilu) {  // line 100 with M = LU (reading R24): t = A_W v_j (row sums in W), w = U⁻¹L⁻¹t
+      std::vector<W> t(n);
+      for (int64_t i = 0; i < n; ++i) {
+        W acc = 0;
+        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) acc = acc + aW[e] * vj[ci[e]];
+        t[i] = acc;
+      }
+      (*ilu)(t.data(), w.data());
+    } else {
+      jacobi_spmv<W>(n, rp, ci, aW, dinvW, vj, w.data());  // line 100
+    }
     for (int i = 0; i <= m; ++i) h[i] = 0.0;
     if (ortho == ORACLE_MGS) mgs<W>(n, j, V, ldv, w.data(), h.data(), acc32);  // line 101
     else cgsr<W>(n, j, V, ldv, w.data(), h.data(), passes, acc32);
@@ -416,6 +495,31 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
     aW[e] = (W)a[e];
   }
   for (int64_t i = 0; i < n; ++i) dinvW[i] = (W)dinv64[i];
+  // ILU(0) preconditioner (§8 f2, reading R24): factors in W from A_W, or in
+  // fp32 from RN32(A64) inside the fp64 solver ("single-precision ILU")
+  std::vector<W> fW;
+  std::vector<float> f32, t32a, t32b;
+  std::function<void(const W*, W*)> pc;
+  if (flags & ORACLE_F_ILU0) {
+    fW = aW;
+    if (ilu0<W>(n, rp, ci, fW.data()) >= 0) return ORACLE_EZERODIAG;
+    pc = [&](const W* in, W* out) { ilu0_apply<W>(n, rp, ci, fW.data(), in, out); };
+  } else if (flags & ORACLE_F_ILU32) {
+    if (mixed) return ORACLE_EINVAL;
+    f32.resize(nnz); t32a.resize(n); t32b.resize(n);
+    for (int64_t e = 0; e < nnz; ++e) {
+      if (std::fabs(a[e]) > (double)FLT_MAX) return ORACLE_EFP32RANGE;
+      f32[e] = (float)a[e];
+    }
+    if (ilu0<float>(n, rp, ci, f32.data()) >= 0) return ORACLE_EZERODIAG;
+    pc = [&](const W* in, W* out) {
+      for (int64_t i = 0; i < n; ++i) t32a[i] = (float)in[i];
+      ilu0_apply<float>(n, rp, ci, f32.data(), t32a.data(), t32b.data());
+      for (int64_t i = 0; i < n; ++i) out[i] = (W)t32b[i];
+    };
+  }
+  const std::function<void(const W*, W*)>* pcp = pc ? &pc : nullptr;
+  std::vector<W> rz(pcp ? n : 0);
   std::vector<float> a32;  // resid32 ablation only
   if (resid32) { a32.resize(nnz); for (int64_t e = 0; e < nnz; ++e) a32[e] = (float)a[e]; }
 
@@ -458,8 +562,10 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
         zuse = (double)((float)b[i] - s32);
       }
       if (mixed && std::fabs(zuse) > (double)FLT_MAX) return ORACLE_EFP32RANGE;
-      r[i] = dinvW[i] * (W)zuse;
+      if (pcp) rz[i] = (W)zuse;
+      else r[i] = dinvW[i] * (W)zuse;
     }
+    if (pcp) (*pcp)(rz.data(), r.data());  // line 90 with M = LU (reading R24)
     double znorm = std::sqrt(zz);
     double rho = znorm / nb;
     if (res->history_len < history_cap) history[res->history_len] = rho;
@@ -478,7 +584,7 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
     int32_t J = 0, bd = 0;
     int rc = arnoldi<W>(ortho, flags, n, rp, ci, aW.data(), dinvW.data(), r.data(), m, thr, V.data(), ldv,
                         Hbar.data(), R.data(), s.data(), &J, &bd, ih.data(), repeat ? J1 : m, stall_w, stall_factor,
-                        policy == ORACLE_POLICY_ORTHLOSS ? &mon : nullptr, mh.data());
+                        policy == ORACLE_POLICY_ORTHLOSS ? &mon : nullptr, mh.data(), pcp);
     if (rc != 0) return rc;
     if (policy == ORACLE_POLICY_ORTHLOSS && orth_hist)
       for (int t = 0; t < J; ++t)

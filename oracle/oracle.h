@@ -26,7 +26,11 @@ enum {
   ORACLE_F_CGS1 = 1,     /* CGSR with one pass only (no re-orthogonalisation) */
   ORACLE_F_RESID32 = 2,  /* residual z = b − A x computed in fp32             */
   ORACLE_F_UPDATE32 = 4, /* solution x stored/updated in fp32                  */
-  ORACLE_F_ACC32 = 8     /* fp32 accumulators for dots/norms (mixed only)      */
+  ORACLE_F_ACC32 = 8,    /* fp32 accumulators for dots/norms (mixed only)      */
+  /* preconditioner selection (§8 f2, reading R24): default Jacobi (R11) */
+  ORACLE_F_ILU0 = 16,    /* ILU(0) factorised and applied in W                 */
+  ORACLE_F_ILU32 = 32    /* fp64 solver with an fp32 ILU(0) ("single-precision
+                            ILU"); requires ORACLE_FP64          */
 };
 enum {
   ORACLE_OK = 0, ORACLE_NOT_CONVERGED = 1, ORACLE_EINVAL = -1, ORACLE_EBADCSR = -2,
@@ -46,6 +50,13 @@ void oracle_spmv64(int64_t n, const int32_t* rp, const int32_t* ci, const double
 void oracle_spmv32(int64_t n, const int32_t* rp, const int32_t* ci, const float* a, const float* x, float* y);
 int oracle_dinv(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, double* dinv64, int64_t* bad_row);
 int oracle_cast32(int64_t cnt, const double* in, float* out);
+/* §8 f2 (reading R24): ILU(0) of A_W on A's pattern, IKJ order, in W
+   (prec): f = factors (strict lower part = L with unit diagonal implicit, rest = U).
+   Returns ORACLE_EZERODIAG (bad_row set) on a missing diagonal or a zero pivot. */
+int oracle_ilu0(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* aW, void* f, int64_t* bad_row);
+/* out = U⁻¹ L⁻¹ z in W (forward then backward substitution, k ascending per row) */
+void oracle_ilu0_apply(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* f, const void* z,
+                       void* out);
 void oracle_jacobi_spmv(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* aW,
                         const void* dinvW, const void* v, void* w);
 int oracle_resid(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const double* a64,

@@ -471,3 +471,119 @@ def test_orthloss_monitor_matches_dense_definition():
                 max_cycles=1)
     hit = np.nonzero(r.orth >= 0.05)[0]
     assert hit.size and len(r.orth) == hit[0] + 1 < m
+
+
+# ------------------------------------------------------------------- ILU(0) (§8 f2, reading R24)
+def _factors_dense(A, f):
+    """Split the combined factor array into dense unit-lower L and upper U."""
+    n = A.n
+    L, U = np.eye(n), np.zeros((n, n))
+    for i in range(n):
+        for e in range(A.row_ptr[i], A.row_ptr[i + 1]):
+            j = int(A.col[e])
+            if j < i:
+                L[i, j] = f[e]
+            else:
+                U[i, j] = f[e]
+    return L, U
+
+
+def lapl2d(k):
+    """5-point Laplacian on a k×k grid (SPEC's 2-D Poisson pin)."""
+    T = lapl1d(k)
+    return np.kron(np.eye(k), T) + np.kron(T, np.eye(k))
+
+
+def test_ilu0_trivial_cases():
+    # diagonal matrix: L = I, U = A (SPEC precond examples); diag(2,4) applied to [2,4] is [1,1]
+    A = csr_from_dense(np.diag([2.0, 3.0]))
+    assert np.array_equal(O.ilu0(O.FP64, A), [2.0, 3.0])
+    A = csr_from_dense(np.diag([2.0, 4.0]))
+    assert np.array_equal(O.ilu0_apply(O.FP64, A, O.ilu0(O.FP64, A), np.array([2.0, 4.0])), [1.0, 1.0])
+    A = csr_from_dense(np.eye(5))
+    z = np.arange(5.0)
+    for prec in (O.FP64, O.MIXED):
+        assert np.array_equal(O.ilu0_apply(prec, A, O.ilu0(prec, A), z), z)
+
+
+@pytest.mark.parametrize("D", [lapl1d(5), random_dd(40, 3, density=0.0) + np.diag(np.full(39, -0.7), 1)
+                               + np.diag(np.full(39, 0.4), -1)], ids=["tridiag5", "tridiag40"])
+def test_ilu0_is_exact_lu_without_fill(D):
+    # tridiagonal: LU has no fill, so ILU(0) = the exact LU (dense product equals A everywhere)
+    A = csr_from_dense(D)
+    f = O.ilu0(O.FP64, A)
+    L, U = _factors_dense(A, f)
+    assert np.allclose(L @ U, D, rtol=0, atol=1e-14 * np.abs(D).max())
+    x = np.random.default_rng(1).uniform(-1, 1, A.n)
+    y = O.ilu0_apply(O.FP64, A, f, D @ x)
+    assert np.linalg.norm(y - x) <= 1e-12 * np.linalg.norm(x)
+    # and it matches the dense solve
+    assert np.allclose(y, np.linalg.solve(D, D @ x), rtol=0, atol=1e-12)
+
+
+def test_ilu0_lower_triangular_is_exact():
+    rng = np.random.default_rng(4)
+    D = np.tril(rng.standard_normal((12, 12)) * (rng.random((12, 12)) < 0.4), -1) + np.diag(rng.uniform(2, 3, 12))
+    A = csr_from_dense(D)
+    x = rng.uniform(-1, 1, 12)
+    y = O.ilu0_apply(O.FP64, A, O.ilu0(O.FP64, A), D @ x)
+    assert np.linalg.norm(y - x) <= 1e-12 * np.linalg.norm(x)
+
+
+def test_ilu0_pattern_identity_2d_poisson():
+    # SPEC: (LU)[i,j] = A[i,j] on the pattern (relative 1e-13), nnz(F) = nnz(A);
+    # off the pattern LU carries the dropped fill (it is incomplete: not A)
+    D = lapl2d(4)
+    A = csr_from_dense(D)
+    f = O.ilu0(O.FP64, A)
+    assert f.size == A.nnz
+    L, U = _factors_dense(A, f)
+    P = L @ U
+    mask = D != 0
+    assert np.allclose(P[mask], D[mask], rtol=1e-13, atol=0)
+    assert np.abs(P[~mask]).max() > 0.05
+    # full LU would differ from ILU(0) on this pattern (the incomplete factor is not exact)
+    x = np.ones(A.n)
+    assert np.linalg.norm(O.ilu0_apply(O.FP64, A, f, D @ x) - x) > 1e-6
+
+
+def test_ilu0_fp32_matches_fp64_to_fp32_roundoff():
+    # SPEC: factorising in LOW then applying equals HIGH to LOW round-off (rel 1e-5), 16×16
+    D = random_dd(16, 7, density=0.4)
+    A = csr_from_dense(D)
+    f64, f32 = O.ilu0(O.FP64, A), O.ilu0(O.MIXED, A)
+    assert f32.dtype == np.float32
+    assert np.allclose(f32, f64, rtol=1e-5, atol=0)
+    z = np.random.default_rng(2).uniform(-1, 1, 16)
+    y64 = O.ilu0_apply(O.FP64, A, f64, z)
+    y32 = O.ilu0_apply(O.MIXED, A, f32, z.astype(np.float32))
+    assert np.allclose(y32, y64, rtol=1e-5, atol=1e-6 * np.abs(y64).max())
+
+
+def test_ilu0_zero_pivot_names_the_row():
+    with pytest.raises(ZeroDivisionError, match="row 1"):
+        O.ilu0(O.FP64, csr_from_dense(np.array([[1.0, 1.0], [1.0, 1.0]])))   # u_22 = 1 − 1·1 = 0
+    with pytest.raises(ZeroDivisionError, match="row 0"):
+        O.ilu0(O.FP64, csr_from_dense(np.array([[0.0, 1.0], [1.0, 2.0]])))   # no diagonal in row 0
+
+
+def test_ilu_gmres_exact_preconditioner_one_step():
+    # M = LU = A (tridiagonal, no fill): M⁻¹A = I, so the first Arnoldi step exits (J = 1)
+    D = lapl1d(30) + np.diag(np.linspace(0.1, 0.5, 29), 1)
+    A = csr_from_dense(D)
+    b = D @ np.random.default_rng(3).uniform(-1, 1, 30)
+    r = O.solve(A, b, m=10, ortho=O.MGS, prec=O.FP64, flags=O.F_ILU0)
+    assert r.inner_iters == 1 and r.final_relres <= 1e-13
+
+
+@pytest.mark.parametrize("prec,flags", [(O.FP64, O.F_ILU0), (O.MIXED, O.F_ILU0), (O.FP64, O.F_ILU32)])
+@pytest.mark.parametrize("ortho", [O.MGS, O.CGSR])
+def test_ilu_gmres_converges_faster_than_jacobi(prec, flags, ortho):
+    # C1-recipe problem (5-pt convection-diffusion): ILU(0) needs fewer inner iterations,
+    # and the mixed / fp32-ILU solves still reach 1e-10 (PAPER.md:428-444)
+    P = inputs.make("C1", 16)
+    rj = O.solve(P.A, P.b, m=30, ortho=ortho, prec=prec)
+    ri = O.solve(P.A, P.b, m=30, ortho=ortho, prec=prec, flags=flags)
+    assert ri.final_relres <= 1e-10 and rj.final_relres <= 1e-10
+    assert ri.inner_iters < rj.inner_iters
+    assert np.linalg.norm(ri.x - P.x_true) <= 1e-8 * np.linalg.norm(P.x_true)
