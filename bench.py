@@ -297,6 +297,21 @@ def run_ours(args, rank, world, local_rank):
                           "model_GBps": model_bytes(n, nnz, 8, ortho, r.cycle_iters) / (r.device_ms * 1e-3) / 1e9}
     speedup = {o: variants[f"fp64_{o}"]["tts_ms"] / variants[f"mixed_{o}"]["tts_ms"] for o in ("mgs", "cgsr")}
 
+    # §8 f2: the paper's preconditioner, ILU(0), on the same problem —
+    # one solve per variant outside the timed step, factorisation included
+    ilu = {}
+    if world == 1 and not args.no_ilu:
+        for prec in (G.MIXED, G.FP64):
+            for ortho in (G.MGS, G.CGSR):
+                xi = torch.zeros_like(x)
+                r = S.solve_device(b, xi, m=M, tol=TOL, ortho=ortho, precision=prec, precond=G.ILU0)
+                assert r.status == 0, r.status_name
+                ilu[("mixed_" if prec == G.MIXED else "fp64_") + ("mgs" if ortho == 0 else "cgsr")] = {
+                    "tts_ms": r.device_ms, "cycles": r.cycles, "inner_iters": r.inner_iters,
+                    "us_per_inner": 1e3 * r.kernel_ms / max(1, r.inner_iters), "final_relres": r.final_relres}
+        lo, up = S.ilu0_levels()
+        ilu["levels"] = {"lower": lo, "upper": up}
+
     # e2e through gmres_solve with pinned host buffers (h2d b, d2h x inside every call)
     hb = torch.from_numpy(prob.b[r0:r1].copy()).pin_memory()
     hb_np = hb.numpy()
@@ -339,6 +354,7 @@ def run_ours(args, rank, world, local_rank):
             "tts_ms": {k: v["tts_ms"] for k, v in variants.items()},
             "mixed_over_fp64_tts_speedup": speedup,
             "variants": variants,
+            "ilu0_untimed": ilu or None,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -356,6 +372,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-ilu", action="store_true", help="skip the untimed ILU(0) solves (§8 f2)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -81,7 +81,15 @@ typedef struct {
                              ‖S_k‖_F ≥ orth_thresh, S_k = (I+U_k)⁻¹U_k, U_k = strict upper
                              part of V_kᵀV_k; ≤ 0 → 1.0.  Adds
                              one pass over the basis per inner iteration               */
+  int32_t precond;        /* left preconditioner M: GMRES_PRECOND_JACOBI (0, default;
+                             reading R11) or GMRES_PRECOND_ILU0 (1: ILU(0) of A_W on A's
+                             pattern, factorised on the device inside every timed solve,
+                             PAPER.md:291, 427; reading R24).  ILU(0): single-rank contexts,
+                             restart policies 0–2                                       */
 } gmres_opts;
+
+#define GMRES_PRECOND_JACOBI 0
+#define GMRES_PRECOND_ILU0 1
 
 /* Create a solver context on the current CUDA device: validates the CSR on the
  * host, copies A (fp64) to the device and extracts the Jacobi diagonal.
@@ -222,6 +230,25 @@ int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_
  * and y[J] = R⁻¹ s_{1..J}. */
 int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar, double beta, double* R,
                        double* s, double* y);
+
+/* §8 f2 (reading R24): ILU(0) of A_W (W = fp32 for GMRES_MIXED
+ * from the fp32 copy of A, fp64 otherwise) on A's pattern, IKJ order, rows in
+ * natural order, one launch per level of the lower dependency graph.  d_f
+ * (device, nnz W values, may be NULL) receives the factors: strict lower part
+ * L (unit diagonal implicit), the rest U, in A's CSR order.  The factors stay
+ * in the context for gmres_k_ilu_apply.  EZERODIAG (message names the row) on a
+ * missing diagonal or a zero / non-finite pivot; single-rank contexts only. */
+int gmres_ilu0_factor(gmres_ctx* ctx, int32_t precision, void* d_f);
+
+/* d_out = U⁻¹ L⁻¹ d_z (device, n W values each; d_out == d_z allowed) with the
+ * factors of the last gmres_ilu0_factor of this precision: level-scheduled
+ * forward then backward substitution, each row's sum in ascending column order
+ * in W (one cooperative launch, a grid barrier per level). */
+int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* d_out);
+
+/* Level counts of the ILU(0) triangular solves (lower, upper): the length of
+ * the dependency chains a level-scheduled solve serialises over. */
+int gmres_ilu0_levels(gmres_ctx* ctx, int32_t* nlev_lower, int32_t* nlev_upper);
 
 /* a0: build the fp32 copy of A on the device (also rebuilt
  * inside every mixed solve, timed).  EFP32RANGE on overflow. */

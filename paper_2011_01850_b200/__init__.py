@@ -7,7 +7,7 @@ device memory, streams and process groups.  There is no CPU fallback: if the
 CUDA library is missing, importing the binding raises.
 """
 from .gmres import (  # noqa: F401
-    CGSR, FP64, MGS, MIXED, GmresError, Solver, SolveResult, library_path, load_library,
+    CGSR, FP64, ILU0, JACOBI, MGS, MIXED, GmresError, Solver, SolveResult, library_path, load_library,
 )
 
-__all__ = ["Solver", "SolveResult", "GmresError", "MGS", "CGSR", "FP64", "MIXED", "load_library", "library_path"]
+__all__ = ["Solver", "SolveResult", "GmresError", "MGS", "CGSR", "FP64", "MIXED", "JACOBI", "ILU0", "load_library", "library_path"]

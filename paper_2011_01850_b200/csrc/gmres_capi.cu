@@ -37,6 +37,18 @@ struct gmres_ctx {
   double* d_dinv64 = nullptr;
   float* d_dinv32 = nullptr;
   cudaStream_t stream = nullptr;
+  // ILU(0) (§8 f2): level schedules (built once per context) and the factors per
+  // precision (index = gmres_precision)
+  bool ilu_plan = false;
+  int ilu_nlev[2] = {0, 0};
+  std::vector<int> ilu_hlev0;  // lower-solve level offsets (one factor launch per level)
+  int* d_ilu_dpos = nullptr;
+  int* d_ilu_lev[2] = {nullptr, nullptr};
+  int* d_ilu_rows[2] = {nullptr, nullptr};
+  void* d_ilu_f[2] = {nullptr, nullptr};
+  bool ilu_ready[2] = {false, false};
+  void* d_ones[2] = {nullptr, nullptr};  // W ones (nvec): the Jacobi scale of ILU solves
+  int* d_ilu_bad = nullptr;
   double* d_hb = nullptr;  // device staging of b / x for the host-array gmres_solve
   double* d_hx = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
@@ -235,6 +247,15 @@ void* pick_solve_chunked(int prec, int L) {
   return L == 1 ? (void*)&solve_kernel<double, 1, false, false, true> : (void*)&solve_kernel<double, 4, false, false, true>;
 }
 
+// ILU(0)-preconditioned launches (§8 f2): L ∈ {1, 4}
+void* pick_solve_ilu(int prec, int L) {
+  if (prec == GMRES_MIXED)
+    return L == 1 ? (void*)&solve_kernel<float, 1, false, false, false, true>
+                  : (void*)&solve_kernel<float, 4, false, false, false, true>;
+  return L == 1 ? (void*)&solve_kernel<double, 1, false, false, false, true>
+                : (void*)&solve_kernel<double, 4, false, false, false, true>;
+}
+
 // virtual-rank launches (several row blocks on one device): L ∈ {1, 4}
 void* pick_solve_virtual(int prec, int L) {
   if (prec == GMRES_MIXED) return L == 1 ? (void*)&solve_kernel<float, 1, true> : (void*)&solve_kernel<float, 4, true>;
@@ -263,6 +284,7 @@ void* pick_kernel_templ(int kind, int L) {
         default: return (void*)&k_resid_kernel<W, 32>;
       }
     case 2: return (void*)&k_ortho_kernel<W>;
+    case 4: return (void*)&k_ilu_apply_kernel<W>;
     default: return (void*)&k_xupdate_kernel<W>;
   }
 }
@@ -561,6 +583,111 @@ int ensure_a32(gmres_ctx* ctx, cudaStream_t st, bool force = false) {
   return 0;
 }
 
+// ---------------------------------------------------------------- ILU(0) (§8 f2)
+// Level schedules of the triangular solves (reading R24): lower level of row i =
+// 1 + max over its columns k < i (0 if none), upper level = 1 + max over k > i;
+// rows sorted by level, ascending row inside a level.  The factorisation follows
+// the lower schedule.
+int ensure_ilu_plan(gmres_ctx* ctx) {
+  if (ctx->ilu_plan) return 0;
+  if (ctx->dist()) return fail(ctx, GMRES_EINVAL, "ILU(0) needs a single-rank context");
+  const int64_t n = ctx->n, nnz = ctx->nnz;
+  const std::vector<int32_t>& rp = ctx->h_rp;
+  std::vector<int32_t> ci(nnz);
+  CK(cudaMemcpy(ci.data(), ctx->d_ci, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+  std::vector<int> dpos(n, -1), lev(n);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e)
+      if (ci[e] == i) dpos[i] = (int)e;
+    if (dpos[i] < 0) return fail(ctx, GMRES_EZERODIAG, "ILU(0): row " + std::to_string(i) + " has no diagonal entry");
+  }
+  auto sched = [&](int t, bool lower) -> int {
+    int nl = 0;
+    for (int64_t s = 0; s < n; ++s) {
+      const int64_t i = lower ? s : n - 1 - s;
+      int l = 0;
+      const int64_t e0 = lower ? rp[i] : dpos[i] + 1, e1 = lower ? dpos[i] : rp[i + 1];
+      for (int64_t e = e0; e < e1; ++e) l = std::max(l, lev[ci[e]] + 1);
+      lev[i] = l;
+      nl = std::max(nl, l + 1);
+    }
+    std::vector<int> off(nl + 1, 0), rows(n);
+    for (int64_t i = 0; i < n; ++i) off[lev[i] + 1]++;
+    for (int l = 0; l < nl; ++l) off[l + 1] += off[l];
+    std::vector<int> cur(off.begin(), off.end() - 1);
+    for (int64_t i = 0; i < n; ++i) rows[cur[lev[i]]++] = (int)i;
+    if (cudaMalloc(&ctx->d_ilu_lev[t], sizeof(int) * (nl + 1)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ilu_rows[t], sizeof(int) * n) != cudaSuccess)
+      return -1;
+    cudaMemcpy(ctx->d_ilu_lev[t], off.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->d_ilu_rows[t], rows.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+    ctx->ilu_nlev[t] = nl;
+    if (lower) ctx->ilu_hlev0 = off;
+    return 0;
+  };
+  if (sched(0, true) || sched(1, false)) return fail(ctx, GMRES_ENOMEM, "ILU(0) level schedule allocation failed");
+  CK(cudaMalloc(&ctx->d_ilu_dpos, sizeof(int) * n));
+  CK(cudaMemcpy(ctx->d_ilu_dpos, dpos.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->d_ilu_bad, sizeof(int)));
+  ctx->ilu_plan = true;
+  return 0;
+}
+
+// factorise A_W (mixed: the fp32 copy, already (re)built on st) into
+// d_ilu_f[prec]: copy, then one launch per lower level; a zero pivot is reported
+// unless the fp32 cast overflowed (the solve reports that)
+int ilu_factor(gmres_ctx* ctx, int prec, cudaStream_t st) {
+  if (int rc = ensure_ilu_plan(ctx)) return rc;
+  const size_t wb = prec == GMRES_MIXED ? 4 : 8;
+  if (!ctx->d_ilu_f[prec]) CK(cudaMalloc(&ctx->d_ilu_f[prec], wb * (ctx->nnz + ARR_PAD)));
+  if (!ctx->d_ones[prec]) {
+    CK(cudaMalloc(&ctx->d_ones[prec], wb * ctx->nvec));
+    if (prec == GMRES_MIXED) {
+      std::vector<float> one(ctx->nvec, 1.0f);
+      CK(cudaMemcpy(ctx->d_ones[prec], one.data(), wb * ctx->nvec, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<double> one(ctx->nvec, 1.0);
+      CK(cudaMemcpy(ctx->d_ones[prec], one.data(), wb * ctx->nvec, cudaMemcpyHostToDevice));
+    }
+  }
+  ctx->ilu_ready[prec] = false;
+  const void* src = prec == GMRES_MIXED ? (const void*)ctx->d_a32 : (const void*)ctx->d_a64;
+  CK(cudaMemcpyAsync(ctx->d_ilu_f[prec], src, wb * ctx->nnz, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(ctx->d_ilu_bad, 0x7f, sizeof(int), st));
+  const std::vector<int>& off = ctx->ilu_hlev0;
+  for (int l = 0; l < ctx->ilu_nlev[0]; ++l) {
+    const int cnt = off[l + 1] - off[l];
+    const int blocks = (cnt + 255) / 256;
+    if (prec == GMRES_MIXED)
+      ilu_factor_level_kernel<float><<<blocks, 256, 0, st>>>(ctx->d_rp, ctx->d_ci, ctx->d_ilu_dpos,
+                                                             ctx->d_ilu_rows[0] + off[l], cnt,
+                                                             (float*)ctx->d_ilu_f[prec], ctx->d_ilu_bad);
+    else
+      ilu_factor_level_kernel<double><<<blocks, 256, 0, st>>>(ctx->d_rp, ctx->d_ci, ctx->d_ilu_dpos,
+                                                              ctx->d_ilu_rows[0] + off[l], cnt,
+                                                              (double*)ctx->d_ilu_f[prec], ctx->d_ilu_bad);
+  }
+  CK(cudaGetLastError());
+  int hb[2] = {0, 0};
+  CK(cudaMemcpyAsync(&hb[0], ctx->d_ilu_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (ctx->d_flags) CK(cudaMemcpyAsync(&hb[1], ctx->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hb[0] != 0x7f7f7f7f && !(prec == GMRES_MIXED && hb[1] != 0))
+    return fail(ctx, GMRES_EZERODIAG, "ILU(0): zero or non-finite pivot at row " + std::to_string(hb[0]));
+  ctx->ilu_ready[prec] = true;
+  return 0;
+}
+
+void set_ilu_dev(gmres_ctx* ctx, Dev& d, int prec) {
+  d.iluW = ctx->d_ilu_f[prec];
+  d.ilu_dpos = ctx->d_ilu_dpos;
+  for (int t = 0; t < 2; ++t) {
+    d.ilu_lev[t] = ctx->d_ilu_lev[t];
+    d.ilu_rows[t] = ctx->d_ilu_rows[t];
+    d.ilu_nlev[t] = ctx->ilu_nlev[t];
+  }
+}
+
 Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   Dev d{};
   d.n = (int)ctx->n;
@@ -761,6 +888,14 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_a32);
   cudaFree(ctx->d_dinv64);
   cudaFree(ctx->d_dinv32);
+  cudaFree(ctx->d_ilu_dpos);
+  cudaFree(ctx->d_ilu_bad);
+  for (int t = 0; t < 2; ++t) {
+    cudaFree(ctx->d_ilu_lev[t]);
+    cudaFree(ctx->d_ilu_rows[t]);
+    cudaFree(ctx->d_ilu_f[t]);
+    cudaFree(ctx->d_ones[t]);
+  }
   cudaFree(ctx->d_ws);
   cudaFree(ctx->d_hb);
   cudaFree(ctx->d_hx);
@@ -829,13 +964,20 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   int L = (opts && opts->lanes_per_row) ? opts->lanes_per_row : auto_lanes(ctx->n, ctx->nnz);
   if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16 && L != 32)
     return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 1/2/4/8/16/32");
-  if ((virt || policy == 3) && L != 1) L = 4;
+  const int precond = opts ? opts->precond : GMRES_PRECOND_JACOBI;
+  if (precond != GMRES_PRECOND_JACOBI && precond != GMRES_PRECOND_ILU0)
+    return fail(ctx, GMRES_EINVAL, "precond must be 0 (Jacobi) or 1 (ILU(0))");
+  const bool ilu = precond == GMRES_PRECOND_ILU0;
+  if (ilu && (virt || ctx->dist())) return fail(ctx, GMRES_EINVAL, "ILU(0) needs a single-rank context");
+  if (ilu && policy == 3) return fail(ctx, GMRES_EINVAL, "restart_policy 3 is not available with ILU(0)");
+  if ((virt || policy == 3 || ilu) && L != 1) L = 4;
   P.st = stream ? (cudaStream_t)stream : ctx->stream;
   P.prec = precision;
   const cudaStream_t st = P.st;
 
   const void* kern = virt ? pick_solve_virtual(precision, L)
-                           : policy == 3 ? pick_solve_monitor(precision, L) : pick_solve(precision, L);
+                    : policy == 3 ? pick_solve_monitor(precision, L)
+                    : ilu ? pick_solve_ilu(precision, L) : pick_solve(precision, L);
   if (virt && policy == 3) return fail(ctx, GMRES_EINVAL, "restart_policy 3 is not available for virtual ranks");
   // CGSR's row tiles take all the shared memory left; MGS needs only the CSR
   // stream's ring (more L1 for the non-resident sweep's loads)
@@ -871,7 +1013,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
         tile_bytes = tb;
       }
     }
-    if (!mgs_resident && !(tune & 4) && !virt && policy != 3 && (L == 1 || L == 4)) {  // the chunk-ring kernels
+    if (!mgs_resident && !(tune & 4) && !virt && policy != 3 && !ilu && (L == 1 || L == 4)) {  // the chunk-ring kernels
       const int nch = (nq + NT - 1) / NT;
       const int wsm = std::max(0, nch - MGS_MV);
       const int ns = std::min<int>(MGS_MAXSLOT, tile_bytes_for(m) / MGS_CHUNK - wsm);
@@ -909,6 +1051,8 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
     if (int rc = launch_cast(ctx, st, ctx->d_flags + 1)) return rc;
     ctx->a32_ready = false;  // validated only by a completed solve
   }
+  if (ilu)  // ILU(0) factorisation, inside the timed solve
+    if (int rc = ilu_factor(ctx, precision, st)) return rc;
   double* xin = ctx->dist() ? ctx->d_gx + ctx->row_begin : d_x;  // the kernel's x (local view)
   if (d_x0 && d_x0 != xin) CK(cudaMemcpyAsync(xin, d_x0, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
   if (!d_x0) CK(cudaMemsetAsync(xin, 0, sizeof(double) * ctx->n, st));
@@ -934,6 +1078,10 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   d.mgs_resident = mgs_resident;
   d.mgs_nbuf = mgs_nbuf;
   d.mgs_wsm = mgs_wsm;
+  if (ilu) {  // M = LU: the SpMV/residual epilogues scale by one, the kernel applies U⁻¹L⁻¹
+    set_ilu_dev(ctx, d, precision);
+    d.dinvW = ctx->d_ones[precision];
+  }
   set_vlayout(d, vl);
   d.tune = opts ? opts->tune : 0;
   if (ctx->dist()) {
@@ -1570,3 +1718,45 @@ int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar,
 }
 
 }  // extern "C"
+
+int gmres_ilu0_factor(gmres_ctx* ctx, int32_t precision, void* d_f) {
+  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
+  if (int rc = check_prec(ctx, precision)) return rc;
+  if (ctx->dist()) return fail(ctx, GMRES_EINVAL, "ILU(0) needs a single-rank context");
+  if (precision == GMRES_MIXED)
+    if (int rc = ensure_a32(ctx, ctx->stream)) return rc;
+  if (int rc = ilu_factor(ctx, precision, ctx->stream)) return rc;
+  if (d_f)
+    CK(cudaMemcpyAsync(d_f, ctx->d_ilu_f[precision], (precision == GMRES_MIXED ? 4 : 8) * ctx->nnz,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* d_out) {
+  if (!ctx || !d_z || !d_out) return fail(ctx, GMRES_EINVAL, "null argument");
+  if (int rc = check_prec(ctx, precision)) return rc;
+  if (!ctx->ilu_ready[precision]) return fail(ctx, GMRES_EINVAL, "no ILU(0) factors of this precision: call gmres_ilu0_factor");
+  const void* kern;
+  int G;
+  size_t smem;
+  int mws;
+  if (int rc = comp_setup(ctx, precision, 1, 4, 1, &kern, &G, &smem, &mws)) return rc;
+  Dev d = make_dev(ctx, mws, precision, 0, G);
+  set_ilu_dev(ctx, d, precision);
+  void* args[] = {&d, (void*)&d_z, &d_out};
+  if (int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream)) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  int flags[2] = {0, 0};
+  CK(cudaMemcpy(flags, ctx->d_flags, sizeof(int) * 2, cudaMemcpyDeviceToHost));
+  if (flags[0]) return fail(ctx, GMRES_ETIMEOUT, "grid barrier watchdog fired");
+  return 0;
+}
+
+int gmres_ilu0_levels(gmres_ctx* ctx, int32_t* nlev_lower, int32_t* nlev_upper) {
+  if (!ctx || !nlev_lower || !nlev_upper) return fail(ctx, GMRES_EINVAL, "null argument");
+  if (int rc = ensure_ilu_plan(ctx)) return rc;
+  *nlev_lower = ctx->ilu_nlev[0];
+  *nlev_upper = ctx->ilu_nlev[1];
+  return 0;
+}

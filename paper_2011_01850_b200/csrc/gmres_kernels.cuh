@@ -144,6 +144,15 @@ struct Dev {
   int mgs_nbuf;         // ring depth: basis-vector buffers (mgs_resident) or MGS_CHUNK-byte slots (mgs_chunked)
   int mgs_wsm;          // chunks of w kept in shared memory (after the ring) by the resident MGS
   long long timeout_ns;
+  // ILU(0) preconditioner (§8 f2, reading R24; PC kernel instantiations only):
+  // factors on A's pattern (W), diagonal position per row, and the level
+  // schedules of the lower (forward) and upper (backward) triangular solves:
+  // rows of level l are ilu_rows[t][ilu_lev[t][l] .. ilu_lev[t][l+1])
+  const void* iluW;
+  const int* ilu_dpos;
+  const int* ilu_lev[2];
+  const int* ilu_rows[2];
+  int ilu_nlev[2];
 };
 
 // ------------------------------------------------------------ primitives
@@ -947,6 +956,73 @@ __device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __rest
   csr_any_stream<W, L>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, epi);
 }
 
+// ------------------------------------------------------------------ f2: ILU(0)
+// Factorisation (reading R24), one launch per level of the lower
+// dependency graph, one thread per row in the IKJ order of the oracle: for each
+// k < i in row i (ascending) l_ik = a_ik / u_kk, then a_ij −= l_ik·u_kj over the
+// columns j > k common to rows i and k (a merge of the two sorted rows).  Rows
+// k belong to earlier levels (earlier launches).  A zero or non-finite pivot
+// records the smallest such row in *bad.
+template <class W>
+__global__ void ilu_factor_level_kernel(const int* __restrict__ rp, const int* __restrict__ ci,
+                                        const int* __restrict__ dpos, const int* __restrict__ rows, int cnt, W* f,
+                                        int* bad) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int i = rows[t];
+  const int e_end = rp[i + 1], di = dpos[i];
+  for (int e = rp[i]; e < di; ++e) {
+    const int k = ci[e];
+    const W lik = f[e] / f[dpos[k]];
+    f[e] = lik;
+    int p = e + 1;
+    const int q_end = rp[k + 1];
+    for (int q = dpos[k] + 1; q < q_end; ++q) {
+      const int cj = ci[q];
+      while (p < e_end && ci[p] < cj) ++p;
+      if (p == e_end) break;
+      if (ci[p] == cj) f[p] = subw(f[p], mulw(lik, f[q]));
+    }
+  }
+  const W u = f[di];
+  if (u == (W)0 || !isfinite((double)u)) atomicMin(bad, i);
+}
+
+// M⁻¹: out = U⁻¹ L⁻¹ in (in == out allowed), level by level over the whole grid
+// with a grid barrier between levels; each row's sum runs sequentially in
+// ascending column order in W, as in the oracle (bit-identical).  Rows of
+// other CTAs are read through L2 (__ldcg).
+template <class W>
+__device__ bool ilu_apply_phase(const Dev& d, Shm& sh, const W* in, W* out) {
+  const W* __restrict__ f = (const W*)d.iluW;
+  const int gt = sh.cta * NT + threadIdx.x, gs = d.G * NT;
+  for (int l = 0; l < d.ilu_nlev[0]; ++l) {  // L y = in (unit lower)
+    const int a = d.ilu_lev[0][l], b = d.ilu_lev[0][l + 1];
+    for (int t = a + gt; t < b; t += gs) {
+      const int i = d.ilu_rows[0][t];
+      W acc = __ldcg(in + i);
+      const int e1 = d.ilu_dpos[i];
+      for (int e = d.rp[i]; e < e1; ++e) acc = subw(acc, mulw(f[e], __ldcg(out + d.ci[e])));
+      out[i] = acc;
+    }
+    if (!grid_sync(d, sh)) return false;
+  }
+  for (int l = 0; l < d.ilu_nlev[1]; ++l) {  // U out = y
+    const int a = d.ilu_lev[1][l], b = d.ilu_lev[1][l + 1];
+    for (int t = a + gt; t < b; t += gs) {
+      const int i = d.ilu_rows[1][t];
+      W acc = __ldcg(out + i);
+      const int e0 = d.ilu_dpos[i], e1 = d.rp[i + 1];
+      for (int e = e0 + 1; e < e1; ++e) acc = subw(acc, mulw(f[e], __ldcg(out + d.ci[e])));
+      out[i] = acc / f[e0];
+    }
+    // the next phase may stage these rows with bulk copies (async proxy)
+    if (l + 1 == d.ilu_nlev[1]) fence_proxy_async_global();
+    if (!grid_sync(d, sh)) return false;
+  }
+  return true;
+}
+
 // ------------------------------------------------------------------ a3
 // One fused MGS sweep over the CTA's rows:
 //   w ← RN_W(w − RN_W(RN_W(h_prev)·v_prev))  (line 155 of step i−1), then
@@ -1650,7 +1726,7 @@ struct DevSet {
   int nv;  // ranks in this launch (1 = one rank per process/GPU)
 };
 
-template <class W, int L, bool VR, bool MON = false, bool CH = false>
+template <class W, int L, bool VR, bool MON = false, bool CH = false, bool PC = false>
 __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ DevSet ds) {
   // (VR = false: a static index keeps every field of d a constant-bank operand)
   const int vr = VR ? (int)blockIdx.x / ds.G : 0;
@@ -1719,7 +1795,17 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if ((ef & ERRF_RANGE) || RR > DBL_MAX) { status = ST_EFP32RANGE; break; }
     if (rho <= d.tol) { status = ST_OK; break; }
     if (k >= d.max_cycles) { status = ST_NOT_CONVERGED; break; }
-    const double beta = sqrt(RR);
+    double RRp = RR;
+    if constexpr (PC) {  // line 90 with M = LU (reading R24): r = U⁻¹L⁻¹ RN_W(z), then ‖r‖²
+      if (!ilu_apply_phase<W>(d, sh, wb0, wb0)) { status = ST_ETIMEOUT; break; }
+      double p = 0.0;
+      for (int i = r0 + threadIdx.x; i < min(r1, d.n); i += NT) {
+        const double v = (double)__ldcg(wb0 + i);
+        p += v * v;
+      }
+      if (!allreduce1(d, sh, p, true, RRp)) { status = ST_ETIMEOUT; break; }
+    }
+    const double beta = sqrt(RRp);
     if (!(beta > 0.0) || !isfinite(beta)) { status = ST_ENONFINITE; break; }
     // restart threshold (readings R6, R22): the two-stage policy drops δ after
     // the first cycle and restarts at the first cycle's iteration count J1
@@ -1741,6 +1827,9 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       // ------------ w = M⁻¹ A v_j, v_j (own rows) → V   (lines 100, 105)
       const unsigned long long ts0 = d.profile && threadIdx.x == 0 ? globaltimer() : 0ull;
       spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V, j - 1);
+      if constexpr (PC) {  // w = U⁻¹L⁻¹(A_W v_j) (line 100 with M = LU)
+        if (!grid_sync(d, sh) || !ilu_apply_phase<W>(d, sh, dst, dst)) { fail = true; break; }
+      }
       if (d.profile) {
         if (threadIdx.x == 0) d.prof_cta[cta] += globaltimer() - ts0;
         if (!grid_sync(d, sh)) { fail = true; break; }
@@ -1866,6 +1955,12 @@ template <class W, int L>
 __global__ void __launch_bounds__(NT, 1) k_spmv_kernel(Dev d, const W* v, W* w) {
   G200_SMEM_CARVE(W)
   spmv_phase<W, L>(d, sh, s_tiles, v, 1.0, w, (W*)nullptr, 0);
+}
+
+template <class W>
+__global__ void __launch_bounds__(NT, 1) k_ilu_apply_kernel(Dev d, const W* z, W* out) {
+  G200_SMEM_CARVE(W)
+  ilu_apply_phase<W>(d, sh, z, out);
 }
 
 template <class W, int L>

@@ -18,6 +18,7 @@ _LIB_PATH = os.path.join(_HERE, "libgmres.so")
 _lib = None
 
 MGS, CGSR = 0, 1
+JACOBI, ILU0 = 0, 1   # preconditioners (gmres_opts.precond)
 THRESHOLD, TWOSTAGE, STALL, ORTHLOSS = 0, 1, 2, 3   # restart policies (gmres_opts.restart_policy)
 FP64, MIXED = 0, 1
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "EBADCSR", -3: "EZERODIAG", -4: "EFP32RANGE",
@@ -40,7 +41,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("delta", ctypes.c_double), ("max_cycles", ctypes.c_int32), ("record_inner", ctypes.c_int32),
                 ("lanes_per_row", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32), ("profile", ctypes.c_int32),
                 ("tune", ctypes.c_int32), ("restart_policy", ctypes.c_int32), ("stall_factor", ctypes.c_double),
-                ("stall_frac", ctypes.c_double), ("orth_thresh", ctypes.c_double)]
+                ("stall_frac", ctypes.c_double), ("orth_thresh", ctypes.c_double), ("precond", ctypes.c_int32)]
 
 
 def library_path() -> str:
@@ -70,6 +71,12 @@ def load_library():
     L.gmres_get_cycle_iters.restype = ctypes.c_int
     L.gmres_get_phase_ns.argtypes = [vp, vp, i32]
     L.gmres_get_plan.argtypes = [vp, vp, i32]
+    L.gmres_ilu0_factor.argtypes = [vp, i32, vp]
+    L.gmres_ilu0_factor.restype = ctypes.c_int
+    L.gmres_k_ilu_apply.argtypes = [vp, i32, vp, vp]
+    L.gmres_k_ilu_apply.restype = ctypes.c_int
+    L.gmres_ilu0_levels.argtypes = [vp, vp, vp]
+    L.gmres_ilu0_levels.restype = ctypes.c_int
     L.gmres_get_plan.restype = ctypes.c_int
     L.gmres_get_basis.argtypes = [vp, i32, i32, vp, i64]
     L.gmres_get_basis.restype = ctypes.c_int
@@ -220,8 +227,9 @@ class Solver:
 
     @staticmethod
     def _opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile=False, tune=0, policy=0,
-              stall_factor=0.0, stall_frac=0.0, orth_thresh=0.0):
+              stall_factor=0.0, stall_frac=0.0, orth_thresh=0.0, precond=0):
         o = _Opts()
+        o.precond = int(precond)
         o.orth_thresh = float(orth_thresh)
         o.restart_policy = int(policy)
         o.stall_factor = float(stall_factor)
@@ -256,7 +264,7 @@ class Solver:
 
     def solve(self, b, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None, max_cycles=None,
               record_inner=False, lanes=0, ctas_per_sm=0, out=None, policy=THRESHOLD,
-              orth_thresh=0.0) -> SolveResult:
+              orth_thresh=0.0, precond=0) -> SolveResult:
         """gmres_solve: host arrays in, host x out (h2d/d2h inside the call).  `out` may be a
         preallocated (e.g. pinned) float64 array of length n."""
         b = np.ascontiguousarray(b, np.float64)
@@ -270,7 +278,8 @@ class Solver:
         hist = np.zeros(mc + 2)
         hl = ctypes.c_int32()
         res = _Result()
-        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, policy=policy, orth_thresh=orth_thresh)
+        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, policy=policy, orth_thresh=orth_thresh,
+                       precond=precond)
         rc = self._lib.gmres_solve(self._h, _p(b), _p(x0c), _p(x), int(m), float(tol), _ortho(ortho),
                                    _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
                                    ctypes.byref(hl))
@@ -280,8 +289,9 @@ class Solver:
 
     def solve_device(self, b, x, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None,
                      max_cycles=None, record_inner=False, lanes=0, ctas_per_sm=0, stream=None,
-                     profile=False, tune=0, policy=THRESHOLD) -> SolveResult:
-        """gmres_solve_device on torch CUDA float64 tensors (x is written in place)."""
+                     profile=False, tune=0, policy=THRESHOLD, precond=0) -> SolveResult:
+        """gmres_solve_device on torch CUDA float64 tensors (x is written in place).
+        precond: JACOBI (0) or ILU0 (1, §8 f2)."""
         import torch
         for t in (b, x) + ((x0,) if x0 is not None else ()):
             assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() == self.n
@@ -290,13 +300,38 @@ class Solver:
         hist = np.zeros(mc + 2)
         hl = ctypes.c_int32()
         res = _Result()
-        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile, tune, policy)
+        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile, tune, policy, precond=precond)
         rc = self._lib.gmres_solve_device(self._h, _p(b), _p(x0), _p(x), int(m), float(tol), _ortho(ortho),
                                           _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
                                           ctypes.byref(hl), ctypes.c_void_p(st.cuda_stream))
         out = self._finish(rc, res, hist, hl, record_inner)
         out.x = x
         return out
+
+    def ilu0_factor(self, precision):
+        """gmres_ilu0_factor: ILU(0) factors of A_W on the device (torch tensor, nnz W values)."""
+        import torch
+        f = torch.empty(self.nnz, dtype=torch.float32 if precision == MIXED else torch.float64, device="cuda")
+        rc = self._lib.gmres_ilu0_factor(self._h, _prec(precision), _p(f))
+        if rc < 0:
+            raise self._err(rc)
+        return f
+
+    def ilu_apply(self, z, precision):
+        """gmres_k_ilu_apply: U⁻¹L⁻¹ z with the last factors of this precision (torch tensors)."""
+        import torch
+        out = torch.empty_like(z)
+        rc = self._lib.gmres_k_ilu_apply(self._h, _prec(precision), _p(z), _p(out))
+        if rc < 0:
+            raise self._err(rc)
+        return out
+
+    def ilu0_levels(self):
+        lo, up = ctypes.c_int32(), ctypes.c_int32()
+        rc = self._lib.gmres_ilu0_levels(self._h, ctypes.byref(lo), ctypes.byref(up))
+        if rc < 0:
+            raise self._err(rc)
+        return lo.value, up.value
 
     PLAN_KEYS = ("ctas", "lanes", "mgs_variant", "ring", "w_smem_chunks", "stage_bytes", "smem", "block_stream",
                  "row_tile")
