@@ -45,7 +45,11 @@ struct gmres_ctx {
   int* d_ilu_dpos = nullptr;
   int* d_ilu_lev[2] = {nullptr, nullptr};
   int* d_ilu_rows[2] = {nullptr, nullptr};
+  int* d_ilu_eoff[2] = {nullptr, nullptr};
+  int* d_ilu_ecol[2] = {nullptr, nullptr};
+  int* d_ilu_eidx[2] = {nullptr, nullptr};
   void* d_ilu_f[2] = {nullptr, nullptr};
+  void* d_ilu_rec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [precision][solve]
   bool ilu_ready[2] = {false, false};
   void* d_ones[2] = {nullptr, nullptr};  // W ones (nvec): the Jacobi scale of ILU solves
   int* d_ilu_bad = nullptr;
@@ -616,11 +620,33 @@ int ensure_ilu_plan(gmres_ctx* ctx) {
     for (int l = 0; l < nl; ++l) off[l + 1] += off[l];
     std::vector<int> cur(off.begin(), off.end() - 1);
     for (int64_t i = 0; i < n; ++i) rows[cur[lev[i]]++] = (int)i;
-    if (cudaMalloc(&ctx->d_ilu_lev[t], sizeof(int) * (nl + 1)) != cudaSuccess ||
-        cudaMalloc(&ctx->d_ilu_rows[t], sizeof(int) * n) != cudaSuccess)
+    // entry lists per slot: the row's strictly lower (T = 0) or upper (T = 1) entries
+    std::vector<int> eoff(n + 1, 0), ecol, eidx;
+    for (int64_t s = 0; s < n; ++s) {
+      const int i = rows[s];
+      const int64_t e0 = lower ? rp[i] : dpos[i] + 1, e1 = lower ? dpos[i] : rp[i + 1];
+      for (int64_t e = e0; e < e1; ++e) {
+        ecol.push_back(ci[e]);
+        eidx.push_back((int)e);
+      }
+      eoff[s + 1] = (int)ecol.size();
+    }
+    const size_t ne = std::max<size_t>(ecol.size(), 1);
+    if (cudaMalloc(&ctx->d_ilu_lev[t], sizeof(int) * (nl + 2)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ilu_rows[t], sizeof(int) * n) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ilu_eoff[t], sizeof(int) * (n + 1)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ilu_ecol[t], sizeof(int) * ne) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ilu_eidx[t], sizeof(int) * ne) != cudaSuccess)
       return -1;
-    cudaMemcpy(ctx->d_ilu_lev[t], off.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice);
+    off.push_back(off.back());  // lev[nl + 1]: the prefetch of "level nl" reads an empty range
+    cudaMemcpy(ctx->d_ilu_lev[t], off.data(), sizeof(int) * (nl + 2), cudaMemcpyHostToDevice);
+    off.pop_back();
     cudaMemcpy(ctx->d_ilu_rows[t], rows.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->d_ilu_eoff[t], eoff.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice);
+    if (!ecol.empty()) {
+      cudaMemcpy(ctx->d_ilu_ecol[t], ecol.data(), sizeof(int) * ecol.size(), cudaMemcpyHostToDevice);
+      cudaMemcpy(ctx->d_ilu_eidx[t], eidx.data(), sizeof(int) * eidx.size(), cudaMemcpyHostToDevice);
+    }
     ctx->ilu_nlev[t] = nl;
     if (lower) ctx->ilu_hlev0 = off;
     return 0;
@@ -667,6 +693,31 @@ int ilu_factor(gmres_ctx* ctx, int prec, cudaStream_t st) {
                                                               ctx->d_ilu_rows[0] + off[l], cnt,
                                                               (double*)ctx->d_ilu_f[prec], ctx->d_ilu_bad);
   }
+  // packed per-slot records of both solves from the new factors
+  const size_t recb = prec == GMRES_MIXED ? sizeof(IluRec<float>) : sizeof(IluRec<double>);
+  for (int t = 0; t < 2; ++t) {
+    if (!ctx->d_ilu_rec[prec][t]) CK(cudaMalloc(&ctx->d_ilu_rec[prec][t], recb * ctx->n));
+    const int blocks = ctx->sms * 8;
+    if (prec == GMRES_MIXED) {
+      if (t == 0)
+        ilu_records_kernel<float, 0><<<blocks, 256, 0, st>>>((int)ctx->n, ctx->d_ilu_rows[0], ctx->d_ilu_eoff[0],
+            ctx->d_ilu_ecol[0], ctx->d_ilu_eidx[0], ctx->d_ilu_dpos, (const float*)ctx->d_ilu_f[prec],
+            (IluRec<float>*)ctx->d_ilu_rec[prec][0]);
+      else
+        ilu_records_kernel<float, 1><<<blocks, 256, 0, st>>>((int)ctx->n, ctx->d_ilu_rows[1], ctx->d_ilu_eoff[1],
+            ctx->d_ilu_ecol[1], ctx->d_ilu_eidx[1], ctx->d_ilu_dpos, (const float*)ctx->d_ilu_f[prec],
+            (IluRec<float>*)ctx->d_ilu_rec[prec][1]);
+    } else {
+      if (t == 0)
+        ilu_records_kernel<double, 0><<<blocks, 256, 0, st>>>((int)ctx->n, ctx->d_ilu_rows[0], ctx->d_ilu_eoff[0],
+            ctx->d_ilu_ecol[0], ctx->d_ilu_eidx[0], ctx->d_ilu_dpos, (const double*)ctx->d_ilu_f[prec],
+            (IluRec<double>*)ctx->d_ilu_rec[prec][0]);
+      else
+        ilu_records_kernel<double, 1><<<blocks, 256, 0, st>>>((int)ctx->n, ctx->d_ilu_rows[1], ctx->d_ilu_eoff[1],
+            ctx->d_ilu_ecol[1], ctx->d_ilu_eidx[1], ctx->d_ilu_dpos, (const double*)ctx->d_ilu_f[prec],
+            (IluRec<double>*)ctx->d_ilu_rec[prec][1]);
+    }
+  }
   CK(cudaGetLastError());
   int hb[2] = {0, 0};
   CK(cudaMemcpyAsync(&hb[0], ctx->d_ilu_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -685,6 +736,10 @@ void set_ilu_dev(gmres_ctx* ctx, Dev& d, int prec) {
     d.ilu_lev[t] = ctx->d_ilu_lev[t];
     d.ilu_rows[t] = ctx->d_ilu_rows[t];
     d.ilu_nlev[t] = ctx->ilu_nlev[t];
+    d.ilu_eoff[t] = ctx->d_ilu_eoff[t];
+    d.ilu_ecol[t] = ctx->d_ilu_ecol[t];
+    d.ilu_eidx[t] = ctx->d_ilu_eidx[t];
+    d.ilu_rec[t] = ctx->d_ilu_rec[prec][t];
   }
 }
 
@@ -893,7 +948,12 @@ void gmres_destroy(gmres_ctx* ctx) {
   for (int t = 0; t < 2; ++t) {
     cudaFree(ctx->d_ilu_lev[t]);
     cudaFree(ctx->d_ilu_rows[t]);
+    cudaFree(ctx->d_ilu_eoff[t]);
+    cudaFree(ctx->d_ilu_ecol[t]);
+    cudaFree(ctx->d_ilu_eidx[t]);
     cudaFree(ctx->d_ilu_f[t]);
+    cudaFree(ctx->d_ilu_rec[t][0]);
+    cudaFree(ctx->d_ilu_rec[t][1]);
     cudaFree(ctx->d_ones[t]);
   }
   cudaFree(ctx->d_ws);

@@ -153,6 +153,13 @@ struct Dev {
   const int* ilu_lev[2];
   const int* ilu_rows[2];
   int ilu_nlev[2];
+  // per slot (level order) of each solve: its off-diagonal entries, contiguous —
+  // ilu_eoff[t][slot] .. [slot+1] index ilu_ecol[t] (column) and ilu_eidx[t]
+  // (position in the factor array), in the row's ascending column order
+  const int* ilu_eoff[2];
+  const int* ilu_ecol[2];
+  const int* ilu_eidx[2];
+  const void* ilu_rec[2];  // packed per-slot records (IluRec<W>), rebuilt after each factorisation
 };
 
 // ------------------------------------------------------------ primitives
@@ -990,37 +997,114 @@ __global__ void ilu_factor_level_kernel(const int* __restrict__ rp, const int* _
 
 // M⁻¹: out = U⁻¹ L⁻¹ in (in == out allowed), level by level over the whole grid
 // with a grid barrier between levels; each row's sum runs sequentially in
-// ascending column order in W, as in the oracle (bit-identical).  Rows of
-// other CTAs are read through L2 (__ldcg).
+// ascending column order in W, as in the oracle (bit-identical).  A thread
+// takes slot gt of every level (level-ordered entry lists, built on the host)
+// and loads the next level's row, columns, factor values, diagonal and
+// right-hand side BEFORE the barrier, so after it only the ≤ ILU_KP solution
+// values it depends on remain to be read (through L2: other CTAs wrote them).
+// Slots beyond the first per thread and entries beyond ILU_KP take a plain loop.
+constexpr int ILU_KP = 4;
+// one slot's operands, packed so a level's prefetch is one round of independent
+// 16-byte loads: {row, entries, first entry, –}, 4 columns, 4 factor values, the
+// diagonal (U solve); entries beyond ILU_KP are read from the entry lists
 template <class W>
-__device__ bool ilu_apply_phase(const Dev& d, Shm& sh, const W* in, W* out) {
+struct alignas(16) IluRec {
+  int row, ne, e0, pad;
+  int col[ILU_KP];
+  W val[ILU_KP];
+  W diag;
+  W pad2[16 / sizeof(W) - 1];
+};
+
+template <class W, int T>
+__global__ void ilu_records_kernel(int n, const int* __restrict__ rows, const int* __restrict__ eoff,
+                                   const int* __restrict__ ecol, const int* __restrict__ eidx,
+                                   const int* __restrict__ dpos, const W* __restrict__ f, IluRec<W>* rec) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    IluRec<W> r{};
+    r.row = rows[s];
+    r.e0 = eoff[s];
+    r.ne = eoff[s + 1] - r.e0;
+    for (int k = 0; k < ILU_KP; ++k) {
+      r.col[k] = k < r.ne ? ecol[r.e0 + k] : 0;
+      r.val[k] = k < r.ne ? f[eidx[r.e0 + k]] : (W)0;
+    }
+    r.diag = T == 1 ? f[dpos[r.row]] : (W)1;
+    rec[s] = r;
+  }
+}
+
+template <class W>
+struct IluSlot {
+  IluRec<W> r;
+  W rhs;
+  bool on;
+};
+
+template <class W, int T>
+__device__ __forceinline__ void ilu_load(const Dev& d, const W* rhs_src, int slot, int end, IluSlot<W>& p) {
+  p.on = slot < end;
+  if (!p.on) return;
+  using V4 = int4;
+  const V4* src = reinterpret_cast<const V4*>(reinterpret_cast<const IluRec<W>*>(d.ilu_rec[T]) + slot);
+  V4* dst = reinterpret_cast<V4*>(&p.r);
+#pragma unroll
+  for (int k = 0; k < (int)(sizeof(IluRec<W>) / 16); ++k) dst[k] = __ldg(src + k);
+  if (d.tune & 32768) p.rhs = __ldcg(rhs_src + p.r.row);  // dev A/B: rhs before the barrier
+}
+
+template <class W, int T>
+__device__ __forceinline__ void ilu_row(const Dev& d, const W* __restrict__ f, const IluSlot<W>& p, const W* rhs_src,
+                                        W* out) {
+  // the right-hand side is read with the solution values (one L2 round trip)
+  const W rhs = (d.tune & 32768) ? p.rhs : __ldcg(rhs_src + p.r.row);
+  W x[ILU_KP];
+#pragma unroll
+  for (int k = 0; k < ILU_KP; ++k)
+    if (k < p.r.ne) x[k] = __ldcg(out + p.r.col[k]);
+  W acc = rhs;
+#pragma unroll
+  for (int k = 0; k < ILU_KP; ++k)
+    if (k < p.r.ne) acc = subw(acc, mulw(p.r.val[k], x[k]));
+  for (int k = ILU_KP; k < p.r.ne; ++k)
+    acc = subw(acc, mulw(f[d.ilu_eidx[T][p.r.e0 + k]], __ldcg(out + d.ilu_ecol[T][p.r.e0 + k])));
+  out[p.r.row] = T == 1 ? acc / p.r.diag : acc;
+}
+
+template <class W, int T>
+__device__ __forceinline__ bool ilu_solve(const Dev& d, Shm& sh, const W* rhs_src, W* out) {
   const W* __restrict__ f = (const W*)d.iluW;
   const int gt = sh.cta * NT + threadIdx.x, gs = d.G * NT;
-  for (int l = 0; l < d.ilu_nlev[0]; ++l) {  // L y = in (unit lower)
-    const int a = d.ilu_lev[0][l], b = d.ilu_lev[0][l + 1];
-    for (int t = a + gt; t < b; t += gs) {
-      const int i = d.ilu_rows[0][t];
-      W acc = __ldcg(in + i);
-      const int e1 = d.ilu_dpos[i];
-      for (int e = d.rp[i]; e < e1; ++e) acc = subw(acc, mulw(f[e], __ldcg(out + d.ci[e])));
-      out[i] = acc;
+  const int nl = d.ilu_nlev[T];
+  const int* lev = d.ilu_lev[T];
+  IluSlot<W> p;
+  ilu_load<W, T>(d, rhs_src, lev[0] + gt, lev[1], p);
+  for (int l = 0; l < nl; ++l) {
+    const int a = lev[l], b = lev[l + 1];
+    if (d.tune & 16384) {  // dev A/B: barriers only (wrong results)
+      if (!grid_sync(d, sh)) return false;
+      continue;
     }
-    if (!grid_sync(d, sh)) return false;
-  }
-  for (int l = 0; l < d.ilu_nlev[1]; ++l) {  // U out = y
-    const int a = d.ilu_lev[1][l], b = d.ilu_lev[1][l + 1];
-    for (int t = a + gt; t < b; t += gs) {
-      const int i = d.ilu_rows[1][t];
-      W acc = __ldcg(out + i);
-      const int e0 = d.ilu_dpos[i], e1 = d.rp[i + 1];
-      for (int e = e0 + 1; e < e1; ++e) acc = subw(acc, mulw(f[e], __ldcg(out + d.ci[e])));
-      out[i] = acc / f[e0];
+    if (p.on) ilu_row<W, T>(d, f, p, rhs_src, out);
+    for (int t = a + gt + gs; t < b; t += gs) {  // wide levels: further slots, plain loop
+      const int row = d.ilu_rows[T][t];
+      W acc = __ldcg(rhs_src + row);
+      for (int e = d.ilu_eoff[T][t]; e < d.ilu_eoff[T][t + 1]; ++e)
+        acc = subw(acc, mulw(f[d.ilu_eidx[T][e]], __ldcg(out + d.ilu_ecol[T][e])));
+      out[row] = T == 1 ? acc / f[d.ilu_dpos[row]] : acc;
     }
-    // the next phase may stage these rows with bulk copies (async proxy)
-    if (l + 1 == d.ilu_nlev[1]) fence_proxy_async_global();
+    if (l + 1 < nl) ilu_load<W, T>(d, rhs_src, b + gt, lev[l + 2], p);
+    // the next phase may stage the result with bulk copies (async proxy)
+    if (T == 1 && l + 1 == nl) fence_proxy_async_global();
     if (!grid_sync(d, sh)) return false;
   }
   return true;
+}
+
+template <class W>
+__device__ __noinline__ bool ilu_apply_phase(const Dev& d, Shm& sh, const W* in, W* out) {
+  if (!ilu_solve<W, 0>(d, sh, in, out)) return false;  // L y = in (unit lower)
+  return ilu_solve<W, 1>(d, sh, out, out);              // U out = y
 }
 
 // ------------------------------------------------------------------ a3
