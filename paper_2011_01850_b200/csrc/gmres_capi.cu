@@ -53,6 +53,7 @@ struct gmres_ctx {
   bool ilu_ready[2] = {false, false};
   void* d_ones[2] = {nullptr, nullptr};  // W ones (nvec): the Jacobi scale of ILU solves
   int* d_ilu_bad = nullptr;
+  void* d_ilu_pub[2] = {nullptr, nullptr};  // [n] fp64-sized publish buffers of the sync-free solves
   double* d_hb = nullptr;  // device staging of b / x for the host-array gmres_solve
   double* d_hx = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
@@ -655,6 +656,8 @@ int ensure_ilu_plan(gmres_ctx* ctx) {
   CK(cudaMalloc(&ctx->d_ilu_dpos, sizeof(int) * n));
   CK(cudaMemcpy(ctx->d_ilu_dpos, dpos.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&ctx->d_ilu_bad, sizeof(int)));
+  CK(cudaMalloc(&ctx->d_ilu_pub[0], sizeof(double) * n));
+  CK(cudaMalloc(&ctx->d_ilu_pub[1], sizeof(double) * n));
   ctx->ilu_plan = true;
   return 0;
 }
@@ -680,6 +683,8 @@ int ilu_factor(gmres_ctx* ctx, int prec, cudaStream_t st) {
   const void* src = prec == GMRES_MIXED ? (const void*)ctx->d_a32 : (const void*)ctx->d_a64;
   CK(cudaMemcpyAsync(ctx->d_ilu_f[prec], src, wb * ctx->nnz, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(ctx->d_ilu_bad, 0x7f, sizeof(int), st));
+  for (int t = 0; t < 2; ++t)  // arm the publish buffers (all-ones: the "not yet" NaN)
+    CK(cudaMemsetAsync(ctx->d_ilu_pub[t], 0xff, sizeof(double) * ctx->n, st));
   const std::vector<int>& off = ctx->ilu_hlev0;
   for (int l = 0; l < ctx->ilu_nlev[0]; ++l) {
     const int cnt = off[l + 1] - off[l];
@@ -741,6 +746,8 @@ void set_ilu_dev(gmres_ctx* ctx, Dev& d, int prec) {
     d.ilu_eidx[t] = ctx->d_ilu_eidx[t];
     d.ilu_rec[t] = ctx->d_ilu_rec[prec][t];
   }
+  d.ilu_pub[0] = ctx->d_ilu_pub[0];
+  d.ilu_pub[1] = ctx->d_ilu_pub[1];
 }
 
 Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
@@ -945,6 +952,8 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_dinv32);
   cudaFree(ctx->d_ilu_dpos);
   cudaFree(ctx->d_ilu_bad);
+  cudaFree(ctx->d_ilu_pub[0]);
+  cudaFree(ctx->d_ilu_pub[1]);
   for (int t = 0; t < 2; ++t) {
     cudaFree(ctx->d_ilu_lev[t]);
     cudaFree(ctx->d_ilu_rows[t]);
@@ -1804,6 +1813,8 @@ int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* 
   if (int rc = comp_setup(ctx, precision, 1, 4, 1, &kern, &G, &smem, &mws)) return rc;
   Dev d = make_dev(ctx, mws, precision, 0, G);
   set_ilu_dev(ctx, d, precision);
+  for (int t = 0; t < 2; ++t)
+    CK(cudaMemsetAsync(ctx->d_ilu_pub[t], 0xff, sizeof(double) * ctx->n, ctx->stream));
   void* args[] = {&d, (void*)&d_z, &d_out};
   if (int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream)) return rc;
   CK(cudaStreamSynchronize(ctx->stream));

@@ -160,6 +160,7 @@ struct Dev {
   const int* ilu_ecol[2];
   const int* ilu_eidx[2];
   const void* ilu_rec[2];  // packed per-slot records (IluRec<W>), rebuilt after each factorisation
+  void* ilu_pub[2];        // [n] W each, sync-free solves: published row values (all-ones NaN = not yet)
 };
 
 // ------------------------------------------------------------ primitives
@@ -1101,9 +1102,121 @@ __device__ __forceinline__ bool ilu_solve(const Dev& d, Shm& sh, const W* rhs_sr
   return true;
 }
 
+// Sync-free variant: no barrier per level.  Thread gt takes slots gt, gt + gs, …
+// of the level-ordered slot list (so its rows come in non-decreasing level
+// order).  A row's result is also stored into the publish buffer of its solve,
+// which was filled with the all-ones bit pattern (a NaN that arithmetic never
+// produces: the GPU returns the canonical NaN); a row polls the published
+// values of all its inputs in one round of relaxed loads (re-polling only those
+// still unpublished) and uses them directly — the value is its own ready flag,
+// so no fence sits on the dependency chain.  (Measured on C2: a flag + release/
+// acquire protocol ran 2× slower than the level-synchronous solve; polling the
+// inputs one after another, 1.6× slower than one round.)  Progress: the lowest-level unfinished row has all its
+// inputs done, and every thread is resident (cooperative launch); a watchdog
+// raises the abort flag instead of hanging.  Each solve re-arms the other
+// solve's buffer (the grid barrier between the solves orders it).
+template <class W> struct PubBits;
+template <> struct PubBits<float> { using U = unsigned; static constexpr U SENT = 0xffffffffu; };
+template <> struct PubBits<double> { using U = unsigned long long; static constexpr U SENT = ~0ull; };
+
+__device__ __forceinline__ unsigned ld_relaxed_bits(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_bits(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_bits(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_bits(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// one input of a row beyond the first ILU_KP (27-point stencils, long rows): poll until published
 template <class W>
-__device__ __noinline__ bool ilu_apply_phase(const Dev& d, Shm& sh, const W* in, W* out) {
-  if (!ilu_solve<W, 0>(d, sh, in, out)) return false;  // L y = in (unit lower)
+__device__ __forceinline__ bool ilu_take(const Dev& d, const typename PubBits<W>::U* pub, int col, W& x) {
+  using U = typename PubBits<W>::U;
+  U v = ld_relaxed_bits(pub + col);
+  if (v != PubBits<W>::SENT) { x = *reinterpret_cast<W*>(&v); return true; }
+  const unsigned long long t0 = globaltimer();
+  for (int it = 0;; ++it) {
+    v = ld_relaxed_bits(pub + col);
+    if (v != PubBits<W>::SENT) { x = *reinterpret_cast<W*>(&v); return true; }
+    if ((it & 63) == 63) {
+      if (*(volatile int*)d.abort_flag) return false;
+      if ((long long)(globaltimer() - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); return false; }
+    }
+  }
+}
+
+template <class W, int T>
+__device__ __forceinline__ bool ilu_solve_sf(const Dev& d, Shm& sh, const W* rhs_src, W* out) {
+  using U = typename PubBits<W>::U;
+  const W* __restrict__ f = (const W*)d.iluW;
+  const int gt = sh.cta * NT + threadIdx.x, gs = d.G * NT, n = d.n;
+  U* pub = reinterpret_cast<U*>(d.ilu_pub[T]);
+  U* other = reinterpret_cast<U*>(d.ilu_pub[1 - T]);
+  for (int i = gt; i < n; i += gs) other[i] = PubBits<W>::SENT;  // re-arm the other solve's buffer
+  bool ok = true;
+  for (int s = gt; s < n && ok; s += gs) {
+    IluSlot<W> p;
+    ilu_load<W, T>(d, rhs_src, s, n, p);
+    // all inputs polled in one round (re-polling only those still unpublished)
+    W acc = __ldcg(rhs_src + p.r.row);
+    U v[ILU_KP];
+#pragma unroll
+    for (int k = 0; k < ILU_KP; ++k) v[k] = k < p.r.ne ? ld_relaxed_bits(pub + p.r.col[k]) : (U)0;
+    {
+      unsigned long long t0 = 0;
+      for (int it = 0;; ++it) {
+        bool pend = false;
+#pragma unroll
+        for (int k = 0; k < ILU_KP; ++k) pend |= v[k] == PubBits<W>::SENT;
+        if (!pend) break;
+#pragma unroll
+        for (int k = 0; k < ILU_KP; ++k)
+          if (v[k] == PubBits<W>::SENT) v[k] = ld_relaxed_bits(pub + p.r.col[k]);
+        if ((it & 63) == 63) {
+          const unsigned long long t = globaltimer();
+          if (t0 == 0) t0 = t;
+          if (*(volatile int*)d.abort_flag) { ok = false; break; }
+          if ((long long)(t - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); ok = false; break; }
+        }
+      }
+    }
+    W x[ILU_KP];
+#pragma unroll
+    for (int k = 0; k < ILU_KP; ++k) x[k] = *reinterpret_cast<const W*>(&v[k]);
+#pragma unroll
+    for (int k = 0; k < ILU_KP; ++k)
+      if (k < p.r.ne) acc = subw(acc, mulw(p.r.val[k], x[k]));
+    for (int k = ILU_KP; k < p.r.ne && ok; ++k) {
+      W xk;
+      ok = ilu_take<W>(d, pub, d.ilu_ecol[T][p.r.e0 + k], xk);
+      acc = subw(acc, mulw(f[d.ilu_eidx[T][p.r.e0 + k]], xk));
+    }
+    if (!ok) break;
+    const W res = T == 1 ? acc / p.r.diag : acc;
+    out[p.r.row] = res;
+    st_relaxed_bits(pub + p.r.row, *reinterpret_cast<const U*>(&res));
+  }
+  if (T == 1) fence_proxy_async_global();  // the next phase may stage the result with bulk copies
+  return grid_sync(d, sh) && ok;
+}
+
+// seq: this apply's index within the launch (unused by the value-publishing solves)
+template <class W>
+__device__ __noinline__ bool ilu_apply_phase(const Dev& d, Shm& sh, const W* in, W* out, unsigned seq) {
+  (void)seq;
+  if (!(d.tune & 65536)) {  // sync-free (default)
+    if (!ilu_solve_sf<W, 0>(d, sh, in, out)) return false;
+    return ilu_solve_sf<W, 1>(d, sh, out, out);
+  }
+  if (!ilu_solve<W, 0>(d, sh, in, out)) return false;  // L y = in (unit lower), level-synchronous
   return ilu_solve<W, 1>(d, sh, out, out);              // U out = y
 }
 
@@ -1835,6 +1948,8 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   };
 
   int k = 0, total_inner = 0, inner_len = 0, status = ST_OK, J1 = 0;
+  unsigned ilu_seq = 0;  // ILU applies so far (sync-free solve sequence numbers)
+  (void)ilu_seq;
   // (every rank reads its own flag: the cast overflow check is the same on all
   // ranks only if the caller built A32 on all of them; ranks agree on it via
   // the residual all-reduce below, which carries the error bits)
@@ -1881,7 +1996,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (k >= d.max_cycles) { status = ST_NOT_CONVERGED; break; }
     double RRp = RR;
     if constexpr (PC) {  // line 90 with M = LU (reading R24): r = U⁻¹L⁻¹ RN_W(z), then ‖r‖²
-      if (!ilu_apply_phase<W>(d, sh, wb0, wb0)) { status = ST_ETIMEOUT; break; }
+      if (!ilu_apply_phase<W>(d, sh, wb0, wb0, ilu_seq++)) { status = ST_ETIMEOUT; break; }
       double p = 0.0;
       for (int i = r0 + threadIdx.x; i < min(r1, d.n); i += NT) {
         const double v = (double)__ldcg(wb0 + i);
@@ -1912,7 +2027,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       const unsigned long long ts0 = d.profile && threadIdx.x == 0 ? globaltimer() : 0ull;
       spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V, j - 1);
       if constexpr (PC) {  // w = U⁻¹L⁻¹(A_W v_j) (line 100 with M = LU)
-        if (!grid_sync(d, sh) || !ilu_apply_phase<W>(d, sh, dst, dst)) { fail = true; break; }
+        if (!grid_sync(d, sh) || !ilu_apply_phase<W>(d, sh, dst, dst, ilu_seq++)) { fail = true; break; }
       }
       if (d.profile) {
         if (threadIdx.x == 0) d.prof_cta[cta] += globaltimer() - ts0;
@@ -2044,7 +2159,7 @@ __global__ void __launch_bounds__(NT, 1) k_spmv_kernel(Dev d, const W* v, W* w) 
 template <class W>
 __global__ void __launch_bounds__(NT, 1) k_ilu_apply_kernel(Dev d, const W* z, W* out) {
   G200_SMEM_CARVE(W)
-  ilu_apply_phase<W>(d, sh, z, out);
+  ilu_apply_phase<W>(d, sh, z, out, 0u);
 }
 
 template <class W, int L>

@@ -8,7 +8,7 @@ S = G.Solver.from_csr(P.A)
 b = torch.from_numpy(P.b).cuda()
 for ortho in (G.MGS, G.CGSR):
     for prec in (G.MIXED, G.FP64):
-        for tune in (0, 32768, 16384):
+        for tune in (0, 65536):
             x = torch.zeros_like(b)
             r = S.solve_device(b, x, m=50, ortho=ortho, precision=prec, precond=G.ILU0, max_cycles=1, delta=0.0,
                                tol=1e-30, tune=tune)
