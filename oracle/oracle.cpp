@@ -6,7 +6,7 @@
 // Plain single-threaded C++ following Alg. 1 in the paper's
 // order and notation, with the precision split of PAPER.md:285-289 ("computing
 // the residual and updating x in double-precision and computing everything else
-// in single-precision") and the readings of DESIGN.md §2 (R1–R14).  Compiled
+// in single-precision") and the readings of DESIGN.md §2 (R1–R24).  Compiled
 // -O2 -ffp-contract=off (every W operation rounds on its own), no fast-math.
 //
 // W is the working precision of Alg. 1 lines 89–146: float in mixed mode,
