@@ -45,8 +45,11 @@ template <class AT> __host__ __device__ constexpr int NSTG() { return sizeof(AT)
 template <class AT> __host__ __device__ constexpr int stage_bytes() { return ST_OFF_A + (CHUNK_CAP + 8) * (int)sizeof(AT); }
 constexpr int MAXSTG = 4;
 // block stream (short-row matrices): a ring of NBS per-CTA stages of BS_BYTES each
-constexpr int NBS = 3;
-constexpr int BS_BYTES = 57344;
+// (measured on C2, one solve each: 6 × 28 KB +23 %, 4 × 42 KB +6 %, 3 × 56 KB
+// baseline, 2 × 84 KB −7 % mixed MGS / −5 % CGSR, 2 × 96 KB −4 % (less L1):
+// the per-stage cost — refill hand-off, metadata, the first gathers — dominates)
+constexpr int NBS = 2;
+constexpr int BS_BYTES = 86016;
 constexpr int BS_MAXROW = 64;  // longest row the block stream takes (else the chunk stream)
 constexpr int TILE_BYTES = NGRP * 3 * (ST_OFF_A + (CHUNK_CAP + 8) * 8);  // 172032 (≥ the fp32 ring, 161792)
 constexpr int MAX_M = 256;                               // restart length limit (shared-memory bound)
