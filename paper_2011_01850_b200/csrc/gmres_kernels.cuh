@@ -46,7 +46,8 @@ template <class AT> __host__ __device__ constexpr int stage_bytes() { return ST_
 constexpr int MAXSTG = 4;
 // block stream (short-row matrices): a ring of NBS per-CTA stages of BS_BYTES each
 // (measured on C2, one solve each: 6 × 28 KB +23 %, 4 × 42 KB +6 %, 3 × 56 KB
-// baseline, 2 × 84 KB −7 % mixed MGS / −5 % CGSR, 2 × 96 KB −4 % (less L1):
+// baseline, 2 × 72 KB −5 %, 2 × 80 KB −6.5 %, 2 × 84 KB −7 % mixed MGS / −5 % CGSR,
+// 2 × 96 KB −4 % (less L1):
 // the per-stage cost — refill hand-off, metadata, the first gathers — dominates)
 constexpr int NBS = 2;
 constexpr int BS_BYTES = 86016;
