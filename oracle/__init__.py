@@ -37,22 +37,38 @@ class _Result(ctypes.Structure):
                 ("final_relres", ctypes.c_double)]
 
 
-def build(force: bool = False) -> str:
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+_use_omp = False
+
+
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile the oracle.  omp=True builds liboracle_omp.so (-fopenmp): the same
+    source with its element-parallel loops (ORACLE_PAR, oracle.cpp) spread over
+    threads and every reduction kept sequential — bitwise equal to the default
+    single-threaded build (tests/test_oracle.py)."""
+    out = _LIB_OMP if omp else _LIB
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+    if force or not os.path.exists(out) or os.path.getmtime(out) < newest:
         # -ffp-contract=off: every W operation rounds on its own (no FMA fusion);
         # SSE2 arithmetic on x86-64 (no x87 extended precision).
         cmd = ["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
-               "-std=c++17", "-o", _LIB, _SRC]
+               "-std=c++17"] + (["-fopenmp"] if omp else []) + ["-o", out, _SRC]
         subprocess.check_call(cmd)
-    return _LIB
+    return out
+
+
+def use_omp(flag: bool = True) -> None:
+    """Route every later call through the OpenMP build (full-size golden runs only)."""
+    global _use_omp, _lib
+    if flag != _use_omp:
+        _use_omp = flag
+        _lib = None
 
 
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_LIB)
+        L = ctypes.CDLL(build(omp=_use_omp))
         vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
         L.oracle_spmv64.argtypes = [i64, vp, vp, vp, vp, vp]; L.oracle_spmv64.restype = None
         L.oracle_spmv32.argtypes = [i64, vp, vp, vp, vp, vp]; L.oracle_spmv32.restype = None
@@ -314,3 +330,13 @@ def solve(A, b, x0=None, m=30, tol=1e-10, ortho=CGSR, prec=MIXED, delta=None, ma
                       inner[:min(res.inner_len, inner.size)].copy(), res.final_relres)
     out.orth = orth[:min(res.inner_len, orth.size)].copy() if policy == ORTHLOSS else None
     return out
+
+
+def backward_error(A, b, x):
+    """Normwise backward error ‖b − A x‖₂ / (‖A‖_F ‖x‖₂ + ‖b‖₂) (the paper's
+    stopping metric at PAPER.md:317, 431-433 is named but not defined — reading Q5/Q17).
+    Report only; the stop test is ‖b − Ax‖/‖b‖ (reading R5).  Pins: tests/test_oracle.py."""
+    z = np.asarray(b, np.float64) - spmv64(A, x)
+    na = float(np.sqrt(np.sum(np.asarray(A.val, np.float64) ** 2)))
+    den = na * float(np.linalg.norm(x)) + float(np.linalg.norm(b))
+    return float(np.linalg.norm(z) / den) if den > 0 else 0.0

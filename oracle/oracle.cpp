@@ -22,6 +22,21 @@
 #include <functional>
 #include <vector>
 
+// Optional OpenMP build (liboracle_omp.so, -fopenmp; BASELINE.md §4 / SURVEY.md
+// §8(c) "optional OpenMP build … results bitwise thread-count-invariant"):
+// ORACLE_PAR parallelises ONLY loops whose iterations write disjoint outputs and
+// contain no cross-iteration reduction (rows of an SpMV, elements of an axpy,
+// whole dot products in a set of independent dots).  Every reduction (dots,
+// norms, ‖z‖²) stays one sequential loop in index order, so each floating-point
+// operation and its operands are the same as in the single-threaded build and
+// the two builds agree bit for bit (tests/test_oracle.py::test_omp_build_bitwise).
+// Without -fopenmp the pragma is ignored: the default build is plain sequential C++.
+#ifdef _OPENMP
+#define ORACLE_PAR _Pragma("omp parallel for schedule(static)")
+#else
+#define ORACLE_PAR
+#endif
+
 namespace {
 
 // ---------------------------------------------------------------- helpers
@@ -45,6 +60,7 @@ double dot(int64_t n, const W* x, const W* y, bool acc32) {
 // Row sum in W in ascending column order, then the Jacobi scale in W.
 template <class W>
 void jacobi_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const W* a, const W* dinv, const W* v, W* w) {
+  ORACLE_PAR
   for (int64_t i = 0; i < n; ++i) {
     W acc = (W)0;
     for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
@@ -110,6 +126,7 @@ void mgs(int64_t n, int j, const W* V, int64_t ldv, W* w, double* h, bool acc32)
     const W* vi = V + (int64_t)i * ldv;
     double hij = dot<W>(n, w, vi, acc32);   // line 154
     W hw = rn<W>(hij);
+    ORACLE_PAR
     for (int64_t l = 0; l < n; ++l) {        // line 155
       W t = hw * vi[l];
       w[l] = w[l] - t;
@@ -126,8 +143,10 @@ void cgsr(int64_t n, int j, const W* V, int64_t ldv, W* w, double* h, int passes
   std::vector<W> cw(j);
   for (int i = 0; i < j; ++i) h[i] = 0.0;
   for (int p = 0; p < passes; ++p) {
+    ORACLE_PAR
     for (int i = 0; i < j; ++i) c[i] = dot<W>(n, V + (int64_t)i * ldv, w, acc32);  // line 161
     for (int i = 0; i < j; ++i) cw[i] = rn<W>(c[i]);
+    ORACLE_PAR
     for (int64_t l = 0; l < n; ++l) {                                                // line 162
       W acc = (W)0;
       for (int i = 0; i < j; ++i) {
@@ -147,6 +166,7 @@ void cgsr(int64_t n, int j, const W* V, int64_t ldv, W* w, double* h, int passes
 template <class W>
 void scale(int64_t n, const W* w, double inv, W* v) {
   const W iw = rn<W>(inv);
+  ORACLE_PAR
   for (int64_t l = 0; l < n; ++l) v[l] = w[l] * iw;
 }
 
@@ -167,6 +187,7 @@ int backsolve(int J, const double* R, int64_t ldr, const double* s, double* y) {
 // u_l = Σ_i (double)v_il · y_i in fp64, i ascending, then x_l ← x_l + u_l.
 template <class W>
 void xupdate(int64_t n, int J, const W* V, int64_t ldv, const double* y, double* x, bool update32) {
+  ORACLE_PAR
   for (int64_t l = 0; l < n; ++l) {
     double u = 0.0;
     for (int i = 0; i < J; ++i) u += (double)V[(int64_t)i * ldv + l] * y[i];
@@ -185,6 +206,7 @@ extern "C" {
 
 // ----------------------------------------------------------- components
 void oracle_spmv64(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, const double* x, double* y) {
+  ORACLE_PAR
   for (int64_t i = 0; i < n; ++i) {
     double s = 0.0;
     for (int64_t e = rp[i]; e < rp[i + 1]; ++e) s += a[e] * x[ci[e]];
@@ -193,6 +215,7 @@ void oracle_spmv64(int64_t n, const int32_t* rp, const int32_t* ci, const double
 }
 
 void oracle_spmv32(int64_t n, const int32_t* rp, const int32_t* ci, const float* a, const float* x, float* y) {
+  ORACLE_PAR
   for (int64_t i = 0; i < n; ++i) {
     float s = 0.0f;
     for (int64_t e = rp[i]; e < rp[i + 1]; ++e) s = s + a[e] * x[ci[e]];
@@ -422,6 +445,7 @@ int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* c
     const W* vj = V + (int64_t)(j - 1) * ldv;
     if (ilu) {  // line 100 with M = LU (reading R24): t = A_W v_j (row sums in W), w = U⁻¹L⁻¹t
       std::vector<W> t(n);
+      ORACLE_PAR
       for (int64_t i = 0; i < n; ++i) {
         W acc = 0;
         for (int64_t e = rp[i]; e < rp[i + 1]; ++e) acc = acc + aW[e] * vj[ci[e]];
@@ -449,6 +473,7 @@ int arnoldi(int ortho, int flags, int64_t n, const int32_t* rp, const int32_t* c
     bool orth = false;
     if (mon && !breakdown) {  // column j of U: v_i · v_{j+1}, i = 1..j (fp64 accumulation)
       const W* vn = V + (int64_t)j * ldv;
+      ORACLE_PAR
       for (int i = 0; i < j; ++i) ucol[i] = dot<W>(n, V + (int64_t)i * ldv, vn, false);
       const double sn = mon->append(j, ucol.data());
       if (mon_hist) mon_hist[j - 1] = sn;
@@ -494,6 +519,7 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
     if (mixed && std::fabs(a[e]) > (double)FLT_MAX) return ORACLE_EFP32RANGE;
     aW[e] = (W)a[e];
   }
+  ORACLE_PAR
   for (int64_t i = 0; i < n; ++i) dinvW[i] = (W)dinv64[i];
   // ILU(0) preconditioner (§8 f2, reading R24): factors in W from A_W, or in
   // fp32 from RN32(A64) inside the fp64 solver ("single-precision ILU")
@@ -538,6 +564,7 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
 
   const int64_t ldv = n;
   std::vector<W> V((size_t)n * (m + 1)), r(n);
+  std::vector<double> zrow(n), zuse_row(n);
   std::vector<double> Hbar((size_t)(m + 1) * m), R((size_t)(m + 1) * m), s(m + 1), y(m), ih(m);
   int k = 0, total_inner = 0, J1 = 0;
   const int stall_w = policy == ORACLE_POLICY_STALL ? std::max(1, (int)std::ceil(stall_frac * m)) : 0;
@@ -548,22 +575,29 @@ int solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* a, cons
   for (;;) {
     // line 86: z_k ← b − A x_k (fp64); line 90: r_k ← M⁻¹ z_k
     // in W after casting the residual (reading R10).
-    double zz = 0.0;
+    // rows (independent), then ‖z‖² and the error checks in row order
+    ORACLE_PAR
     for (int64_t i = 0; i < n; ++i) {
       double sacc = 0.0;
       for (int64_t e = rp[i]; e < rp[i + 1]; ++e) sacc += a[e] * x[ci[e]];
       double zi = b[i] - sacc;
-      if (!std::isfinite(zi)) return ORACLE_ENONFINITE;
-      zz += zi * zi;
+      zrow[i] = zi;
       double zuse = zi;
       if (resid32) {  // ablation: the same residual formed in fp32 arithmetic
         float s32 = 0.0f;
         for (int64_t e = rp[i]; e < rp[i + 1]; ++e) s32 = s32 + a32[e] * (float)x[ci[e]];
         zuse = (double)((float)b[i] - s32);
       }
-      if (mixed && std::fabs(zuse) > (double)FLT_MAX) return ORACLE_EFP32RANGE;
+      zuse_row[i] = zuse;
       if (pcp) rz[i] = (W)zuse;
       else r[i] = dinvW[i] * (W)zuse;
+    }
+    double zz = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double zi = zrow[i];
+      if (!std::isfinite(zi)) return ORACLE_ENONFINITE;
+      zz += zi * zi;
+      if (mixed && std::fabs(zuse_row[i]) > (double)FLT_MAX) return ORACLE_EFP32RANGE;
     }
     if (pcp) (*pcp)(rz.data(), r.data());  // line 90 with M = LU (reading R24)
     double znorm = std::sqrt(zz);

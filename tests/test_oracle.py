@@ -587,3 +587,106 @@ def test_ilu_gmres_converges_faster_than_jacobi(prec, flags, ortho):
     assert ri.final_relres <= 1e-10 and rj.final_relres <= 1e-10
     assert ri.inner_iters < rj.inner_iters
     assert np.linalg.norm(ri.x - P.x_true) <= 1e-8 * np.linalg.norm(P.x_true)
+
+
+# ------------------------------------------------------------------ a1 residual
+# Alg. 1 lines 86/90: z = b − A x in fp64, then
+# r = M⁻¹ RN_W(z) in W with M = diag(A) (readings R10, R11).  Pinned against a
+# library SpMV (scipy.sparse), elementwise, at x ≠ 0 on a matrix whose diagonal
+# varies row to row (so a missing or misplaced dinv, a sign error or a dropped
+# b would each fail), in both precisions.
+@pytest.mark.parametrize("prec", [O.FP64, O.MIXED])
+@pytest.mark.parametrize("kind", ["randdd", "ragged_stencil"])
+def test_resid_pinned_against_library_spmv(prec, kind):
+    sp = pytest.importorskip("scipy.sparse")
+    A = inputs.randdd(3001, 7) if kind == "randdd" else inputs.stencil(7, 9, (3.0, -2.0, 1.0))
+    n = A.n
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-1, 1, n)
+    b = rng.uniform(-1, 1, n) * np.abs(A.val).max()
+    M = sp.csr_matrix((A.val, A.col, A.row_ptr), shape=(n, n))
+    z_lib = b - M @ x
+    diag = M.diagonal()
+    assert np.ptp(diag) > 0 or kind == "ragged_stencil"
+    dW = (1.0 / diag).astype(np.float32 if prec == O.MIXED else np.float64)
+    rc, r, zz, rr = O.resid(prec, A, b, x, dW)
+    assert rc == 0
+    # z: componentwise γ-bound of an fp64 row sum in any order, |b_i| + (|A||x|)_i
+    k = np.diff(A.row_ptr) + 2
+    u = 2.0 ** -53
+    bound = k * u / (1 - k * u) * (np.abs(b) + abs(M) @ np.abs(x))
+    assert zz == pytest.approx(float(np.dot(z_lib, z_lib)), rel=1e-12)
+    # r_i = RN_W(dinv_i · RN_W(z_i)): the library z rounded through the same two W operations
+    if prec == O.MIXED:
+        r_lib = (dW * z_lib.astype(np.float32)).astype(np.float32)
+        # |z − z_lib| ≤ bound moves RN32(z) by at most one ulp; dinv·(·) adds one rounding
+        ulp = np.spacing(np.abs(r_lib).astype(np.float32)).astype(np.float64)
+        assert np.all(np.abs(r.astype(np.float64) - r_lib) <= 2 * ulp + 2 * np.abs(dW) * bound)
+    else:
+        r_lib = dW * z_lib
+        assert np.all(np.abs(r - r_lib) <= np.abs(dW) * bound + 2 * u * np.abs(r_lib))
+    assert rr == pytest.approx(float(np.dot(r.astype(np.float64), r.astype(np.float64))), rel=1e-12)
+    assert rr == pytest.approx(float(np.dot(r_lib.astype(np.float64), r_lib.astype(np.float64))),
+                               rel=1e-12 if prec == O.FP64 else 1e-6)
+    # special cases: x solving A x = b exactly (b = A x) → z ≈ 0; b = 0 → z = −A x
+    rc, _, zz0, _ = O.resid(prec, A, M @ x, x, dW)
+    assert rc == 0 and math.sqrt(zz0) <= 1e-13 * np.linalg.norm(M @ x)
+    rc, r1, zz1, _ = O.resid(O.FP64, A, np.zeros(n), x, np.ones(n))
+    assert np.allclose(r1, -(M @ x), rtol=1e-13, atol=1e-13 * np.abs(M @ x).max())
+
+
+def test_resid_error_codes():
+    A = inputs.stencil(5, 6, (1.0, 1.0, 0.0))
+    n = A.n
+    d = O.dinv(A)
+    x = np.zeros(n)
+    b = np.ones(n)
+    b[5] = 1e39          # |z_5| > FLT_MAX: the cast of the residual to fp32 overflows (reading R10)
+    assert O.resid(O.MIXED, A, b, x, d.astype(np.float32))[0] == -4
+    assert O.resid(O.FP64, A, b, x, d)[0] == 0
+    x[3] = np.inf        # non-finite residual
+    assert O.resid(O.FP64, A, np.ones(n), x, d)[0] == -5
+
+
+# ------------------------------------------------------------------ normwise backward error (Q5/Q17)
+def test_backward_error_properties():
+    D = random_dd(40, 3)
+    A = csr_from_dense(D)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(40)
+    xs = np.linalg.solve(D, b)
+    assert O.backward_error(A, b, xs) <= 1e-15          # exact solution → ~u
+    assert O.backward_error(A, b, np.zeros(40)) == pytest.approx(1.0)   # x = 0 → ‖b‖/‖b‖
+    x = xs + 1e-3 * rng.standard_normal(40)
+    e = O.backward_error(A, b, x)
+    # invariant under scaling the system (A, b) → (cA, cb)
+    A2 = inputs.CSR(A.row_ptr, A.col, 8.0 * A.val)
+    assert O.backward_error(A2, 8.0 * b, x) == pytest.approx(e, rel=1e-14)
+    # Rigal–Gaches: the smallest normwise perturbation ‖ΔA‖_F/‖A‖_F = ‖Δb‖/‖b‖ = η making x exact
+    # has η = e; check the explicit perturbation ΔA = η‖A‖_F r xᵀ/(‖r‖‖x‖), Δb = −η‖b‖ r/‖r‖
+    r = b - D @ x
+    na, nx, nb = np.linalg.norm(D), np.linalg.norm(x), np.linalg.norm(b)
+    dA = e * na * np.outer(r, x) / (np.linalg.norm(r) * nx)
+    db = -e * nb * r / np.linalg.norm(r)
+    assert np.linalg.norm((D + dA) @ x - (b + db)) <= 1e-12 * nb
+
+
+# ------------------------------------------------------------------ OpenMP oracle build
+def test_omp_build_bitwise():
+    """liboracle_omp.so (used for the full-size golden records) equals the
+    single-threaded build bit for bit: only element-parallel loops are threaded."""
+    P = inputs.make("C3", 12000)
+    Q = inputs.make("C2", 20)
+    try:
+        for prob in (P, Q):
+            for prec in (O.MIXED, O.FP64):
+                for ortho in (O.MGS, O.CGSR):
+                    O.use_omp(False)
+                    a = O.solve(prob.A, prob.b, m=prob.m, ortho=ortho, prec=prec)
+                    O.use_omp(True)
+                    c = O.solve(prob.A, prob.b, m=prob.m, ortho=ortho, prec=prec)
+                    assert (a.cycles, a.inner_iters) == (c.cycles, c.inner_iters)
+                    assert np.array_equal(a.x.view(np.uint64), c.x.view(np.uint64))
+                    assert np.array_equal(a.history, c.history) and np.array_equal(a.inner, c.inner)
+    finally:
+        O.use_omp(False)
