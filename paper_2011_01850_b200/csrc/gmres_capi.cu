@@ -15,7 +15,9 @@
 #include <vector>
 
 #include "../../include/gmres.h"
+#define G200_HOST_TU
 #include "gmres_kernels.cuh"
+#include "ktab.h"
 
 using namespace g200;
 
@@ -215,87 +217,25 @@ void set_vlayout(Dev& d, const VLayout& vl) {
   d.vbs = vl.bs;
 }
 
-template <class W, int L>
-void* solve_kernel_ptr() { return (void*)&solve_kernel<W, L, false>; }
-
+// kernel pointers (ktab.h: one translation unit per group, compiled in parallel)
 void* pick_solve(int prec, int L) {
-  if (prec == GMRES_MIXED) {
-    switch (L) {
-      case 1: return solve_kernel_ptr<float, 1>();
-      case 2: return solve_kernel_ptr<float, 2>();
-      case 4: return solve_kernel_ptr<float, 4>();
-      case 8: return solve_kernel_ptr<float, 8>();
-      case 16: return solve_kernel_ptr<float, 16>();
-      default: return solve_kernel_ptr<float, 32>();
-    }
-  }
-  switch (L) {
-    case 1: return solve_kernel_ptr<double, 1>();
-    case 2: return solve_kernel_ptr<double, 2>();
-    case 4: return solve_kernel_ptr<double, 4>();
-    case 8: return solve_kernel_ptr<double, 8>();
-    case 16: return solve_kernel_ptr<double, 16>();
-    default: return solve_kernel_ptr<double, 32>();
-  }
+  if (prec == GMRES_MIXED) return L <= 4 ? ktab_solve_f32_lo(L) : ktab_solve_f32_hi(L);
+  return L <= 4 ? ktab_solve_f64_lo(L) : ktab_solve_f64_hi(L);
 }
-
+void* pick_solve_ext(int prec, int variant, int L) {
+  return prec == GMRES_MIXED ? ktab_solve_f32_ext(variant, L) : ktab_solve_f64_ext(variant, L);
+}
 // orthogonality-monitor launches (restart policy 3): L ∈ {1, 4}
-void* pick_solve_monitor(int prec, int L) {
-  if (prec == GMRES_MIXED) return L == 1 ? (void*)&solve_kernel<float, 1, false, true> : (void*)&solve_kernel<float, 4, false, true>;
-  return L == 1 ? (void*)&solve_kernel<double, 1, false, true> : (void*)&solve_kernel<double, 4, false, true>;
-}
-
+void* pick_solve_monitor(int prec, int L) { return pick_solve_ext(prec, 1, L); }
 // chunk-ring MGS launches (d.mgs_resident == 2): L ∈ {1, 4}
-void* pick_solve_chunked(int prec, int L) {
-  if (prec == GMRES_MIXED)
-    return L == 1 ? (void*)&solve_kernel<float, 1, false, false, true> : (void*)&solve_kernel<float, 4, false, false, true>;
-  return L == 1 ? (void*)&solve_kernel<double, 1, false, false, true> : (void*)&solve_kernel<double, 4, false, false, true>;
-}
-
+void* pick_solve_chunked(int prec, int L) { return pick_solve_ext(prec, 2, L); }
 // ILU(0)-preconditioned launches (§8 f2): L ∈ {1, 4}
-void* pick_solve_ilu(int prec, int L) {
-  if (prec == GMRES_MIXED)
-    return L == 1 ? (void*)&solve_kernel<float, 1, false, false, false, true>
-                  : (void*)&solve_kernel<float, 4, false, false, false, true>;
-  return L == 1 ? (void*)&solve_kernel<double, 1, false, false, false, true>
-                : (void*)&solve_kernel<double, 4, false, false, false, true>;
-}
-
+void* pick_solve_ilu(int prec, int L) { return pick_solve_ext(prec, 3, L); }
 // virtual-rank launches (several row blocks on one device): L ∈ {1, 4}
-void* pick_solve_virtual(int prec, int L) {
-  if (prec == GMRES_MIXED) return L == 1 ? (void*)&solve_kernel<float, 1, true> : (void*)&solve_kernel<float, 4, true>;
-  return L == 1 ? (void*)&solve_kernel<double, 1, true> : (void*)&solve_kernel<double, 4, true>;
-}
-
-template <class W>
-void* pick_kernel_templ(int kind, int L) {
-  switch (kind) {
-    case 0:
-      switch (L) {
-        case 1: return (void*)&k_spmv_kernel<W, 1>;
-        case 2: return (void*)&k_spmv_kernel<W, 2>;
-        case 4: return (void*)&k_spmv_kernel<W, 4>;
-        case 8: return (void*)&k_spmv_kernel<W, 8>;
-        case 16: return (void*)&k_spmv_kernel<W, 16>;
-        default: return (void*)&k_spmv_kernel<W, 32>;
-      }
-    case 1:
-      switch (L) {
-        case 1: return (void*)&k_resid_kernel<W, 1>;
-        case 2: return (void*)&k_resid_kernel<W, 2>;
-        case 4: return (void*)&k_resid_kernel<W, 4>;
-        case 8: return (void*)&k_resid_kernel<W, 8>;
-        case 16: return (void*)&k_resid_kernel<W, 16>;
-        default: return (void*)&k_resid_kernel<W, 32>;
-      }
-    case 2: return (void*)&k_ortho_kernel<W>;
-    case 4: return (void*)&k_ilu_apply_kernel<W>;
-    default: return (void*)&k_xupdate_kernel<W>;
-  }
-}
+void* pick_solve_virtual(int prec, int L) { return pick_solve_ext(prec, 4, L); }
 
 void* pick_kernel(int prec, int kind, int L) {
-  return prec == GMRES_MIXED ? pick_kernel_templ<float>(kind, L) : pick_kernel_templ<double>(kind, L);
+  return prec == GMRES_MIXED ? ktab_comp_f32(kind, L) : ktab_comp_f64(kind, L);
 }
 
 // stride of the per-CTA partial sums: m+1 Gram-Schmidt coefficients, and at
@@ -758,6 +698,7 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.kmax = kmax_for(m);
   d.ortho = ortho;
   d.tile_bytes = tile_bytes_for(m);
+  set_smem_offsets(d);
   d.rp = ctx->d_rp;
   d.ci = ctx->d_ci;
   d.a64 = ctx->d_a64;
@@ -1069,12 +1010,24 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
     const int nq = ctx->part_max_rows / per_vec;
     const int buf_bytes = ((nq + 7) & ~7) * 16;
     const int tune = opts ? opts->tune : 0;
+    // a candidate staging size fits when dynamic + the kernel's static shared memory stay within the
+    // per-block opt-in limit and the grid stays co-resident; a failed probe leaves no latched error
     auto fits = [&](const void* k, int tb) {
+      cudaFuncAttributes fa{};
+      if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return false; }
+      int optin = 0;
+      if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      if (smem_bytes(m, tb) + fa.sharedSizeBytes > (size_t)optin) return false;
       int G2 = 0;
-      return smem_bytes(m, tb) <= kMaxDynSmem &&
-             grid_for(ctx, k, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 >= G;
+      const bool ok = grid_for(ctx, k, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 >= G;
+      if (!ok) { cudaGetLastError(); ctx->err.clear(); }
+      return ok;
     };
-    for (int nb = (tune & 256) ? 2 : 3; nb >= 2 && nq <= MGS_MV * NT && !(tune & (4 | 8192)) && !mgs_resident; --nb) {
+    const bool force_stream = (tune & 524288) != 0;  // dev/test: the streamed MGS even where w fits on chip
+    for (int nb = (tune & 256) ? 2 : 3; nb >= 2 && nq <= MGS_MV * NT && !(tune & (4 | 8192)) && !force_stream && !mgs_resident; --nb) {
       const int tb = std::max(tile_bytes, nb * buf_bytes);
       if (fits(kern, tb)) {
         mgs_resident = 1;
@@ -1082,7 +1035,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
         tile_bytes = tb;
       }
     }
-    if (!mgs_resident && !(tune & 4) && !virt && policy != 3 && !ilu && (L == 1 || L == 4)) {  // the chunk-ring kernels
+    if (!mgs_resident && !(tune & 4) && !force_stream && !virt && policy != 3 && !ilu && (L == 1 || L == 4)) {  // the chunk-ring kernels
       const int nch = (nq + NT - 1) / NT;
       const int wsm = std::max(0, nch - MGS_MV);
       const int ns = std::min<int>(MGS_MAXSLOT, tile_bytes_for(m) / MGS_CHUNK - wsm);
@@ -1090,6 +1043,23 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
       if (ns >= nch && fits(pick_solve_chunked(precision, L), tb)) {
         kern = pick_solve_chunked(precision, L);
         mgs_resident = 2;
+        mgs_nbuf = ns;
+        mgs_wsm = wsm;
+        tile_bytes = tb;
+      }
+    }
+    // streamed MGS (w off chip: C4-sized row blocks): a ring of NS chunk slots and
+    // as many w chunks in shared memory as the rest of the staging region holds
+    if (!mgs_resident && !(tune & (4 | 16384)) && !virt && policy != 3 && !ilu && (L == 1 || L == 4)) {
+      const int nch = (nq + NT - 1) / NT;
+      const int slots = tile_bytes_for(m) / MGS_CHUNK;            // chunk-sized pieces of the staging region
+      const int ns = std::min(MGS_STREAM_SLOTS, slots / MGS_IC);  // item slots of the ring
+      int wsm = std::max(0, std::min(force_stream ? MGS_IC : slots - ns * MGS_IC, nch));
+      wsm -= wsm % MGS_IC;                                        // whole items of shared w
+      const int tb = std::max(tile_bytes, ns * MGS_ITEM + wsm * MGS_CHUNK);
+      if ((nch > MGS_MV || force_stream) && ns >= 2 && fits(pick_solve_chunked(precision, L), tb)) {
+        kern = pick_solve_chunked(precision, L);
+        mgs_resident = 3;
         mgs_nbuf = ns;
         mgs_wsm = wsm;
         tile_bytes = tb;
@@ -1144,6 +1114,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   d.inner_cap = inner_cap_dev;
   d.profile = (opts && opts->profile) ? 1 : 0;
   d.tile_bytes = tile_bytes;
+  set_smem_offsets(d);
   d.mgs_resident = mgs_resident;
   d.mgs_nbuf = mgs_nbuf;
   d.mgs_wsm = mgs_wsm;
@@ -1738,7 +1709,7 @@ int gmres_k_micro(gmres_ctx* ctx, int32_t precision, int32_t what, int32_t iters
   size_t smem;
   int m;
   if (int rc = comp_setup(ctx, precision, std::max(ncols, 1), 2, L, &kern0, &G, &smem, &m)) return rc;
-  const void* kern = precision == GMRES_MIXED ? (const void*)&k_micro_kernel<float> : (const void*)&k_micro_kernel<double>;
+  const void* kern = pick_kernel(precision, 5, 1);
   int Gk = 0;
   if (int rc = grid_for(ctx, kern, smem, 0, &Gk)) return rc;
   if (Gk < G) return fail(ctx, GMRES_ECUDA, "micro kernel occupancy below the solve grid");

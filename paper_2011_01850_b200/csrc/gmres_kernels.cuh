@@ -69,6 +69,9 @@ struct Dev {
   int kmax;         // m + 1 (stride of the partial buffers)
   int ortho;        // 0 MGS, 1 CGSR
   int tile_bytes;   // shared bytes reserved for the staging region
+  int soff[11];     // SmemLayout(kmax, tile_bytes) offsets (host-computed: each shared array is one
+                    // add from the dynamic-smem base, cheap to rematerialise — solve_kernel keeps no
+                    // shared pointers live in registers)
   const int* rp;
   const int* ci;
   const double* a64;
@@ -222,6 +225,19 @@ __device__ __forceinline__ double dotv(const float4& a, const float4& b) {
 }
 __device__ __forceinline__ double dotv(const double2& a, const double2& b) { return a.x * b.x + a.y * b.y; }
 
+// a ← RN_W(a − RN_W(h·b)) element-wise on a 16-byte vector (MGS line 155); named
+// members, no pointer casts, so the vectors stay in registers
+__device__ __forceinline__ void sub_scaled(float4& a, const float4& b, float h) {
+  a.x = __fsub_rn(a.x, __fmul_rn(h, b.x));
+  a.y = __fsub_rn(a.y, __fmul_rn(h, b.y));
+  a.z = __fsub_rn(a.z, __fmul_rn(h, b.z));
+  a.w = __fsub_rn(a.w, __fmul_rn(h, b.w));
+}
+__device__ __forceinline__ void sub_scaled(double2& a, const double2& b, double h) {
+  a.x = __dsub_rn(a.x, __dmul_rn(h, b.x));
+  a.y = __dsub_rn(a.y, __dmul_rn(h, b.y));
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
@@ -240,9 +256,56 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                                 unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_normal() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// plain arrival (no transaction bytes) on a shared mbarrier
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 16-byte global store with an L2 eviction-priority policy
+__device__ __forceinline__ void st_hint(float4* p, const float4& v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(double2* p, const double2& v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 // bulk prefetch of [src, src+bytes) into L2 (bytes multiple of 16)
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// non-blocking probe of a phase (test_wait: never suspends the thread)
+__device__ __forceinline__ bool mbar_test_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
   unsigned ok;
@@ -258,6 +321,7 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned 
 struct Shm {
   unsigned long long mbar[NGRP][MAXSTG];  // TMA stage barriers (per CSR-stream group)
   unsigned long long mbar_v[32];     // TMA barriers of the resident MGS's ring (≤ MGS_MAXSLOT)
+  unsigned long long mbar_e[32];     // streamed MGS: slot-consumed barriers (one arrival per warp)
   unsigned long long mbar_t[3];      // TMA barriers of the row-tile passes' V tiles
   unsigned long long mbar_b[NBS];    // TMA barriers of the block stream's stages
   int bcnt[NBS];                     // warps done with a block-stream stage
@@ -273,6 +337,7 @@ struct Shm {
   int red_epoch;                     // all-reduces done (partial buffer parity; thread 0 writes)
   double red[NW * 8];
   double red2[NW * 4];
+  unsigned long long pmin, pmax;     // profile mode: all-reduce arrival spread (ar_probe)
 };
 
 // wait for stage s of group grp's TMA pipeline; watchdog on %globaltimer
@@ -307,6 +372,7 @@ __device__ __forceinline__ void init_shm(Shm& sh, int cta) {
       for (int t = 0; t < MAXSTG; ++t) mbar_init(&sh.mbar[g][t], 1);
     }
     for (int b = 0; b < 32; ++b) mbar_init(&sh.mbar_v[b], 1);
+    for (int b = 0; b < 32; ++b) mbar_init(&sh.mbar_e[b], NW);
     for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_t[b], 1);
     sh.tphase = 0;
     for (int b = 0; b < NBS; ++b) { mbar_init(&sh.mbar_b[b], 1); sh.bcnt[b] = 0; }
@@ -410,6 +476,20 @@ __device__ __forceinline__ void block_sum(double (&v)[K], Shm& sh, double* out) 
   __syncthreads();
 }
 
+// profile mode, CTA 0: spread of the CTAs' arrival times at this all-reduce
+// (each CTA stored its %globaltimer next to its partial) → sh.pmin / sh.pmax
+static __device__ __noinline__ void ar_probe(const Dev& d, Shm& sh, int buf) {
+  unsigned long long tmin = ~0ull, tmax = 0ull;
+  for (int g = threadIdx.x; g < d.GG; g += NT) {
+    const unsigned long long t = (unsigned long long)__double_as_longlong(__ldcg(slot_row(d, d.slots, buf, g) + 1));
+    tmin = min(tmin, t);
+    tmax = max(tmax, t);
+  }
+  if (threadIdx.x == 0) { sh.pmin = ~0ull; sh.pmax = 0ull; }
+  __syncthreads();
+  if (tmax) { atomicMin(&sh.pmin, tmin); atomicMax(&sh.pmax, tmax); }
+}
+
 // One-value all-reduce of a per-thread contribution: CTA sum (warp trees,
 // warps in order) → push → arrive/wait → fixed-order sum over all GG CTAs.
 // (acq is implied: the counter acquire orders every later read.)
@@ -432,6 +512,7 @@ __device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool
     if (lane == 0) {
       const int gc = d.cta0 + sh.cta;
       for (int q = 0; q < d.nranks; ++q) slot_row(d, d.slot_peer[q], buf, gc)[0] = s;
+      if (d.profile) slot_row(d, d.slot_peer[0], buf, gc)[1] = __longlong_as_double((long long)globaltimer());
     }
     const bool ok = arrive_wait(d, sh);  // (the partial store precedes lane 0's release)
     if (lane == 0) {
@@ -447,10 +528,16 @@ __device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool
     x = warp_sum(x);
     if (lane == 0) sh.red2[warp] = x;
   }
+  if (d.profile && sh.cta == 0) ar_probe(d, sh, buf);
   __syncthreads();
   double s = 0.0;
   for (int w = 0; w < nwp; ++w) s += sh.red2[w];
   out = s;
+  if (d.profile && sh.cta == 0 && threadIdx.x == 0) {  // prof[11] Σ arrival spread, [12] Σ last arrival → result, [13] count
+    d.prof[11] += sh.pmax - sh.pmin;
+    d.prof[12] += globaltimer() - sh.pmax;
+    d.prof[13] += 1ull;
+  }
   return sh.abort == 0;
 }
 
@@ -1252,11 +1339,8 @@ __device__ __noinline__ double mgs_sweep(int r0, int r1, W* __restrict__ w, cons
     for (int u = 0; u < UB; ++u) {
       const int q = qb + u * NT;
       if (q < q1) {
-        W* pa = reinterpret_cast<W*>(&a[u]);
         if (vprev) {
-          const W* pb = reinterpret_cast<const W*>(&b[u]);
-#pragma unroll
-          for (int t = 0; t < N; ++t) pa[t] = subw(pa[t], mulw(hprev, pb[t]));
+          sub_scaled(a[u], b[u], hprev);
           reinterpret_cast<V4*>(w)[q] = a[u];
         }
         if (vnext) {
@@ -1482,7 +1566,7 @@ __device__ __forceinline__ double hess_step(int j, double* h, double* cs, double
 // ------------------------------------------------------------------ a7
 // Back-substitution R y = s_{1..J} (Alg. 1), column-oriented over the
 // CTA; R (ld = ldr) read from global, s copied into s_rhs.
-__device__ void backsolve_cta(int J, const double* R, int ldr, const double* s, double* s_rhs, double* y_out,
+__device__ inline void backsolve_cta(int J, const double* R, int ldr, const double* s, double* s_rhs, double* y_out,
                               double* s_y) {
   for (int k = threadIdx.x; k < J; k += NT) s_rhs[k] = s[k];
   __syncthreads();
@@ -1519,6 +1603,13 @@ struct SmemLayout {
     total = o;
   }
 };
+
+__host__ inline void set_smem_offsets(Dev& d) {
+  const SmemLayout lay(d.kmax, d.tile_bytes);
+  const size_t o[11] = {lay.off_part, lay.off_out, lay.off_tmp, lay.off_h, lay.off_cs, lay.off_sn,
+                        lay.off_s, lay.off_y, lay.off_rhs, lay.off_coef, lay.off_tiles};
+  for (int i = 0; i < 11; ++i) d.soff[i] = (int)o[i];
+}
 
 #define CTA_INDEX ((int)blockIdx.x)
 #define G200_SMEM_CARVE(W)                                                  \
@@ -1609,13 +1700,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     for (int k = 0; k < MGS_MV; ++k) {
       const int t = threadIdx.x + k * NT;
       if (t < nq) {
-        if (i > 1) {
-          const V4 y = Y[t];
-          W* pa = reinterpret_cast<W*>(&wr[k]);
-          const W* pb = reinterpret_cast<const W*>(&y);
-#pragma unroll
-          for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hprev, pb[u]));
-        }
+        if (i > 1) sub_scaled(wr[k], Y[t], hprev);
         acc += dotv(wr[k], X[t]);
       }
     }
@@ -1638,11 +1723,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     for (int k = 0; k < MGS_MV; ++k) {
       const int t = threadIdx.x + k * NT;
       if (t < nq) {
-        const V4 x = X[t];
-        W* pa = reinterpret_cast<W*>(&wr[k]);
-        const W* pb = reinterpret_cast<const W*>(&x);
-#pragma unroll
-        for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hprev, pb[u]));
+        sub_scaled(wr[k], X[t], hprev);
         nn += dotv(wr[k], wr[k]);
         wg[t] = wr[k];
       }
@@ -1670,6 +1751,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
 // the unfused update costs a pass and a barrier per step, mgs_resident.)
 constexpr int MGS_CHUNK = NT * 16;    // bytes of one ring slot = one vector of every thread
 constexpr int MGS_MAXSLOT = 32;       // ring slots (barriers in Shm)
+constexpr int MGS_STREAM_SLOTS = 4;   // item slots of the streamed MGS (mgs_stream): 4 × 32 KB of operands in flight
 template <class W>
 __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
                                              W* w, double* s_h, char* s_tiles, double& NN) {
@@ -1750,12 +1832,7 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
     issued = max(issued, min(gend, gi + NS));
     if (threadIdx.x == 0) s_h[i - 1] = h;
     const W hw = RN<W>(h);
-    auto upd = [&](V4& a, const V4& x) {
-      W* pa = reinterpret_cast<W*>(&a);
-      const W* pb = reinterpret_cast<const W*>(&x);
-#pragma unroll
-      for (int u = 0; u < N; ++u) pa[u] = subw(pa[u], mulw(hw, pb[u]));
-    };
+    auto upd = [&](V4& a, const V4& x) { sub_scaled(a, x, hw); };
 #pragma unroll
     for (int k = 0; k < MGS_MV; ++k)
       if (threadIdx.x + k * NT < nq) upd(wr[k], *slot(k));
@@ -1782,6 +1859,205 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
     const V4 a = ws[t];
     nn += dotv(a, a);
     wo[t] = a;
+  }
+  if (threadIdx.x == 0) sh.vg = gend;  // read by every thread at entry, before the syncs below
+  NN = nn;  // this thread's share of ‖w‖²; the caller pushes the halo and all-reduces it
+  return true;
+}
+
+// ------------------------------------------------------------------ a3 (streamed, w off chip)
+// MGS for row blocks whose w does not fit on chip (C4: 113 k
+// rows per CTA).  Chunk k of the CTA's rows = the 16-byte vector k·NT + t of
+// every thread t (MGS_CHUNK bytes); an item = MGS_IC consecutive chunks of one
+// basis vector, one bulk copy (single-thread bulk copies below ~16 KB are paced
+// at ~0.4 µs each, tools/tma_bench.cu r02).  w: the first d.mgs_wsm chunks in
+// shared memory (after the ring), the rest in global memory (the w buffer
+// itself: thread t alone reads and writes its vectors, so plain loads —
+// prefetched one item ahead — and evict_last stores keep it in L2 with no
+// cross-proxy ordering; w in registers spilled).  Step i = 1..j in two passes:
+//   A: the partial of h_i = w·v_i (line 154), all-reduce;
+//   B: w ← RN_W(w − RN_W(h_i)·v_i) (line 155), and at i = j the partial of ‖w‖²
+//      (line 104).
+// v_i streams through a ring of NS = d.mgs_nbuf item slots by TMA twice — from
+// HBM in A (evict_normal), from L2 in B right after the reduction (evict_first:
+// its last use).  (Measured on C4, r02: a fused update-then-dot pass re-reads
+// v_{i−1} a whole step later and misses in L2 — 20 % hit rate, 1.3× slower.)
+// One kernel-lifetime item sequence (sh.vg; per step: A's items, then B's),
+// slot = item mod NS, full barrier mbar_v (transaction bytes), consumed barrier
+// mbar_e (one arrival per warp).  Thread 0 issues items up to NS ahead of its
+// own consumption, after the consumed barrier of the slot's previous item; in
+// the all-reduce (A's items all consumed) it fills the ring with B's items.
+// Same operations and order per element and per thread partial as mgs_sweep /
+// mgs_resident (bit-identical solves).
+constexpr int MGS_IC = 4;                       // chunks per streamed item (32 KB)
+constexpr int MGS_ITEM = MGS_IC * MGS_CHUNK;
+__device__ __forceinline__ float4 ld_hint(const float4* p, unsigned long long pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_hint(const double2* p, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+template <class W>
+__device__ __forceinline__ bool mgs_stream(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
+                                           W* w, double* s_h, char* s_tiles, double& NN) {
+  using V4 = typename VecT<W>::T;
+  constexpr int N = VecT<W>::N;
+  const int lane = threadIdx.x & 31;
+  const int q0 = r0 / N, nq = r1 / N - q0;
+  const int nch = (nq + NT - 1) / NT;
+  const int nit = (nch + MGS_IC - 1) / MGS_IC;  // items per pass
+  const unsigned NS = (unsigned)d.mgs_nbuf;
+  const int MG = min(nch, d.mgs_wsm);           // first global w chunk (a multiple of MGS_IC)
+  V4* sv = reinterpret_cast<V4*>(s_tiles);
+  V4* ws = sv + (size_t)NS * MGS_IC * NT;       // shared w chunk k < MG at ws + k·NT
+  V4* wg = reinterpret_cast<V4*>(w) + q0;       // w chunk k at wg + k·NT
+  const unsigned g0 = sh.vg;
+  const unsigned gend = g0 + 2u * (unsigned)j * (unsigned)nit;
+  const unsigned long long pol_last = policy_evict_last();
+  const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
+  // ---- producer (thread 0): cursor over (step ci, pass cp: 0 A / 1 B, item ck)
+  unsigned issued = g0;
+  int ci = 1, cp = 0, ck = 0;
+  unsigned long long pol_first = 0, pol_norm = 0;
+  if (threadIdx.x == 0) {
+    pol_first = policy_evict_first();
+    pol_norm = policy_evict_normal();
+  }
+  auto wait_bar = [&](unsigned long long* bar, unsigned par) -> bool {
+    if (mbar_try_wait(bar, par)) return true;
+    const unsigned long long t0 = globaltimer();
+    for (;;) {
+      if (mbar_try_wait(bar, par)) return true;
+      if ((long long)(globaltimer() - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); return false; }
+    }
+  };
+  auto pump = [&](unsigned limit) {  // thread 0
+    const unsigned long long tp0 = lead ? globaltimer() : 0ull;
+    for (; issued < gend && issued < limit; ++issued) {
+      const unsigned s = issued % NS;
+      if (issued >= NS && !wait_bar(&sh.mbar_e[s], ((issued / NS) - 1u) & 1u)) return;
+      const unsigned bytes = (unsigned)min(MGS_IC * NT, nq - ck * MGS_IC * NT) * 16u;
+      const V4* src = reinterpret_cast<const V4*>(V + (long long)(ci - 1) * ldv + r0) + (size_t)ck * MGS_IC * NT;
+      mbar_expect_tx(&sh.mbar_v[s], bytes);
+      tma_load_1d_hint(sv + (size_t)s * MGS_IC * NT, src, bytes, &sh.mbar_v[s], cp ? pol_first : pol_norm);
+      if (++ck == nit) {
+        ck = 0;
+        if (++cp == 2) { cp = 0; ++ci; }
+      }
+    }
+    if (lead) d.prof[11] += globaltimer() - tp0;  // profile: producer time
+  };
+  // ---- consumers (every thread; thread t owns vector t of every chunk)
+  unsigned g = g0;  // next item to consume
+  // the next item: wait for its bytes, return this thread's vectors in the slot (chunk c at [c·NT])
+  auto acquire = [&]() -> const V4* {
+    if (threadIdx.x == 0) pump(g + NS);
+    const unsigned e = g;
+    const unsigned long long tw0 = lead ? globaltimer() : 0ull;
+    wait_bar(&sh.mbar_v[e % NS], (e / NS) & 1u);
+    if (lead) d.prof[12] += globaltimer() - tw0;  // profile: waiting for ring data
+    return sv + (size_t)(e % NS) * MGS_IC * NT + threadIdx.x;
+  };
+  auto release = [&]() {  // this warp is done with the item's slot
+    const unsigned e = g++;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.mbar_e[e % NS]);
+  };
+  if (threadIdx.x == 0) pump(g0 + NS);
+  for (int k = 0; k < MG; ++k) {
+    const int t = threadIdx.x + k * NT;
+    if (t < nq) ws[t] = wg[t];
+  }
+  double nn = 0.0;
+  for (int i = 1; i <= j; ++i) {
+    // ---- pass A: h_i = w·v_i
+    double acc = 0.0;
+    {
+      V4 pf[MGS_IC];  // global w: the next item's vectors in flight
+      auto prefetch = [&](int it) {
+#pragma unroll
+        for (int c = 0; c < MGS_IC; ++c) {
+          const int t = (it * MGS_IC + c) * NT + threadIdx.x;
+          if (it < nit && it * MGS_IC >= MG && t < nq) pf[c] = ld_hint(wg + t, pol_last);
+        }
+      };
+      prefetch(MG / MGS_IC);
+      for (int it = 0; it < nit; ++it) {
+        V4 wv[MGS_IC];
+        const bool glob = it * MGS_IC >= MG;
+        if (glob) {
+#pragma unroll
+          for (int c = 0; c < MGS_IC; ++c) wv[c] = pf[c];
+          prefetch(it + 1);
+        } else {
+#pragma unroll
+          for (int c = 0; c < MGS_IC; ++c)
+            if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) wv[c] = ws[(it * MGS_IC + c) * NT + threadIdx.x];
+        }
+        const V4* x = acquire();
+#pragma unroll
+        for (int c = 0; c < MGS_IC; ++c)
+          if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) acc += dotv(wv[c], x[c * NT]);
+        release();
+      }
+    }
+    double h;
+    auto mid = [&]() {
+      if (threadIdx.x == 0) pump(g + NS);  // A's items are all consumed: fill the ring with B's
+    };
+    const unsigned long long ta0 = lead ? globaltimer() : 0ull;
+    if (!allreduce1(d, sh, acc, false, h, mid)) return false;
+    if (lead) d.prof[13] += globaltimer() - ta0;  // profile: all-reduce (incl. the refill)
+    if (threadIdx.x == 0) s_h[i - 1] = h;
+    const W hw = RN<W>(h);
+    // ---- pass B: w ← w − h_i v_i (and ‖w‖² after the last step)
+    {
+      const bool last = i == j;
+      V4 pf[MGS_IC];
+      auto prefetch = [&](int it) {
+#pragma unroll
+        for (int c = 0; c < MGS_IC; ++c) {
+          const int t = (it * MGS_IC + c) * NT + threadIdx.x;
+          if (it < nit && it * MGS_IC >= MG && t < nq) pf[c] = ld_hint(wg + t, pol_last);
+        }
+      };
+      prefetch(MG / MGS_IC);
+      for (int it = 0; it < nit; ++it) {
+        V4 wv[MGS_IC];
+        const bool glob = it * MGS_IC >= MG;
+        if (glob) {
+#pragma unroll
+          for (int c = 0; c < MGS_IC; ++c) wv[c] = pf[c];
+          prefetch(it + 1);
+        } else {
+#pragma unroll
+          for (int c = 0; c < MGS_IC; ++c)
+            if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) wv[c] = ws[(it * MGS_IC + c) * NT + threadIdx.x];
+        }
+        const V4* x = acquire();
+#pragma unroll
+        for (int c = 0; c < MGS_IC; ++c) {
+          const int t = (it * MGS_IC + c) * NT + threadIdx.x;
+          if (t < nq) {
+            sub_scaled(wv[c], x[c * NT], hw);
+            if (last) nn += dotv(wv[c], wv[c]);
+            if (glob) st_hint(wg + t, wv[c], pol_last);
+            else ws[t] = wv[c];
+          }
+        }
+        release();
+      }
+    }
+  }
+  // shared chunks of w back to global for the next SpMV (global chunks were stored in the last pass)
+  for (int k = 0; k < MG; ++k) {
+    const int t = threadIdx.x + k * NT;
+    if (t < nq) wg[t] = ws[t];
   }
   if (threadIdx.x == 0) sh.vg = gend;  // read by every thread at entry, before the syncs below
   NN = nn;  // this thread's share of ‖w‖²; the caller pushes the halo and all-reduces it
@@ -1829,7 +2105,11 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   if constexpr (CH) {
     if (d.ortho == 0) {
       double nn = 0.0;
-      if (!mgs_chunked<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
+      if (d.mgs_resident == 3) {
+        if (!mgs_stream<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
+      } else if (!mgs_chunked<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) {
+        return false;
+      }
       return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
     }
   } else if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4)) {
@@ -1932,11 +2212,20 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   // (VR = false: a static index keeps every field of d a constant-bank operand)
   const int vr = VR ? (int)blockIdx.x / ds.G : 0;
   const Dev& d = ds.d[VR ? vr : 0];
-#undef CTA_INDEX
-#define CTA_INDEX ((int)blockIdx.x - vr * ds.G)
-  G200_SMEM_CARVE(W)
-#undef CTA_INDEX
-#define CTA_INDEX ((int)blockIdx.x)
+  extern __shared__ __align__(128) char dsm[];
+  __shared__ Shm sh;
+  double* const s_part = reinterpret_cast<double*>(dsm + d.soff[0]);
+  double* const s_out = reinterpret_cast<double*>(dsm + d.soff[1]);
+  double* const s_tmp = reinterpret_cast<double*>(dsm + d.soff[2]);
+  double* const s_h = reinterpret_cast<double*>(dsm + d.soff[3]);
+  double* const s_cs = reinterpret_cast<double*>(dsm + d.soff[4]);
+  double* const s_sn = reinterpret_cast<double*>(dsm + d.soff[5]);
+  double* const s_s = reinterpret_cast<double*>(dsm + d.soff[6]);
+  double* const s_y = reinterpret_cast<double*>(dsm + d.soff[7]);
+  double* const s_rhs = reinterpret_cast<double*>(dsm + d.soff[8]);
+  W* const s_coefW = reinterpret_cast<W*>(dsm + d.soff[9]);
+  char* const s_tiles = dsm + d.soff[10];
+  init_shm(sh, (int)blockIdx.x - vr * ds.G);
   const int cta = sh.cta;
   if (threadIdx.x == 0) { sh.epoch = d.epoch0; sh.red_epoch = d.red0; }
   __syncthreads();
@@ -2096,6 +2385,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   }
 }
 
+#ifdef G200_HOST_TU  // non-template kernels: defined once, in gmres_capi.cu
 // ------------------------------------------------------ setup kernels
 // a0: A32 = RN32(A64), overflow flagged.
 __global__ void cast32_kernel(const double* __restrict__ a, float* __restrict__ o, long long cnt, int* err) {
@@ -2105,6 +2395,8 @@ __global__ void cast32_kernel(const double* __restrict__ a, float* __restrict__ 
     o[e] = __double2float_rn(v);
   }
 }
+
+#endif
 
 // column-major V (ncols columns, leading dimension ldv, rows ≥ nvalid read
 // as 0) → row-blocked layout (Dev::vtb); component entry points only
@@ -2132,6 +2424,7 @@ __global__ void unpack_basis_kernel(const W* __restrict__ V, long long ldv, int 
   }
 }
 
+#ifdef G200_HOST_TU
 // Jacobi M = diag(A) (reading R11): dinv64 = 1/a_ii (fp64), dinv32 = RN32(dinv64).
 __global__ void dinv_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                             const double* __restrict__ a, double* dinv64, float* dinv32, int* bad_row,
@@ -2151,6 +2444,7 @@ __global__ void dinv_kernel(int n, const int* __restrict__ rp, const int* __rest
     }
   }
 }
+#endif
 
 // ------------------------------------------------- component kernels
 // Each runs the same device functions as solve_kernel for one step.
@@ -2251,6 +2545,7 @@ __global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int ite
   if (acc == 12345.678) out_ns[1] = 1;  // keep the work alive
 }
 
+#ifdef G200_HOST_TU
 // a6 + a7 on a given unrotated Hessenberg (tests): one CTA.
 __global__ void __launch_bounds__(NT, 1) k_hess_kernel(int m, int J, const double* Hbar, double beta, double* R,
                                                      double* s, double* y) {
@@ -2274,5 +2569,6 @@ __global__ void __launch_bounds__(NT, 1) k_hess_kernel(int m, int J, const doubl
   __syncthreads();
   backsolve_cta(J, R, m + 1, s_s, s_rhs, y, s_y);
 }
+#endif
 
 }  // namespace g200

@@ -1,0 +1,16 @@
+// ks_f32_ext.cu — kernel-table translation unit (see ktab.h): the monitor / chunk-ring / ILU / virtual-rank solve kernels (float).
+#include "gmres_kernels.cuh"
+#include "ktab.h"
+
+namespace g200 {
+void* ktab_solve_f32_ext(int variant, int L) {
+  const bool l1 = L == 1;
+  switch (variant) {
+    case 1: return l1 ? (void*)&solve_kernel<float, 1, false, true> : (void*)&solve_kernel<float, 4, false, true>;
+    case 2: return l1 ? (void*)&solve_kernel<float, 1, false, false, true> : (void*)&solve_kernel<float, 4, false, false, true>;
+    case 3: return l1 ? (void*)&solve_kernel<float, 1, false, false, false, true>
+                      : (void*)&solve_kernel<float, 4, false, false, false, true>;
+    default: return l1 ? (void*)&solve_kernel<float, 1, true> : (void*)&solve_kernel<float, 4, true>;
+  }
+}
+}  // namespace g200

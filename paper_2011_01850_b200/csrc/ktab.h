@@ -1,0 +1,19 @@
+// ktab.h — kernel table: the host stubs of the __global__ template
+// instantiations, each group defined in its own translation unit (ks_*.cu,
+// kc_*.cu) so that build.py compiles them in parallel; gmres_capi.cu launches
+// through these pointers.
+#pragma once
+
+namespace g200 {
+// fused solve kernels (gmres_kernels.cuh solve_kernel<W, L, VR, MON, CH, PC>)
+void* ktab_solve_f32_lo(int L);   // default instantiation, L ∈ {1, 2, 4}
+void* ktab_solve_f32_hi(int L);   // default instantiation, L ∈ {8, 16, 32}
+void* ktab_solve_f64_lo(int L);
+void* ktab_solve_f64_hi(int L);
+// variant: 1 orthogonality monitor (MON), 2 chunk-ring MGS (CH), 3 ILU(0) (PC), 4 virtual ranks (VR); L ∈ {1, 4}
+void* ktab_solve_f32_ext(int variant, int L);
+void* ktab_solve_f64_ext(int variant, int L);
+// component kernels: kind 0 spmv, 1 resid, 2 ortho, 3 xupdate, 4 ilu apply, 5 micro, 6 chunk-ring ortho
+void* ktab_comp_f32(int kind, int L);
+void* ktab_comp_f64(int kind, int L);
+}  // namespace g200

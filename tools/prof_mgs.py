@@ -19,4 +19,4 @@ for prec in (G.MIXED, G.FP64):
             if best is None or r.kernel_ms < best.kernel_ms: best = r
         ph = best.phase_ns / 1e6
         print(f"{G._LIB_PATH.split('/')[-1]} {name} {'mixed' if prec else 'fp64'} prof={int(prof)} st={best.status} cyc={best.cycles} "
-              f"kern={best.kernel_ms:.2f} ms  spmv={ph[1]:.1f} ortho={ph[2]:.1f} s8={ph[8]:.1f} dot={ph[9]:.1f} red+upd={ph[10]:.1f} nslow={best.phase_ns[11]} slow_ms={ph[12]:.1f}", flush=True)
+              f"kern={best.kernel_ms:.2f} ms  spmv={ph[1]:.1f} ortho={ph[2]:.1f} s8={ph[8]:.1f} dot={ph[9]:.1f} red+upd={ph[10]:.1f} ar_n={int(best.phase_ns[13])} skew_us={best.phase_ns[11]/max(1,best.phase_ns[13])/1e3:.2f} prop_us={best.phase_ns[12]/max(1,best.phase_ns[13])/1e3:.2f}", flush=True)

@@ -79,7 +79,7 @@ int main() {
     {1, 0, 0, 0},
     {0, 16384, 1, 2}, {0, 16384, 1, 4}, {0, 32768, 1, 2}, {0, 32768, 1, 4}, {0, 49152, 1, 3},
     {0, 32768, 8, 4}, {0, 32768, 16, 4}, {0, 32768, 32, 4}, {0, 65536, 32, 3}, {0, 65536, 16, 2},
-    {0, 4096, 1, 8}, {0, 8192, 1, 8}, {0, 86016, 21, 2},
+    {0, 4096, 1, 8}, {0, 8192, 1, 8}, {0, 8192, 1, 16}, {0, 8192, 1, 24}, {0, 16384, 1, 8}, {0, 86016, 21, 2},
   };
   for (auto& c : cs) {
     float best = 1e9;
