@@ -229,6 +229,8 @@ void* pick_solve_ext(int prec, int variant, int L) {
 void* pick_solve_monitor(int prec, int L) { return pick_solve_ext(prec, 1, L); }
 // chunk-ring MGS launches (d.mgs_resident == 2): L ∈ {1, 4}
 void* pick_solve_chunked(int prec, int L) { return pick_solve_ext(prec, 2, L); }
+// streamed MGS launches (d.mgs_resident == 3): L ∈ {1, 4}
+void* pick_solve_stream(int prec, int L) { return pick_solve_ext(prec, 5, L); }
 // ILU(0)-preconditioned launches (§8 f2): L ∈ {1, 4}
 void* pick_solve_ilu(int prec, int L) { return pick_solve_ext(prec, 3, L); }
 // virtual-rank launches (several row blocks on one device): L ∈ {1, 4}
@@ -1057,8 +1059,8 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
       int wsm = std::max(0, std::min(force_stream ? MGS_IC : slots - ns * MGS_IC, nch));
       wsm -= wsm % MGS_IC;                                        // whole items of shared w
       const int tb = std::max(tile_bytes, ns * MGS_ITEM + wsm * MGS_CHUNK);
-      if ((nch > MGS_MV || force_stream) && ns >= 2 && fits(pick_solve_chunked(precision, L), tb)) {
-        kern = pick_solve_chunked(precision, L);
+      if ((nch > MGS_MV || force_stream) && ns >= 2 && fits(pick_solve_stream(precision, L), tb)) {
+        kern = pick_solve_stream(precision, L);
         mgs_resident = 3;
         mgs_nbuf = ns;
         mgs_wsm = wsm;

@@ -2094,21 +2094,22 @@ __device__ __forceinline__ bool final_norm(const Dev& d, Shm& sh, int r0, int r1
 // Orthogonalisation of w (own rows) against V[:, 0..j) and its norm: MGS
 // or CGSR (two passes).  s_h[0..j) gets
 // h_{1..j, j}; returns ‖w‖² through NN.
-// CH: the chunk-ring kernel instantiation (mgs_chunked, launched only with
-// d.mgs_resident == 2); the default one holds mgs_resident and mgs_sweep.  Each
+// CH: 1 the chunk-ring kernel instantiation (mgs_chunked, d.mgs_resident == 2),
+// 2 the streamed one (mgs_stream, d.mgs_resident == 3); the default one (0) holds
+// mgs_resident and mgs_sweep.  Each
 // MGS variant lives in its own kernel: inlined together they raise the register
 // pressure of every phase (tools/regcheck.sh).
-template <class W, bool MON = false, bool CH = false>
+template <class W, bool MON = false, int CH = 0>
 __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
                             double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
                             char* s_tiles, double& NN) {
-  if constexpr (CH) {
+  if constexpr (CH != 0) {
     if (d.ortho == 0) {
       double nn = 0.0;
-      if (d.mgs_resident == 3) {
+      if constexpr (CH == 2) {
         if (!mgs_stream<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
-      } else if (!mgs_chunked<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) {
-        return false;
+      } else {
+        if (!mgs_chunked<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
       }
       return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
     }
@@ -2117,7 +2118,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
     if (!mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
     return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
   }
-  if (!CH && d.ortho == 0) {
+  if (CH == 0 && d.ortho == 0) {
     W hprev = (W)0;
     const bool pf = !(d.tune & 1) && r1 > r0;
     const unsigned pf_bytes = (unsigned)((r1 - r0) * (int)sizeof(W));
@@ -2207,7 +2208,7 @@ struct DevSet {
   int nv;  // ranks in this launch (1 = one rank per process/GPU)
 };
 
-template <class W, int L, bool VR, bool MON = false, bool CH = false, bool PC = false>
+template <class W, int L, bool VR, bool MON = false, int CH = 0, bool PC = false>
 __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ DevSet ds) {
   // (VR = false: a static index keeps every field of d a constant-bank operand)
   const int vr = VR ? (int)blockIdx.x / ds.G : 0;

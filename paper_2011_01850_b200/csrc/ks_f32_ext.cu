@@ -1,4 +1,4 @@
-// ks_f32_ext.cu — kernel-table translation unit (see ktab.h): the monitor / chunk-ring / ILU / virtual-rank solve kernels (float).
+// ks_f32_ext.cu — kernel-table translation unit (see ktab.h): the monitor / chunk-ring / streamed-MGS / ILU / virtual-rank solve kernels (float).
 #include "gmres_kernels.cuh"
 #include "ktab.h"
 
@@ -7,9 +7,10 @@ void* ktab_solve_f32_ext(int variant, int L) {
   const bool l1 = L == 1;
   switch (variant) {
     case 1: return l1 ? (void*)&solve_kernel<float, 1, false, true> : (void*)&solve_kernel<float, 4, false, true>;
-    case 2: return l1 ? (void*)&solve_kernel<float, 1, false, false, true> : (void*)&solve_kernel<float, 4, false, false, true>;
-    case 3: return l1 ? (void*)&solve_kernel<float, 1, false, false, false, true>
-                      : (void*)&solve_kernel<float, 4, false, false, false, true>;
+    case 2: return l1 ? (void*)&solve_kernel<float, 1, false, false, 1> : (void*)&solve_kernel<float, 4, false, false, 1>;
+    case 5: return l1 ? (void*)&solve_kernel<float, 1, false, false, 2> : (void*)&solve_kernel<float, 4, false, false, 2>;
+    case 3: return l1 ? (void*)&solve_kernel<float, 1, false, false, 0, true>
+                      : (void*)&solve_kernel<float, 4, false, false, 0, true>;
     default: return l1 ? (void*)&solve_kernel<float, 1, true> : (void*)&solve_kernel<float, 4, true>;
   }
 }
