@@ -217,6 +217,14 @@ int gmres_k_resid(gmres_ctx* ctx, int32_t precision, const double* d_b, const do
  * CGSR solve keeps its basis in and runs on that copy. */
 int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
                   void* d_w, double* h_out);
+/* The same with the MGS variant chosen: mgs_variant −1 = the one a solve on this
+ * context would run (gmres_k_ortho), 0 global sweep, 1 register-resident w with a
+ * whole-vector TMA ring, 2 chunk ring, 3 streamed (w off chip); GMRES_EINVAL if the
+ * requested variant does not fit.  *variant_used (may be NULL) receives the variant
+ * that ran (−1 for CGSR).  All variants perform the same operations in the same
+ * order (reading R9), so their results agree bit for bit. */
+int gmres_k_ortho_ex(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
+                     void* d_w, double* h_out, int32_t mgs_variant, int32_t* variant_used);
 
 /* a8 (Alg. 1): d_x += Σ_{i<J} (double)V_i · y_i; y host[J];
  * d_V as for gmres_k_ortho.  blocked != 0: run on a row-blocked copy of V

@@ -937,6 +937,80 @@ void gmres_destroy(gmres_ctx* ctx) {
 }
 
 namespace {
+// MGS variant of a launch (gmres_kernels.cuh a3): 1 mgs_resident — w in ≤ MGS_MV
+// 16-byte registers per thread and a ring of NB = 3 (else 2) whole basis-vector
+// row blocks; 2 mgs_chunked — the rest of w in shared memory and a ring of ≥ one
+// vector's worth of MGS_CHUNK slots; 3 mgs_stream — w off chip (shared + L2), a
+// ring of MGS_ITEM slots; 0 mgs_sweep (fallback).  want = −1: the first that
+// fits in that order; else exactly that variant (GMRES_EINVAL if it does not
+// fit).  kern_for(v): the kernel a variant runs in (its static shared memory
+// and occupancy decide "fits").  ext: the chunk-ring / streamed kernels exist
+// for this launch.
+extern "C++" {
+struct MgsPlan { int variant = 0, nbuf = 2, wsm = 0, tile_bytes = 0; const void* kern = nullptr; };
+template <class KernFor>
+int plan_mgs(gmres_ctx* ctx, int precision, int m, int G, int tile_bytes, int want, int tune, bool ext,
+             int ctas_per_sm, KernFor kern_for, MgsPlan& out) {
+  const int wb = precision == GMRES_MIXED ? 4 : 8;
+  const int nq = ctx->part_max_rows / (16 / wb);
+  const int nch = (nq + NT - 1) / NT;
+  const int buf_bytes = ((nq + 7) & ~7) * 16;
+  out = MgsPlan{};
+  out.tile_bytes = tile_bytes;
+  out.kern = kern_for(0);
+  // a candidate staging size fits when dynamic + the kernel's static shared memory stay within the
+  // per-block opt-in limit and the grid stays co-resident; a failed probe leaves no latched error
+  auto fits = [&](const void* k, int tb) {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return false; }
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (smem_bytes(m, tb) + fa.sharedSizeBytes > (size_t)optin) return false;
+    int G2 = 0;
+    const bool ok = grid_for(ctx, k, smem_bytes(m, tb), ctas_per_sm, &G2) == 0 && G2 >= G;
+    if (!ok) { cudaGetLastError(); ctx->err.clear(); }
+    return ok;
+  };
+  const bool any = want < 0;
+  if ((any || want == 1) && nq <= MGS_MV * NT && !(tune & 8192)) {
+    for (int nb = (tune & 256) ? 2 : 3; nb >= 2; --nb) {
+      const int tb = std::max(tile_bytes, nb * buf_bytes);
+      if (fits(kern_for(1), tb)) {
+        out = MgsPlan{1, nb, 0, tb, kern_for(1)};
+        return 0;
+      }
+    }
+  }
+  if ((any || want == 2) && ext) {
+    const int wsm = std::max(0, nch - MGS_MV);
+    const int ns = std::min<int>(MGS_MAXSLOT, tile_bytes_for(m) / MGS_CHUNK - wsm);
+    const int tb = std::max(tile_bytes, (ns + wsm) * MGS_CHUNK);
+    if (ns >= nch && fits(kern_for(2), tb)) {
+      out = MgsPlan{2, ns, wsm, tb, kern_for(2)};
+      return 0;
+    }
+  }
+  // streamed: a ring of item slots, as many whole items of w in shared memory as
+  // the rest of the staging region holds (one item when forced, to exercise both tiers)
+  if ((any || want == 3) && ext && !(tune & 16384) && (nch > MGS_MV || want == 3)) {
+    const int slots = tile_bytes_for(m) / MGS_CHUNK;
+    const int ns = std::min(MGS_STREAM_SLOTS, slots / MGS_IC);
+    int wsm = std::max(0, std::min(want == 3 ? MGS_IC : slots - ns * MGS_IC, nch));
+    wsm -= wsm % MGS_IC;
+    const int tb = std::max(tile_bytes, ns * MGS_ITEM + wsm * MGS_CHUNK);
+    if (ns >= 2 && fits(kern_for(3), tb)) {
+      out = MgsPlan{3, ns, wsm, tb, kern_for(3)};
+      return 0;
+    }
+  }
+  if (any || want == 0) return 0;  // mgs_sweep
+  return fail(ctx, GMRES_EINVAL, "the requested MGS variant does not fit this matrix / launch");
+}
+}  // extern "C++"
+
 // Everything a launch of the fused solve needs for one rank: validation,
 // grid, partition, basis layout, workspace, the a0 cast, x0 and the Dev.
 struct Plan {
@@ -1001,73 +1075,24 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   const VLayout vl = (opts && (opts->tune & 4096)) ? VLayout{} :
                      vlayout_for(ortho, m, precision == GMRES_MIXED ? 4 : 8, tile_bytes);
   if (int rc = ensure_partition(ctx, G, vl.tb ? vl.tb : ROWALIGN)) return rc;
-  // resident MGS: every CTA's rows of w on chip.  mgs_resident: w in ≤ MGS_MV
-  // 16-byte registers per thread and a ring of NB = 3 (else 2) shared buffers
-  // of one basis-vector row block; else mgs_chunked: the rest of w in shared
-  // memory and a ring of ≥ one vector's worth of MGS_CHUNK-byte slots
   int mgs_resident = 0, mgs_nbuf = 2, mgs_wsm = 0;
   if (ortho == GMRES_MGS) {
-    const int wb = precision == GMRES_MIXED ? 4 : 8;
-    const int per_vec = 16 / wb;
-    const int nq = ctx->part_max_rows / per_vec;
-    const int buf_bytes = ((nq + 7) & ~7) * 16;
     const int tune = opts ? opts->tune : 0;
-    // a candidate staging size fits when dynamic + the kernel's static shared memory stay within the
-    // per-block opt-in limit and the grid stays co-resident; a failed probe leaves no latched error
-    auto fits = [&](const void* k, int tb) {
-      cudaFuncAttributes fa{};
-      if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return false; }
-      int optin = 0;
-      if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-      }
-      if (smem_bytes(m, tb) + fa.sharedSizeBytes > (size_t)optin) return false;
-      int G2 = 0;
-      const bool ok = grid_for(ctx, k, smem_bytes(m, tb), opts ? opts->ctas_per_sm : 0, &G2) == 0 && G2 >= G;
-      if (!ok) { cudaGetLastError(); ctx->err.clear(); }
-      return ok;
-    };
-    const bool force_stream = (tune & 524288) != 0;  // dev/test: the streamed MGS even where w fits on chip
-    for (int nb = (tune & 256) ? 2 : 3; nb >= 2 && nq <= MGS_MV * NT && !(tune & (4 | 8192)) && !force_stream && !mgs_resident; --nb) {
-      const int tb = std::max(tile_bytes, nb * buf_bytes);
-      if (fits(kern, tb)) {
-        mgs_resident = 1;
-        mgs_nbuf = nb;
-        tile_bytes = tb;
-      }
-    }
-    if (!mgs_resident && !(tune & 4) && !force_stream && !virt && policy != 3 && !ilu && (L == 1 || L == 4)) {  // the chunk-ring kernels
-      const int nch = (nq + NT - 1) / NT;
-      const int wsm = std::max(0, nch - MGS_MV);
-      const int ns = std::min<int>(MGS_MAXSLOT, tile_bytes_for(m) / MGS_CHUNK - wsm);
-      const int tb = std::max(tile_bytes, (ns + wsm) * MGS_CHUNK);
-      if (ns >= nch && fits(pick_solve_chunked(precision, L), tb)) {
-        kern = pick_solve_chunked(precision, L);
-        mgs_resident = 2;
-        mgs_nbuf = ns;
-        mgs_wsm = wsm;
-        tile_bytes = tb;
-      }
-    }
-    // streamed MGS (w off chip: C4-sized row blocks): a ring of NS chunk slots and
-    // as many w chunks in shared memory as the rest of the staging region holds
-    if (!mgs_resident && !(tune & (4 | 16384)) && !virt && policy != 3 && !ilu && (L == 1 || L == 4)) {
-      const int nch = (nq + NT - 1) / NT;
-      const int slots = tile_bytes_for(m) / MGS_CHUNK;            // chunk-sized pieces of the staging region
-      const int ns = std::min(MGS_STREAM_SLOTS, slots / MGS_IC);  // item slots of the ring
-      int wsm = std::max(0, std::min(force_stream ? MGS_IC : slots - ns * MGS_IC, nch));
-      wsm -= wsm % MGS_IC;                                        // whole items of shared w
-      const int tb = std::max(tile_bytes, ns * MGS_ITEM + wsm * MGS_CHUNK);
-      if ((nch > MGS_MV || force_stream) && ns >= 2 && fits(pick_solve_stream(precision, L), tb)) {
-        kern = pick_solve_stream(precision, L);
-        mgs_resident = 3;
-        mgs_nbuf = ns;
-        mgs_wsm = wsm;
-        tile_bytes = tb;
-      }
-    }
-    if (mgs_resident) smem = smem_bytes(m, tile_bytes);
+    const bool ext = !virt && policy != 3 && !ilu && (L == 1 || L == 4);  // chunk-ring / streamed kernels exist
+    const int want = (tune & 4) ? 0 : (tune & 524288) ? 3 : -1;
+    MgsPlan mp;
+    if (int rc = plan_mgs(ctx, precision, m, G, tile_bytes, want, tune, ext, opts ? opts->ctas_per_sm : 0,
+                          [&](int v) -> const void* {
+                            return v == 2 ? pick_solve_chunked(precision, L)
+                                 : v == 3 ? pick_solve_stream(precision, L) : kern;
+                          }, mp))
+      return rc;
+    mgs_resident = mp.variant;
+    mgs_nbuf = mp.nbuf;
+    mgs_wsm = mp.wsm;
+    tile_bytes = mp.tile_bytes;
+    kern = mp.kern;
+    smem = smem_bytes(m, tile_bytes);
   }
   const int hist_cap_dev = max_cycles + 2;
   const int inner_cap_dev = P.rec_inner ? (int)std::min<int64_t>((int64_t)max_cycles * m, 1 << 22) : 0;
@@ -1627,11 +1652,12 @@ int gmres_k_resid(gmres_ctx* ctx, int32_t precision, const double* d_b, const do
   return rc;
 }
 
-int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
-                  void* d_w, double* h_out) {
+int gmres_k_ortho_ex(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
+                     void* d_w, double* h_out, int32_t mgs_variant, int32_t* variant_used) {
   if (!ctx || !d_V || !d_w || !h_out) return fail(ctx, GMRES_EINVAL, "null argument");
   if (j < 1 || ldv < ctx->ldv || ldv % LDALIGN) return fail(ctx, GMRES_EINVAL, "need j >= 1, ldv >= round_up(n,256), ldv % 64 == 0");
   if (ortho != GMRES_MGS && ortho != GMRES_CGSR) return fail(ctx, GMRES_EINVAL, "bad ortho");
+  if (mgs_variant < -1 || mgs_variant > 3) return fail(ctx, GMRES_EINVAL, "mgs_variant must be -1, 0, 1, 2 or 3");
   const int L = auto_lanes(ctx->n, ctx->nnz);
   const void* kern;
   int G;
@@ -1651,6 +1677,23 @@ int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, c
   Dev d = make_dev(ctx, m, precision, ortho, G);
   set_vlayout(d, vl);
   if (vl.tb) d_V = ctx->d_V;
+  int used = -1;
+  if (ortho == GMRES_MGS) {  // the MGS variant the solve would run (or the one requested)
+    MgsPlan mp;
+    if (int rc = plan_mgs(ctx, precision, m, G, TILE_BYTES, mgs_variant, 0, true, 0,
+                          [&](int v) -> const void* { return pick_kernel(precision, v == 2 ? 6 : v == 3 ? 7 : 2, L); },
+                          mp))
+      return rc;
+    kern = mp.kern;
+    d.mgs_resident = mp.variant;
+    d.mgs_nbuf = mp.nbuf;
+    d.mgs_wsm = mp.wsm;
+    d.tile_bytes = mp.tile_bytes;
+    set_smem_offsets(d);
+    smem = smem_bytes(m, mp.tile_bytes);
+    used = mp.variant;
+  }
+  if (variant_used) *variant_used = used;
   double* d_h = nullptr;
   CK(cudaMalloc(&d_h, sizeof(double) * (j + 1)));
   long long ld = ldv;
@@ -1668,6 +1711,11 @@ int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, c
   cudaMemcpy(&fl, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost);
   if (rc == 0 && fl) rc = fail(ctx, GMRES_ETIMEOUT, "device watchdog fired");
   return rc;
+}
+
+int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
+                  void* d_w, double* h_out) {
+  return gmres_k_ortho_ex(ctx, precision, ortho, j, d_V, ldv, d_w, h_out, -1, nullptr);
 }
 
 int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_V, int64_t ldv, const double* y,

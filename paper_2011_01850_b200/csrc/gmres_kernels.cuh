@@ -2473,12 +2473,13 @@ __global__ void __launch_bounds__(NT, 1) k_resid_kernel(Dev d, W* r, double* out
   if (blockIdx.x == 0 && threadIdx.x < 2) out2[threadIdx.x] = s_out[threadIdx.x];
 }
 
-template <class W>
+template <class W, int CH = 0>
 __global__ void __launch_bounds__(NT, 1) k_ortho_kernel(Dev d, int j, const W* V, long long ldv, W* w, double* hout) {
   G200_SMEM_CARVE(W)
   const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
   double NN = 0.0;
-  if (!ortho_phase<W>(d, sh, r0, r1, j, V, ldv, w, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) return;
+  if (!ortho_phase<W, false, CH>(d, sh, r0, r1, j, V, ldv, w, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN))
+    return;
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < j; i += NT) hout[i] = s_h[i];
     if (threadIdx.x == 0) hout[j] = sqrt(NN);

@@ -23,7 +23,9 @@ void* ktab_comp_f64(int kind, int L) {
         case 16: return (void*)&k_resid_kernel<double, 16>;
         default: return (void*)&k_resid_kernel<double, 32>;
       }
-    case 2: return (void*)&k_ortho_kernel<double>;
+    case 2: return (void*)&k_ortho_kernel<double, 0>;
+    case 6: return (void*)&k_ortho_kernel<double, 1>;  // chunk-ring MGS
+    case 7: return (void*)&k_ortho_kernel<double, 2>;  // streamed MGS
     case 4: return (void*)&k_ilu_apply_kernel<double>;
     case 5: return (void*)&k_micro_kernel<double>;
     default: return (void*)&k_xupdate_kernel<double>;

@@ -88,12 +88,13 @@ def load_library():
     L.gmres_k_spmv.argtypes = [vp, i32, vp, vp]
     L.gmres_k_resid.argtypes = [vp, i32, vp, vp, vp, vp]
     L.gmres_k_ortho.argtypes = [vp, i32, i32, i32, vp, i64, vp, vp]
+    L.gmres_k_ortho_ex.argtypes = [vp, i32, i32, i32, vp, i64, vp, vp, i32, ctypes.POINTER(i32)]
     L.gmres_k_xupdate.argtypes = [vp, i32, i32, vp, i64, vp, vp, i32]
     L.gmres_k_hessenberg.argtypes = [vp, i32, i32, vp, dbl, vp, vp, vp]
     L.gmres_k_cast32.argtypes = [vp]
     L.gmres_k_micro.argtypes = [vp, i32, i32, i32, i32, vp, i64, vp, vp]
     L.gmres_k_matrix.argtypes = [vp, vp, vp, vp, vp, vp]
-    for f in ("gmres_k_spmv", "gmres_k_resid", "gmres_k_ortho", "gmres_k_xupdate", "gmres_k_hessenberg",
+    for f in ("gmres_k_spmv", "gmres_k_resid", "gmres_k_ortho", "gmres_k_ortho_ex", "gmres_k_xupdate", "gmres_k_hessenberg",
               "gmres_k_cast32", "gmres_k_matrix", "gmres_k_micro"):
         getattr(L, f).restype = ctypes.c_int
     p64 = ctypes.POINTER(i64)
@@ -368,11 +369,14 @@ class Solver:
         self._ck(self._lib.gmres_k_resid(self._h, _prec(precision), _p(b), _p(x), _p(r), _p(out)))
         return float(out[0]), float(out[1])
 
-    def k_ortho(self, precision, ortho, j, V, ldv, w):
+    def k_ortho(self, precision, ortho, j, V, ldv, w, mgs_variant=-1, return_variant=False):
+        """gmres_k_ortho_ex: h_{1..j} and h[j] = ‖w‖ (w orthogonalised in place); mgs_variant −1 = the
+        solve's choice, 0 sweep, 1 resident, 2 chunk ring, 3 streamed."""
         h = np.zeros(j + 1)
-        self._ck(self._lib.gmres_k_ortho(self._h, _prec(precision), _ortho(ortho), int(j), _p(V), int(ldv), _p(w),
-                                         _p(h)))
-        return h
+        used = ctypes.c_int32()
+        self._ck(self._lib.gmres_k_ortho_ex(self._h, _prec(precision), _ortho(ortho), int(j), _p(V), int(ldv), _p(w),
+                                            _p(h), int(mgs_variant), ctypes.byref(used)))
+        return (h, used.value) if return_variant else h
 
     def k_xupdate(self, precision, J, V, ldv, y, x, blocked=False):
         y = np.ascontiguousarray(y, np.float64)

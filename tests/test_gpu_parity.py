@@ -6,7 +6,9 @@ oracle's step on identical inputs.  End-to-end parity checks the final
 residual recomputed by the oracle (‖b − A x‖/‖b‖ ≤ 1e-10) and the restart
 count within ±10 % of the oracle's (BASELINE.json).
 """
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -100,10 +102,15 @@ def test_resid_parity(mat, prec):
 
 
 # ------------------------------------------------------------------ a3/a4/a5
-@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+# every MGS variant the solves run (1 resident ring, 2 chunk ring, 3 streamed, 0 sweep),
+# steps up to the bench's m = 50, C4's m = 100 and C5's m = 200
+ORTHO_CASES = [(G.MGS, v) for v in (1, 2, 3, 0)] + [(G.CGSR, -1)]
+
+
+@pytest.mark.parametrize("ortho,variant", ORTHO_CASES, ids=["mgs_resident", "mgs_chunk", "mgs_stream", "mgs_sweep", "cgsr"])
 @pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
-@pytest.mark.parametrize("j", [1, 7, 33])
-def test_ortho_parity(mat, prec, ortho, j):
+@pytest.mark.parametrize("j", [1, 7, 33, 50, 100, 200])
+def test_ortho_parity(mat, prec, ortho, variant, j):
     name, A, S = mat
     n = A.n
     ld = G.ld_for(n)
@@ -118,7 +125,8 @@ def test_ortho_parity(mat, prec, ortho, j):
     Vpad[:, :n] = Vw.T
     Vd = tdev(Vpad)
     wd = tdev(w0)
-    h = S.k_ortho(prec, ortho, j, Vd, ld, wd)
+    h, used = S.k_ortho(prec, ortho, j, Vd, ld, wd, mgs_variant=variant, return_variant=True)
+    assert used == variant
     w = wd.cpu().numpy().astype(np.float64)
     nw = np.linalg.norm(w0.astype(np.float64))
     tol = 1e-12 if prec == G.FP64 else 1e-5
@@ -311,29 +319,64 @@ def _sampled_spmv_rows(P, S, prec, rng, nsample=3000):
         assert abs(float(w[i]) - exact) <= 2 * k * u * scale + 1e-300, (i, e - s)
 
 
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full_size")
+
+
+def golden(cfg, prec, ortho, m):
+    """Oracle record of a full-size config (tools/make_golden.py: the CPU oracle only)."""
+    key = f"{cfg}_{'mixed' if prec == G.MIXED else 'fp64'}_{'mgs' if ortho == G.MGS else 'cgsr'}_m{m}"
+    with open(os.path.join(GOLDEN, key + ".json")) as f:
+        return json.load(f)
+
+
+def within_10pct(c, ref):
+    """BASELINE.json: "restart count within ±10 % of the oracle's" (below 10 cycles: equal)."""
+    return abs(c - ref) <= 0.1 * ref
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("name", sorted(FULL))
 def test_full_size(name):
     P = inputs.make(name)
-    m, precs = FULL[name]
+    m, _ = FULL[name]
     S = G.Solver.from_csr(P.A)
     bd = tdev(P.b)
-    xd = torch.zeros_like(bd)
-    cycles = {}
     for ortho in (G.MGS, G.CGSR):
-        for prec in precs if ortho == G.CGSR else [G.MIXED]:
+        for prec in (G.MIXED, G.FP64):
+            xd = torch.zeros_like(bd)
             r = S.solve_device(bd, xd, m=m, ortho=ortho, precision=prec)
             assert r.status == 0, r.status_name
             rel = check_solution(P.A, P.b, xd.cpu().numpy())
             assert rel <= 1e-10, (name, ortho, prec, rel)
             assert r.final_relres == pytest.approx(rel, rel=1e-3, abs=1e-13)
-            cycles[(ortho, prec)] = r.cycles
-    # mixed vs fp64 (forced-restart regime): same restart count within ±10 %
-    c64, c32 = cycles[(G.CGSR, G.FP64)], cycles[(G.CGSR, G.MIXED)]
-    assert abs(c32 - c64) <= max(1, 0.1 * c64), (c32, c64)
+            ref = golden(name, prec, ortho, m)
+            assert ref["status"] == 0 and ref["final_relres_recomputed"] <= 1e-10
+            assert within_10pct(r.cycles, ref["cycles"]), (name, ortho, prec, r.cycles, ref["cycles"])
+            # inner iterations: the same up to the fp32/fp64 rounding order of the last cycle
+            assert abs(r.inner_iters - ref["inner_iters"]) <= max(3, 0.05 * ref["inner_iters"]), \
+                (r.inner_iters, ref["inner_iters"])
     rng = np.random.default_rng(11)
     for prec in (G.MIXED, G.FP64):
         _sampled_spmv_rows(P, S, prec, rng)
+    S.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("m", [10, 25, 100, 200])
+def test_c5_restart_sweep_matches_oracle(m):
+    """BASELINE.json configs[4]: the C2 matrix at m ∈ {10, 25, 100, 200} (m = 50 is C2) —
+    restart counts within ±10 % of the oracle's for MGS/CGSR × fp64/mixed."""
+    P = inputs.make("C5")
+    S = G.Solver.from_csr(P.A)
+    bd = tdev(P.b)
+    for ortho in (G.MGS, G.CGSR):
+        for prec in (G.MIXED, G.FP64):
+            xd = torch.zeros_like(bd)
+            r = S.solve_device(bd, xd, m=m, ortho=ortho, precision=prec)
+            assert r.status == 0, r.status_name
+            assert check_solution(P.A, P.b, xd.cpu().numpy()) <= 1e-10
+            ref = golden("C5", prec, ortho, m)
+            assert within_10pct(r.cycles, ref["cycles"]), (m, ortho, prec, r.cycles, ref["cycles"])
     S.close()
 
 
@@ -344,22 +387,24 @@ def test_full_size(name):
 # picked so each ring engages (fp64 chunk ring: > 8 register vectors of w per
 # thread; the ragged grid side 109 leaves a partial last chunk).
 @pytest.mark.slow
-@pytest.mark.parametrize("prec,k,variant", [(G.MIXED, 64, 1), (G.FP64, 64, 1), (G.FP64, 109, 2), (G.MIXED, 137, 2)])
+@pytest.mark.parametrize("prec,k,variant", [(G.MIXED, 64, 1), (G.FP64, 64, 1), (G.FP64, 109, 2), (G.MIXED, 137, 2),
+                                            (G.FP64, 128, 2), (G.MIXED, 160, 2)])
 def test_mgs_variants_agree(prec, k, variant):
     P = inputs.make("C2", k)
     S = G.Solver.from_csr(P.A)
     bd = tdev(P.b)
     xs, its = [], []
-    for tune in (0, 4):   # tune bit 2: force the global sweep
+    # tune bit 2: force the global sweep; bit 19: force the streamed MGS (w in shared + global memory)
+    for tune, want in ((0, variant), (4, 0), (524288, 3)):
         xd = torch.zeros_like(bd)
         r = S.solve_device(bd, xd, m=30, ortho=G.MGS, precision=prec, max_cycles=3, tol=1e-14, tune=tune)
         assert r.status in (0, 1), r.status_name
         plan = S.plan()
-        assert plan["mgs_variant"] == (variant if tune == 0 else 0), plan
+        assert plan["mgs_variant"] == want, plan
         xs.append(xd.cpu().numpy())
         its.append((r.cycles, list(r.cycle_iters), r.final_relres))
-    assert its[0] == its[1]
-    assert np.array_equal(xs[0], xs[1])
+    assert its[0] == its[1] == its[2]
+    assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[0], xs[2])
     S.close()
 
 
