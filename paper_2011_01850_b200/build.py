@@ -16,8 +16,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_obj")
-LIB = os.path.join(HERE, "libgmres.so")
+OBJ = os.environ.get("G200_OBJ_DIR") or os.path.join(HERE, "_obj")
+LIB = os.environ.get("G200_LIB_OUT") or os.path.join(HERE, "libgmres.so")
 SOURCES = [os.path.join(CSRC, "gmres_capi.cu")] + sorted(glob.glob(os.path.join(CSRC, "ks_*.cu"))) + \
     sorted(glob.glob(os.path.join(CSRC, "kc_*.cu")))
 HEADERS = [os.path.join(CSRC, "gmres_kernels.cuh"), os.path.join(CSRC, "ktab.h"), os.path.join(ROOT, "include", "gmres.h")]
@@ -27,7 +27,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC",
     "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("G200_DEFINES", "").split()  # dev A/B builds only (e.g. -DG200_NTB=3)
 
 
 def nvcc() -> str:

@@ -198,7 +198,7 @@ VLayout vlayout_for(int ortho, int m, int wb, int tile_bytes) {
   if (ortho != GMRES_CGSR) return L;
   const int pade = 16 / wb;
   for (int tb = 256; tb >= 32; tb /= 2) {
-    if ((long long)(m + 1) * (tb + pade) * wb <= tile_bytes / 2) {
+    if ((long long)(m + 1) * (tb + pade) * wb <= tile_bytes / G200_NTB) {
       L.tb = tb;
       L.tp = tb + pade;
       L.lg = 0;

@@ -56,6 +56,9 @@ constexpr int TILE_BYTES = NGRP * 3 * (ST_OFF_A + (CHUNK_CAP + 8) * 8);  // 1720
 constexpr int MAX_M = 256;                               // restart length limit (shared-memory bound)
 constexpr int ARR_PAD = 8;   // elements of slack after rp/col/val (TMA rounds up to 16 B)
 constexpr int MAXR = 8;      // ranks (GPUs) of a row-partitioned solve
+#ifndef G200_NTB
+#define G200_NTB 2           // row-tile pass ring depth (rowtile_pass)
+#endif
 
 enum { ST_OK = 0, ST_NOT_CONVERGED = 1, ST_EFP32RANGE = -4, ST_ENONFINITE = -5, ST_ETIMEOUT = -8 };
 enum { ERRF_RANGE = 1, ERRF_NONFINITE = 2 };
@@ -322,7 +325,7 @@ struct Shm {
   unsigned long long mbar[NGRP][MAXSTG];  // TMA stage barriers (per CSR-stream group)
   unsigned long long mbar_v[32];     // TMA barriers of the resident MGS's ring (≤ MGS_MAXSLOT)
   unsigned long long mbar_e[32];     // streamed MGS: slot-consumed barriers (one arrival per warp)
-  unsigned long long mbar_t[3];      // TMA barriers of the row-tile passes' V tiles
+  unsigned long long mbar_t[4];      // TMA barriers of the row-tile passes' V tiles
   unsigned long long mbar_b[NBS];    // TMA barriers of the block stream's stages
   int bcnt[NBS];                     // warps done with a block-stream stage
   unsigned bphase;                   // bit s: parity of the next completion of mbar_b[s]
@@ -330,6 +333,7 @@ struct Shm {
   unsigned vphase;                   // bit b: parity of the next completion of mbar_v[b] (mgs_resident)
   unsigned vg;                       // chunk-ring MGS: stream chunks issued so far (thread 0 writes)
   unsigned tphase;                   // bit b: parity of the next completion of mbar_t[b]
+  int cdir;                          // CGSR: direction of the next iteration's first pass
   int abort;
   int flag;
   unsigned long long epoch;          // grid barriers passed by this CTA (thread 0)
@@ -373,8 +377,9 @@ __device__ __forceinline__ void init_shm(Shm& sh, int cta) {
     }
     for (int b = 0; b < 32; ++b) mbar_init(&sh.mbar_v[b], 1);
     for (int b = 0; b < 32; ++b) mbar_init(&sh.mbar_e[b], NW);
-    for (int b = 0; b < 3; ++b) mbar_init(&sh.mbar_t[b], 1);
+    for (int b = 0; b < 4; ++b) mbar_init(&sh.mbar_t[b], 1);
     sh.tphase = 0;
+    sh.cdir = 0;
     for (int b = 0; b < NBS; ++b) { mbar_init(&sh.mbar_b[b], 1); sh.bcnt[b] = 0; }
     sh.bphase = 0;
     fence_mbar_init();
@@ -1374,10 +1379,10 @@ constexpr int MAXSLOT = (MAX_M + 1 + 31) / 32;  // columns per lane
 template <class W, int MODE>
 __device__ __forceinline__ void rowtile_pass(const Dev& d, Shm& sh, int r0, int r1, const W* V, long long ldv,
                                              int ncols, W* w, const W* s_coefW, const double* s_y, double* s_acc,
-                                             char* s_tiles, double& nn) {
+                                             char* s_tiles, double& nn, int dir = 0, bool reuse = false) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
-  constexpr int NTB = 2;  // ring depth (3 was slower on C2: more, smaller bulk copies)
+  constexpr int NTB = G200_NTB;  // ring depth
   constexpr int NWS = MODE == 4 ? 0 : 1;  // w tile staged (MODE 1-3)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nrows = r1 - r0;  // multiple of ROWALIGN
@@ -1426,13 +1431,22 @@ __device__ __forceinline__ void rowtile_pass(const Dev& d, Shm& sh, int r0, int 
                     bar);
     }
   };
+  // tiles in the pass's order: forward or reverse (dir); tile k always in buffer
+  // k mod NTB.  reuse: the previous pass ran over the same tiles in the other
+  // direction, so this pass's first min(NTB, ntile) tiles are still staged (its
+  // last ones) — no copy, no wait — and the rest start where its reads ended
+  // (the most recently streamed V rows, the ones left in L2).
+  auto tile_of = [&](int kk) { return dir ? ntile - 1 - kk : kk; };
+  auto staged = [&](int kk) { return reuse && kk < NTB; };
   if (warp == 0)
-    for (int k = 0; k < NTB - 1 && k < ntile; ++k) issue(k);
-  for (int k = 0; k < ntile; ++k) {
+    for (int kk = 0; kk < NTB - 1 && kk < ntile; ++kk)
+      if (!staged(kk)) issue(tile_of(kk));
+  for (int kk = 0; kk < ntile; ++kk) {
+    const int k = tile_of(kk);
     const int b = k % NTB;
-    // the buffer of tile k−1 is free (barrier at the end of its iteration)
-    if (warp == 0 && k + NTB - 1 < ntile) issue(k + NTB - 1);
-    {
+    // the buffer of the tile before last is free (barrier at the end of its iteration)
+    if (warp == 0 && kk + NTB - 1 < ntile && !staged(kk + NTB - 1)) issue(tile_of(kk + NTB - 1));
+    if (!staged(kk)) {
       const unsigned par = (ph >> b) & 1u;
       ph ^= (1u << b);
       if (!mbar_try_wait(&sh.mbar_t[b], par)) {
@@ -2146,7 +2160,10 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
       if (lead) { const unsigned long long t = globaltimer(); d.prof[8 + slot] += t - tp; tp = t; }
     }
   };
-  rowtile_pass<W, 1>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  // serpentine passes (rowtile_pass: reuse): 1 in direction D, 2 reversed, 3 in D;
+  // D alternates between iterations, so every pass starts on the rows read last
+  const int D = sh.cdir;
+  rowtile_pass<W, 1>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn, D, false);
   combine_acc(d, s_tmp, j, s_part);
   sub(0);
   if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp, false)) return false;
@@ -2156,7 +2173,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
     s_coefW[i] = RN<W>(s_out[i]);
   }
   __syncthreads();
-  rowtile_pass<W, 2>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  rowtile_pass<W, 2>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn, 1 - D, true);
   combine_acc(d, s_tmp, j, s_part);
   sub(2);
   if (!grid_allreduce(d, sh, s_part, j, s_out, s_tmp, false)) return false;
@@ -2167,7 +2184,8 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   }
   __syncthreads();
   nn = 0.0;
-  rowtile_pass<W, 3>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn);
+  rowtile_pass<W, 3>(d, sh, r0, r1, V, ldv, j, w, s_coefW, s_y, s_tmp, s_tiles, nn, D, true);
+  if (threadIdx.x == 0) sh.cdir = 1 - D;  // (every thread read D before the passes' barriers)
   sub(4);
   if (!final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN))
     return false;
