@@ -282,6 +282,18 @@ __device__ __forceinline__ unsigned long long policy_evict_normal() {
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// scalar global loads with an L2 eviction-priority policy (SpMV gathers: evict_last
+// keeps the gathered vector in L2 while the CSR arrays stream past it)
+__device__ __forceinline__ float ld_pol(const float* p, unsigned long long pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_pol(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
 // plain arrival (no transaction bytes) on a shared mbarrier
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -698,6 +710,7 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
   char* gbase = s_stage + grp * NS * SB;
   MetaWin mw;
   mw.init(d, c0, c1, grp);
+  const unsigned long long pol_a = policy_evict_first();  // the CSR arrays are read once per SpMV
   auto issue = [&](const ChunkMeta& m, int s) {  // group leader only
     if (m.direct) return;
     char* st = gbase + s * SB;
@@ -709,11 +722,11 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
     // (no proxy fence: the TMA reads data no generic store of this launch
     // wrote, and overwrites a stage the warp finished reading before the __syncwarp)
     mbar_expect_tx(&sh.mbar[grp][s], b_rp + b_rv + b_ci + b_a);
-    tma_load_1d(st, d.rp + m.rb, b_rp, &sh.mbar[grp][s]);
-    tma_load_1d(st + ST_OFF_RV, rowv + m.rb, b_rv, &sh.mbar[grp][s]);
+    tma_load_1d_hint(st, d.rp + m.rb, b_rp, &sh.mbar[grp][s], pol_a);
+    tma_load_1d_hint(st + ST_OFF_RV, rowv + m.rb, b_rv, &sh.mbar[grp][s], pol_a);
     if (b_ci) {
-      tma_load_1d(st + ST_OFF_CI, d.ci + ea, b_ci, &sh.mbar[grp][s]);
-      tma_load_1d(st + ST_OFF_A, vals + ea, b_a, &sh.mbar[grp][s]);
+      tma_load_1d_hint(st + ST_OFF_CI, d.ci + ea, b_ci, &sh.mbar[grp][s], pol_a);
+      tma_load_1d_hint(st + ST_OFF_A, vals + ea, b_a, &sh.mbar[grp][s], pol_a);
     }
   };
   for (int t = 0; t < NS && t < nk; ++t) {
@@ -847,9 +860,9 @@ __device__ void csr_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __res
         const int p0 = __ldg(d.rp + row), p1 = __ldg(d.rp + row + 1);
         AT acc = (AT)0, dg = (AT)0;
         for (int p = p0 + wl; p < p1; p += 32) {
-          const int col = __ldg(d.ci + p);
+          const int col = __ldcs(d.ci + p);
           const AT g = gat(col);
-          acc = Ops::add(acc, Ops::mul(__ldg(vals + p), g));
+          acc = Ops::add(acc, Ops::mul(__ldcs(vals + p), g));
           if (col == row + gro) dg = g;
         }
 #pragma unroll
@@ -909,17 +922,18 @@ __device__ void csr_block_stream(const Dev& d, Shm& sh, char* s_stage, const AT*
     g.o_va = g.o_ci + (int)g.b_ci;
     return g;
   };
+  const unsigned long long pol_a = policy_evict_first();  // the CSR arrays are read once per SpMV
   auto issue = [&](int k) {  // one thread
     const Geo g = geo(k);
     const int slot = k % NBS;
     char* st = s_stage + slot * BS_BYTES;
     unsigned long long* bar = &sh.mbar_b[slot];
     mbar_expect_tx(bar, g.b_rp + g.b_rv + g.b_ci + g.b_va);
-    tma_load_1d(st, d.rp + g.rb, g.b_rp, bar);
-    tma_load_1d(st + g.o_rv, rowv + g.rb, g.b_rv, bar);
+    tma_load_1d_hint(st, d.rp + g.rb, g.b_rp, bar, pol_a);
+    tma_load_1d_hint(st + g.o_rv, rowv + g.rb, g.b_rv, bar, pol_a);
     if (g.b_ci) {
-      tma_load_1d(st + g.o_ci, d.ci + g.ea, g.b_ci, bar);
-      tma_load_1d(st + g.o_va, vals + g.ea, g.b_va, bar);
+      tma_load_1d_hint(st + g.o_ci, d.ci + g.ea, g.b_ci, bar, pol_a);
+      tma_load_1d_hint(st + g.o_va, vals + g.ea, g.b_va, bar, pol_a);
     }
   };
   if (threadIdx.x == 0)
@@ -1023,7 +1037,8 @@ __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict_
   const W* dinv = (const W*)d.dinvW;
   const double* __restrict__ xg = d.x - d.row_base;  // global-index view (CSR columns are global)
   struct P2 { double b; W di; };
-  auto gat = [&](int col) -> double { return xg[col]; };
+  const unsigned long long pol_g = policy_evict_last();
+  auto gat = [&](int col) -> double { return ld_pol(xg + col, pol_g); };
   auto pre = [&](int row, W di) -> P2 { return P2{d.b[row], di}; };
   auto epi = [&](int row, double acc, P2 pv, double) {
     const double bi = pv.b;
@@ -1051,7 +1066,8 @@ __device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __rest
   const W* dinv = (const W*)d.dinvW;
   const W* __restrict__ srcg = src - d.row_base;  // global-index view (CSR columns are global)
   const W invW = RN<W>(inv);
-  auto gat = [&](int col) -> W { return mulw(srcg[col], invW); };
+  const unsigned long long pol_g = policy_evict_last();
+  auto gat = [&](int col) -> W { return mulw(ld_pol(srcg + col, pol_g), invW); };
   auto pre = [&](int, W di) -> W { return di; };
   auto epi = [&](int row, W acc, W di, W vj) {
     dst[row] = mulw(di, acc);
