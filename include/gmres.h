@@ -5,9 +5,10 @@
  * mixed-precision split of §4: the residual z = b − A·x
  * (Alg. 1 line 86) and the update x ← x + u (line 147) in fp64, everything in
  * between (lines 89–146) in fp32 on an fp32 copy of A ("the matrix is stored
- * twice").  Preconditioner: Jacobi M = diag(A) (BASELINE.json;
- * the paper's ILU(0), is out of scope this round).  H, the
- * Givens rotations and s are fp64 on the device (reading R7).
+ * twice").  Preconditioner: Jacobi M = diag(A) (BASELINE.json)
+ * by default; the paper's ILU(0) in W or, for the fp64 solver, in
+ * fp32 through gmres_opts.precond.  H, the Givens rotations and
+ * s are fp64 on the device (reading R7).
  *
  * All compute runs in hand-written sm_100a kernels (libgmres.so); no
  * cuSPARSE/cuBLAS.  Plain C: no C++ types or exceptions cross this boundary.
@@ -58,6 +59,9 @@ typedef struct {
   double final_relres;    /* ‖b − A x‖₂/‖b‖₂ of the returned x (fp64, on device)        */
   double device_ms;       /* device time of the solve (CUDA events), incl. the A32 cast */
   double kernel_ms;       /* device time of the fused solve kernel alone (CUDA events)  */
+  double final_backward_err; /* ‖b − A x‖₂/(‖A‖_F‖x‖₂ + ‖b‖₂) of the returned x (
+                             the paper's unnamed "backward error", PAPER.md:317, 431-433;
+                             report only — the stop test is final_relres)              */
 } gmres_result;
 
 typedef struct {
@@ -82,14 +86,18 @@ typedef struct {
                              part of V_kᵀV_k; ≤ 0 → 1.0.  Adds
                              one pass over the basis per inner iteration               */
   int32_t precond;        /* left preconditioner M: GMRES_PRECOND_JACOBI (0, default;
-                             reading R11) or GMRES_PRECOND_ILU0 (1: ILU(0) of A_W on A's
+                             reading R11), GMRES_PRECOND_ILU0 (1: ILU(0) of A_W on A's
                              pattern, factorised on the device inside every timed solve,
-                             PAPER.md:291, 427; reading R24).  ILU(0): single-rank contexts,
-                             restart policies 0–2                                       */
+                             PAPER.md:291, 427; reading R24) or GMRES_PRECOND_ILU0_FP32
+                             (2: precision GMRES_FP64 only — the fp64 solver with an fp32
+                             ILU(0) of RN32(A), applied as RN32(in) → fp32 solves → fp64:
+                             the paper's "single-precision ILU" arm, PAPER.md:428, 444,
+                             463).  ILU(0): single-rank contexts, restart policies 0–2  */
 } gmres_opts;
 
 #define GMRES_PRECOND_JACOBI 0
 #define GMRES_PRECOND_ILU0 1
+#define GMRES_PRECOND_ILU0_FP32 2
 
 /* Create a solver context on the current CUDA device: validates the CSR on the
  * host, copies A (fp64) to the device and extracts the Jacobi diagonal.
@@ -249,10 +257,12 @@ int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar,
 int gmres_ilu0_factor(gmres_ctx* ctx, int32_t precision, void* d_f);
 
 /* d_out = U⁻¹ L⁻¹ d_z (device, n W values each; d_out == d_z allowed) with the
- * factors of the last gmres_ilu0_factor of this precision: level-scheduled
- * forward then backward substitution, each row's sum in ascending column order
- * in W (one cooperative launch, a grid barrier per level). */
-int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* d_out);
+ * factors of the last gmres_ilu0_factor of this precision: forward then backward
+ * substitution, each row's sum in ascending column order in W, in one cooperative
+ * launch.  schedule 0: sync-free (rows poll their inputs' published values — the
+ * solve kernel's default); 65536: level-synchronous (a grid barrier per level).
+ * Both reproduce the oracle bit for bit. */
+int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* d_out, int32_t schedule);
 
 /* Level counts of the ILU(0) triangular solves (lower, upper): the length of
  * the dependency chains a level-scheduled solve serialises over. */

@@ -56,6 +56,7 @@ struct gmres_ctx {
   void* d_ones[2] = {nullptr, nullptr};  // W ones (nvec): the Jacobi scale of ILU solves
   int* d_ilu_bad = nullptr;
   void* d_ilu_pub[2] = {nullptr, nullptr};  // [n] fp64-sized publish buffers of the sync-free solves
+  float* d_ilu_s32[2] = {nullptr, nullptr}; // fp32 scratch vectors of the fp32-ILU-in-fp64 solver
   double* d_hb = nullptr;  // device staging of b / x for the host-array gmres_solve
   double* d_hx = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
@@ -126,6 +127,7 @@ struct gmres_ctx {
   unsigned long long epoch_base = 0;
   int red_base = 0;
   bool linked = false, ipc = false;
+  double normA2 = 0.0;                  // ‖A‖_F² of this context's rows (device-computed at create)
   void* peer_w0[MAXR] = {}, *peer_w1[MAXR] = {};
   double* peer_x[MAXR] = {};
   double* peer_slots[MAXR] = {};
@@ -701,6 +703,7 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.ortho = ortho;
   d.tile_bytes = tile_bytes_for(m);
   set_smem_offsets(d);
+  d.normA2 = ctx->normA2;
   d.rp = ctx->d_rp;
   d.ci = ctx->d_ci;
   d.a64 = ctx->d_a64;
@@ -850,6 +853,17 @@ int create_impl(const int32_t* row_ptr, const int32_t* col, const double* val, i
     cudaFree(d_bad);
     if (bad != big)
       return fail(ctx, GMRES_EZERODIAG, "zero or missing diagonal at row " + std::to_string(row_begin + bad));
+    {  // ‖A‖_F² of these rows (the solves report the normwise backward error)
+      const int np = ctx->sms * 4;
+      double* d_part = nullptr;
+      CK(cudaMalloc(&d_part, sizeof(double) * (np + 1)));
+      sumsq_partial_kernel<<<np, 256, 0, ctx->stream>>>(ctx->d_a64, (long long)nnz, d_part);
+      sumsq_final_kernel<<<1, 32, 0, ctx->stream>>>(d_part, np, d_part + np);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(&ctx->normA2, d_part + np, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(d_part);
+    }
     if (nranks > 1) {
       // ghost columns (host) and the buffers peers push into / read from
       for (int64_t i = 0; i < nnz; ++i)
@@ -897,6 +911,8 @@ void gmres_destroy(gmres_ctx* ctx) {
   cudaFree(ctx->d_ilu_bad);
   cudaFree(ctx->d_ilu_pub[0]);
   cudaFree(ctx->d_ilu_pub[1]);
+  cudaFree(ctx->d_ilu_s32[0]);
+  cudaFree(ctx->d_ilu_s32[1]);
   for (int t = 0; t < 2; ++t) {
     cudaFree(ctx->d_ilu_lev[t]);
     cudaFree(ctx->d_ilu_rows[t]);
@@ -1051,9 +1067,12 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16 && L != 32)
     return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 1/2/4/8/16/32");
   const int precond = opts ? opts->precond : GMRES_PRECOND_JACOBI;
-  if (precond != GMRES_PRECOND_JACOBI && precond != GMRES_PRECOND_ILU0)
-    return fail(ctx, GMRES_EINVAL, "precond must be 0 (Jacobi) or 1 (ILU(0))");
-  const bool ilu = precond == GMRES_PRECOND_ILU0;
+  if (precond != GMRES_PRECOND_JACOBI && precond != GMRES_PRECOND_ILU0 && precond != GMRES_PRECOND_ILU0_FP32)
+    return fail(ctx, GMRES_EINVAL, "precond must be 0 (Jacobi), 1 (ILU(0)) or 2 (fp32 ILU(0), fp64 solver)");
+  if (precond == GMRES_PRECOND_ILU0_FP32 && precision != GMRES_FP64)
+    return fail(ctx, GMRES_EINVAL, "precond 2 (fp32 ILU(0)) needs precision GMRES_FP64");
+  const bool ilu = precond != GMRES_PRECOND_JACOBI;
+  const bool ilu32 = precond == GMRES_PRECOND_ILU0_FP32;
   if (ilu && (virt || ctx->dist())) return fail(ctx, GMRES_EINVAL, "ILU(0) needs a single-rank context");
   if (ilu && policy == 3) return fail(ctx, GMRES_EINVAL, "restart_policy 3 is not available with ILU(0)");
   if ((virt || policy == 3 || ilu) && L != 1) L = 4;
@@ -1117,8 +1136,19 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
     if (int rc = launch_cast(ctx, st, ctx->d_flags + 1)) return rc;
     ctx->a32_ready = false;  // validated only by a completed solve
   }
+  if (ilu32) {  // fp32 factors of RN32(A) for the fp64 solver: the A32 copy first (its range check included)
+    if (int rc = launch_cast(ctx, st, ctx->d_flags + 1)) return rc;
+    ctx->a32_ready = false;
+    for (int t = 0; t < 2; ++t)
+      if (!ctx->d_ilu_s32[t]) CK(cudaMalloc(&ctx->d_ilu_s32[t], sizeof(float) * ctx->nvec));
+  }
   if (ilu)  // ILU(0) factorisation, inside the timed solve
-    if (int rc = ilu_factor(ctx, precision, st)) return rc;
+    if (int rc = ilu_factor(ctx, ilu32 ? GMRES_MIXED : precision, st)) return rc;
+  if (ilu32 && !ctx->d_ones[GMRES_FP64]) {  // the fp64 epilogues' unit Jacobi scale
+    CK(cudaMalloc(&ctx->d_ones[GMRES_FP64], sizeof(double) * ctx->nvec));
+    std::vector<double> one(ctx->nvec, 1.0);
+    CK(cudaMemcpy(ctx->d_ones[GMRES_FP64], one.data(), sizeof(double) * ctx->nvec, cudaMemcpyHostToDevice));
+  }
   double* xin = ctx->dist() ? ctx->d_gx + ctx->row_begin : d_x;  // the kernel's x (local view)
   if (d_x0 && d_x0 != xin) CK(cudaMemcpyAsync(xin, d_x0, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, st));
   if (!d_x0) CK(cudaMemsetAsync(xin, 0, sizeof(double) * ctx->n, st));
@@ -1146,8 +1176,11 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   d.mgs_nbuf = mgs_nbuf;
   d.mgs_wsm = mgs_wsm;
   if (ilu) {  // M = LU: the SpMV/residual epilogues scale by one, the kernel applies U⁻¹L⁻¹
-    set_ilu_dev(ctx, d, precision);
+    set_ilu_dev(ctx, d, ilu32 ? GMRES_MIXED : precision);
     d.dinvW = ctx->d_ones[precision];
+    d.ilu32 = ilu32 ? 1 : 0;
+    d.ilu_s32[0] = ctx->d_ilu_s32[0];
+    d.ilu_s32[1] = ctx->d_ilu_s32[1];
   }
   set_vlayout(d, vl);
   d.tune = opts ? opts->tune : 0;
@@ -1225,6 +1258,7 @@ int finish_solve(gmres_ctx* ctx, const Plan& P, float ms, float kms, gmres_resul
   r.inner_iters = oi[2];
   r.history_len = oi[3];
   r.final_relres = od[0];
+  r.final_backward_err = od[1];
   r.device_ms = ms;
   for (int i = 0; i < PH_N; ++i) ctx->phase_ns[i] = (double)prof[i];
   if (P.d.profile) {  // per-CTA own SpMV time: [5] max, [6] mean
@@ -1823,7 +1857,7 @@ int gmres_ilu0_factor(gmres_ctx* ctx, int32_t precision, void* d_f) {
   return 0;
 }
 
-int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* d_out) {
+int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* d_out, int32_t schedule) {
   if (!ctx || !d_z || !d_out) return fail(ctx, GMRES_EINVAL, "null argument");
   if (int rc = check_prec(ctx, precision)) return rc;
   if (!ctx->ilu_ready[precision]) return fail(ctx, GMRES_EINVAL, "no ILU(0) factors of this precision: call gmres_ilu0_factor");
@@ -1836,6 +1870,7 @@ int gmres_k_ilu_apply(gmres_ctx* ctx, int32_t precision, const void* d_z, void* 
   set_ilu_dev(ctx, d, precision);
   for (int t = 0; t < 2; ++t)
     CK(cudaMemsetAsync(ctx->d_ilu_pub[t], 0xff, sizeof(double) * ctx->n, ctx->stream));
+  d.tune = schedule & 65536;
   void* args[] = {&d, (void*)&d_z, &d_out};
   if (int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream)) return rc;
   CK(cudaStreamSynchronize(ctx->stream));

@@ -171,6 +171,9 @@ struct Dev {
   const int* ilu_eidx[2];
   const void* ilu_rec[2];  // packed per-slot records (IluRec<W>), rebuilt after each factorisation
   void* ilu_pub[2];        // [n] W each, sync-free solves: published row values (all-ones NaN = not yet)
+  double normA2;           // ‖A‖_F² of this rank's rows (backward-error report)
+  int ilu32;               // fp64 solver with fp32 factors: iluW / ilu_rec are fp32
+  float* ilu_s32[2];       // ... and its fp32 scratch vectors (right-hand side, solution)
 };
 
 // ------------------------------------------------------------ primitives
@@ -1033,16 +1036,17 @@ __device__ __forceinline__ void csr_any_stream(const Dev& d, Shm& sh, char* s_st
 // r = RN_W(dinv_W · RN_W(z)) (reading R10).  fp64 row sums.
 template <class W, int L>
 __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict__ r_out, double& zz, double& rr,
-                            double& bb, int& err) {
+                            double& bb, double& xx, int& err) {
   const W* dinv = (const W*)d.dinvW;
   const double* __restrict__ xg = d.x - d.row_base;  // global-index view (CSR columns are global)
   struct P2 { double b; W di; };
   const unsigned long long pol_g = policy_evict_last();
   auto gat = [&](int col) -> double { return ld_pol(xg + col, pol_g); };
   auto pre = [&](int row, W di) -> P2 { return P2{d.b[row], di}; };
-  auto epi = [&](int row, double acc, P2 pv, double) {
+  auto epi = [&](int row, double acc, P2 pv, double xd) {  // xd: x at the diagonal column = x_row
     const double bi = pv.b;
     bb += bi * bi;
+    xx += xd * xd;  // ‖x‖² for the normwise backward error (report only, reading R5)
     const double z = bi - acc;
     if (!isfinite(z)) err |= ERRF_NONFINITE;
     zz += z * z;
@@ -1330,6 +1334,28 @@ __device__ __noinline__ bool ilu_apply_phase(const Dev& d, Shm& sh, const W* in,
   }
   if (!ilu_solve<W, 0>(d, sh, in, out)) return false;  // L y = in (unit lower), level-synchronous
   return ilu_solve<W, 1>(d, sh, out, out);              // U out = y
+}
+
+// fp32 ILU(0) inside the fp64 solver (the paper's single-precision
+// ILU arm; oracle F_ILU32): out = (double) U32⁻¹ L32⁻¹ RN32(in), the fp32 solves
+// on scratch vectors (in == out allowed).
+static __device__ __noinline__ bool ilu_apply_f32(const Dev& d, Shm& sh, const double* in, double* out) {
+  float* a = d.ilu_s32[0];
+  float* b = d.ilu_s32[1];
+  const int gt = sh.cta * NT + threadIdx.x, gs = d.G * NT;
+  for (int i = gt; i < d.n; i += gs) a[i] = __double2float_rn(__ldcg(in + i));
+  if (!grid_sync(d, sh)) return false;  // the solves read any row of the right-hand side
+  if (!ilu_apply_phase<float>(d, sh, a, b, 0u)) return false;
+  for (int i = gt; i < d.n; i += gs) out[i] = (double)__ldcg(b + i);
+  fence_proxy_async_global();  // the next phase may stage `out` with bulk copies
+  return grid_sync(d, sh);      // later phases read rows by CTA partition
+}
+template <class W>
+__device__ __forceinline__ bool ilu_apply_any(const Dev& d, Shm& sh, const W* in, W* out, unsigned seq) {
+  if constexpr (sizeof(W) == 8) {
+    if (d.ilu32) return ilu_apply_f32(d, sh, in, out);
+  }
+  return ilu_apply_phase<W>(d, sh, in, out, seq);
 }
 
 // ------------------------------------------------------------------ a3
@@ -2287,9 +2313,10 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   }
   for (; status == ST_OK;) {
     // ---------------- residual, stop test (Alg. 1 lines 86–92)
-    double v3[3] = {0.0, 0.0, 0.0};
+    // ‖z‖², ‖r‖², ‖b‖², ‖x‖² and (CTA 0 of each rank) this rank's ‖A‖_F²
+    double v3[5] = {0.0, 0.0, 0.0, 0.0, cta == 0 && threadIdx.x == 0 ? d.normA2 : 0.0};
     int err = 0;
-    resid_phase<W, L>(d, sh, s_tiles, wb0, v3[0], v3[1], v3[2], err);
+    resid_phase<W, L>(d, sh, s_tiles, wb0, v3[0], v3[1], v3[2], v3[3], err);
     if (err) atomicOr(d.err_flag, err);
     __syncthreads();
     // error indicators of every rank travel inside the sums, so all ranks stop
@@ -2301,13 +2328,13 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       if (f & ERRF_RANGE) v3[1] = __longlong_as_double(0x7ff0000000000000ll);
     }
     halo_push(d, sh, (const W*)wb0, 0);
-    block_sum<3>(v3, sh, s_part);
-    if (!grid_allreduce(d, sh, s_part, 3, s_out, s_tmp)) { status = ST_ETIMEOUT; break; }
+    block_sum<5>(v3, sh, s_part);
+    if (!grid_allreduce(d, sh, s_part, 5, s_out, s_tmp)) { status = ST_ETIMEOUT; break; }
     const double ZZ = s_out[0], RR = s_out[1], nb = sqrt(s_out[2]);
     const int ef = *(volatile int*)d.err_flag;  // (other ranks' errors arrive as NaN/Inf in ZZ/RR)
     if (nb == 0.0) {  // b = 0 → x = 0, no cycle (reading R13)
       for (int i = r0 + threadIdx.x; i < min(r1, d.n); i += NT) d.x[i] = 0.0;
-      if (lead) { if (d.hist_cap > 0) d.history[0] = 0.0; d.out_int[3] = 1; d.out_dbl[0] = 0.0; }
+      if (lead) { if (d.hist_cap > 0) d.history[0] = 0.0; d.out_int[3] = 1; d.out_dbl[0] = 0.0; d.out_dbl[1] = 0.0; }
       status = ST_OK;
       break;
     }
@@ -2316,6 +2343,8 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       if (k < d.hist_cap) d.history[k] = rho;
       d.out_int[3] = k + 1;
       d.out_dbl[0] = rho;
+      // normwise backward error ‖b − Ax‖/(‖A‖_F‖x‖ + ‖b‖) of this iterate (report only)
+      d.out_dbl[1] = sqrt(ZZ) / (sqrt(s_out[4]) * sqrt(s_out[3]) + nb);
     }
     tick(PH_RESID);
     if (ef & ERRF_NONFINITE || !isfinite(ZZ) || !isfinite(nb)) { status = ST_ENONFINITE; break; }
@@ -2324,7 +2353,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (k >= d.max_cycles) { status = ST_NOT_CONVERGED; break; }
     double RRp = RR;
     if constexpr (PC) {  // line 90 with M = LU (reading R24): r = U⁻¹L⁻¹ RN_W(z), then ‖r‖²
-      if (!ilu_apply_phase<W>(d, sh, wb0, wb0, ilu_seq++)) { status = ST_ETIMEOUT; break; }
+      if (!ilu_apply_any<W>(d, sh, wb0, wb0, ilu_seq++)) { status = ST_ETIMEOUT; break; }
       double p = 0.0;
       for (int i = r0 + threadIdx.x; i < min(r1, d.n); i += NT) {
         const double v = (double)__ldcg(wb0 + i);
@@ -2355,7 +2384,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       const unsigned long long ts0 = d.profile && threadIdx.x == 0 ? globaltimer() : 0ull;
       spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V, j - 1);
       if constexpr (PC) {  // w = U⁻¹L⁻¹(A_W v_j) (line 100 with M = LU)
-        if (!grid_sync(d, sh) || !ilu_apply_phase<W>(d, sh, dst, dst, ilu_seq++)) { fail = true; break; }
+        if (!grid_sync(d, sh) || !ilu_apply_any<W>(d, sh, dst, dst, ilu_seq++)) { fail = true; break; }
       }
       if (d.profile) {
         if (threadIdx.x == 0) d.prof_cta[cta] += globaltimer() - ts0;
@@ -2460,6 +2489,31 @@ __global__ void unpack_basis_kernel(const W* __restrict__ V, long long ldv, int 
 }
 
 #ifdef G200_HOST_TU
+// ‖A‖_F² in a fixed order: block g sums its contiguous slice (warp trees, warps
+// in order), then one block sums the partials in order (sumsq_final_kernel)
+__global__ void sumsq_partial_kernel(const double* __restrict__ a, long long cnt, double* part) {
+  const long long per = (cnt + gridDim.x - 1) / gridDim.x;
+  const long long e0 = blockIdx.x * per, e1 = min(cnt, e0 + per);
+  double s = 0.0;
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) s += a[e] * a[e];
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void sumsq_final_kernel(const double* part, int np, double* out) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int g = 0; g < np; ++g) t += part[g];
+    *out = t;
+  }
+}
+
 // Jacobi M = diag(A) (reading R11): dinv64 = 1/a_ii (fp64), dinv32 = RN32(dinv64).
 __global__ void dinv_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                             const double* __restrict__ a, double* dinv64, float* dinv32, int* bad_row,
@@ -2498,9 +2552,9 @@ __global__ void __launch_bounds__(NT, 1) k_ilu_apply_kernel(Dev d, const W* z, W
 template <class W, int L>
 __global__ void __launch_bounds__(NT, 1) k_resid_kernel(Dev d, W* r, double* out2) {
   G200_SMEM_CARVE(W)
-  double v3[3] = {0.0, 0.0, 0.0};
+  double v3[3] = {0.0, 0.0, 0.0}, xx = 0.0;
   int err = 0;
-  resid_phase<W, L>(d, sh, s_tiles, r, v3[0], v3[1], v3[2], err);
+  resid_phase<W, L>(d, sh, s_tiles, r, v3[0], v3[1], v3[2], xx, err);
   if (err) atomicOr(d.err_flag, err);
   block_sum<3>(v3, sh, s_part);
   if (!grid_allreduce(d, sh, s_part, 3, s_out, s_tmp)) return;

@@ -18,7 +18,7 @@ _LIB_PATH = os.path.join(_HERE, "libgmres.so")
 _lib = None
 
 MGS, CGSR = 0, 1
-JACOBI, ILU0 = 0, 1   # preconditioners (gmres_opts.precond)
+JACOBI, ILU0, ILU0_FP32 = 0, 1, 2   # preconditioners (gmres_opts.precond; ILU0_FP32: fp64 solver, fp32 ILU)
 THRESHOLD, TWOSTAGE, STALL, ORTHLOSS = 0, 1, 2, 3   # restart policies (gmres_opts.restart_policy)
 FP64, MIXED = 0, 1
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "EBADCSR", -3: "EZERODIAG", -4: "EFP32RANGE",
@@ -34,7 +34,7 @@ class GmresError(RuntimeError):
 class _Result(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("cycles", ctypes.c_int32), ("inner_iters", ctypes.c_int32),
                 ("history_len", ctypes.c_int32), ("final_relres", ctypes.c_double), ("device_ms", ctypes.c_double),
-                ("kernel_ms", ctypes.c_double)]
+                ("kernel_ms", ctypes.c_double), ("final_backward_err", ctypes.c_double)]
 
 
 class _Opts(ctypes.Structure):
@@ -73,7 +73,7 @@ def load_library():
     L.gmres_get_plan.argtypes = [vp, vp, i32]
     L.gmres_ilu0_factor.argtypes = [vp, i32, vp]
     L.gmres_ilu0_factor.restype = ctypes.c_int
-    L.gmres_k_ilu_apply.argtypes = [vp, i32, vp, vp]
+    L.gmres_k_ilu_apply.argtypes = [vp, i32, vp, vp, i32]
     L.gmres_k_ilu_apply.restype = ctypes.c_int
     L.gmres_ilu0_levels.argtypes = [vp, vp, vp]
     L.gmres_ilu0_levels.restype = ctypes.c_int
@@ -152,6 +152,7 @@ class SolveResult:
     inner: np.ndarray | None = None
     phase_ns: np.ndarray | None = None
     meta: dict = field(default_factory=dict)
+    final_backward_err: float = float("nan")
 
     @property
     def status_name(self) -> str:
@@ -261,11 +262,11 @@ class Solver:
         self._lib.gmres_get_cycle_iters(self._h, _p(cj), ln.value, ctypes.byref(ln))
         return SolveResult(res.status, res.cycles, res.inner_iters, res.final_relres, res.device_ms,
                            hist[:min(hl.value, hist.size)].copy(), kernel_ms=res.kernel_ms, cycle_iters=cj,
-                           inner=inner, phase_ns=ph)
+                           inner=inner, phase_ns=ph, final_backward_err=res.final_backward_err)
 
     def solve(self, b, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None, max_cycles=None,
               record_inner=False, lanes=0, ctas_per_sm=0, out=None, policy=THRESHOLD,
-              orth_thresh=0.0, precond=0) -> SolveResult:
+              orth_thresh=0.0, precond=0, tune=0) -> SolveResult:
         """gmres_solve: host arrays in, host x out (h2d/d2h inside the call).  `out` may be a
         preallocated (e.g. pinned) float64 array of length n."""
         b = np.ascontiguousarray(b, np.float64)
@@ -279,8 +280,8 @@ class Solver:
         hist = np.zeros(mc + 2)
         hl = ctypes.c_int32()
         res = _Result()
-        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, policy=policy, orth_thresh=orth_thresh,
-                       precond=precond)
+        o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, tune=tune, policy=policy,
+                       orth_thresh=orth_thresh, precond=precond)
         rc = self._lib.gmres_solve(self._h, _p(b), _p(x0c), _p(x), int(m), float(tol), _ortho(ortho),
                                    _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
                                    ctypes.byref(hl))
@@ -318,11 +319,12 @@ class Solver:
             raise self._err(rc)
         return f
 
-    def ilu_apply(self, z, precision):
-        """gmres_k_ilu_apply: U⁻¹L⁻¹ z with the last factors of this precision (torch tensors)."""
+    def ilu_apply(self, z, precision, tune=0):
+        """gmres_k_ilu_apply: U⁻¹L⁻¹ z with the last factors of this precision (torch tensors);
+        tune bit 16 (65536): the level-synchronous schedule instead of the sync-free one."""
         import torch
         out = torch.empty_like(z)
-        rc = self._lib.gmres_k_ilu_apply(self._h, _prec(precision), _p(z), _p(out))
+        rc = self._lib.gmres_k_ilu_apply(self._h, _prec(precision), _p(z), _p(out), int(tune))
         if rc < 0:
             raise self._err(rc)
         return out

@@ -64,12 +64,15 @@ def test_ilu0_factors_bit_exact(mat, prec):
 
 
 @pytest.mark.parametrize("prec", [G.FP64, G.MIXED])
-def test_ilu0_apply_bit_exact(mat, prec):
+@pytest.mark.parametrize("tune", [0, 65536], ids=["sync_free", "level_sync"])
+def test_ilu0_apply_bit_exact(mat, prec, tune):
+    """Both triangular-solve schedules — the sync-free default and the level-synchronous
+    fallback (tune bit 16) — reproduce the oracle's substitutions bit for bit."""
     _, A, S = mat
     S.ilu0_factor(prec)
     dt = np.float32 if prec == G.MIXED else np.float64
     z = np.random.default_rng(3).uniform(-1, 1, A.n).astype(dt)
-    y = S.ilu_apply(tdev(z), prec).cpu().numpy()
+    y = S.ilu_apply(tdev(z), prec, tune=tune).cpu().numpy()
     ref = O.ilu0_apply(prec, A, O.ilu0(prec, A), z)
     assert np.array_equal(y, ref)
 
@@ -118,6 +121,25 @@ def test_ilu_solve_end_to_end(prob, ortho, prec):
     assert np.allclose(res.inner[:j1], ref.inner[:j1], rtol=tol, atol=0)
 
 
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+def test_fp32_ilu_in_fp64_solver(prob, ortho):
+    """The paper's third arm: the fp64 solver with an fp32 ILU(0) of
+    RN32(A) applied as RN32(in) → fp32 substitutions → fp64 (oracle F_ILU32)."""
+    P, S = prob
+    m = min(P.m, 50)
+    res = S.solve(P.b, m=m, tol=1e-10, ortho=ortho, precision=G.FP64, record_inner=True, precond=G.ILU0_FP32)
+    ref = O.solve(P.A, P.b, m=m, tol=1e-10, ortho=ortho, prec=O.FP64, flags=O.F_ILU32)
+    assert res.status == 0, res.status_name
+    assert ref.status == O.OK
+    rel = check_solution(P.A, P.b, res.x)
+    assert rel <= 1e-10, rel
+    assert abs(res.cycles - ref.cycles) <= max(1, 0.1 * ref.cycles), (res.cycles, ref.cycles)
+    j1 = min(int(res.cycle_iters[0]), ref.inner.size, 10)
+    assert np.allclose(res.inner[:j1], ref.inner[:j1], rtol=1e-6, atol=0)
+    res2 = S.solve(P.b, m=m, tol=1e-10, ortho=ortho, precision=G.FP64, precond=G.ILU0_FP32, tune=65536)
+    assert res2.status == 0 and check_solution(P.A, P.b, res2.x) <= 1e-10   # level-synchronous schedule
+
+
 def test_ilu_solve_errors():
     P = inputs.make("C1", 8)
     S = G.Solver.from_csr(P.A)
@@ -125,6 +147,8 @@ def test_ilu_solve_errors():
         S.solve(P.b, precond=7)
     with pytest.raises(G.GmresError):
         S.solve(P.b, precond=G.ILU0, policy=G.ORTHLOSS)
+    with pytest.raises(G.GmresError, match="precision GMRES_FP64"):
+        S.solve(P.b, precond=G.ILU0_FP32, precision=G.MIXED)
     with pytest.raises(G.GmresError):                  # apply before any factorisation
         G.Solver.from_csr(P.A).ilu_apply(tdev(P.b), G.FP64)
     # zero pivot: u_22 = 1 − 1·1 = 0 (row 1); the solve reports it before any cycle

@@ -211,6 +211,8 @@ def test_solve_end_to_end(prob, ortho, prec):
     rel = check_solution(P.A, P.b, res.x)
     assert rel <= 1e-10, rel
     assert res.final_relres == pytest.approx(rel, rel=1e-3, abs=1e-13)
+    # normwise backward error of the returned x, recomputed by the oracle
+    assert res.final_backward_err == pytest.approx(O.backward_error(P.A, P.b, res.x), rel=1e-3)
     assert abs(res.cycles - ref.cycles) <= 0.1 * ref.cycles, (res.cycles, ref.cycles)
     # diagnostic: per-cycle history tracks the oracle's
     k = min(len(res.history), len(ref.history))
