@@ -494,3 +494,21 @@ def test_orthloss_policy_matches_oracle(thresh):
     J, Jo = list(r.cycle_iters), _cycle_lengths(ref.inner)
     assert abs(J[0] - Jo[0]) <= 2, (J, Jo)
     assert abs(r.cycles - ref.cycles) <= max(1, 0.1 * ref.cycles)
+
+
+# ------------------------------------------------------------------ f4: Table-1 analogue
+@pytest.mark.parametrize("name,scale,m", [("C2", 24, 150), ("C4", 16, 120)])
+def test_table1_stall_points_match_oracle(name, scale, m):
+    """Iterations before the Arnoldi residual stalls in the first three
+    forced-restart cycles of mixed MGS: device histories vs the oracle's, and the paper's
+    observation that the stall point repeats from cycle to cycle."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import table1
+    row = table1.run(name, scale, m)
+    g, o = row["stall_iters_gpu"], row["stall_iters_oracle"]
+    assert len(g) >= 2 and None not in g and None not in o, row
+    for a, b in zip(g, o):
+        assert abs(a - b) <= max(2, 0.2 * b), row      # ±20 % (SURVEY §8 f4)
+    assert max(g) - min(g) <= max(3, 0.2 * max(g)), row   # about the same after each restart
+
