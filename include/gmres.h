@@ -69,7 +69,9 @@ typedef struct {
                              448); < 0 → default: 1e-6 mixed, 0 fp64                    */
   int32_t max_cycles;     /* ≤ 0 → 10000                                                */
   int32_t record_inner;   /* != 0: keep |s_{j+1}|/β per inner step (gmres_get_inner_history) */
-  int32_t lanes_per_row;  /* SpMV sub-warp width 4/8/16/32; 0 = auto from mean row length */
+  int32_t lanes_per_row;  /* SpMV lanes per row 1/2/4/8/16/32; 0 = auto from the mean row
+                             length.  Virtual ranks, restart_policy 3 and ILU(0): 1 or 4
+                             only (EINVAL otherwise)                                  */
   int32_t ctas_per_sm;    /* 0 = auto (occupancy)                                       */
   int32_t profile;        /* != 0: grid barrier after each phase for clean phase timers */
   int32_t tune;           /* developer A/B switches; 0 = production defaults            */
@@ -79,7 +81,7 @@ typedef struct {
                              251-255, 448); 2 STALL: THRESHOLD plus a restart when |s| improved
                              by less than stall_factor over the last ⌈stall_frac·m⌉ inner
                              iterations (δ defaults to 0)          */
-  double stall_factor;    /* ≤ 0 → 1.001                                */
+  double stall_factor;    /* ≤ 0 → 1.001; else must be > 1 (EINVAL)      */
   double stall_frac;      /* ≤ 0 → 0.05                                */
   double orth_thresh;     /* restart_policy 3 ORTHLOSS: THRESHOLD plus a restart when
                              ‖S_k‖_F ≥ orth_thresh, S_k = (I+U_k)⁻¹U_k, U_k = strict upper
@@ -271,18 +273,6 @@ int gmres_ilu0_levels(gmres_ctx* ctx, int32_t* nlev_lower, int32_t* nlev_upper);
 /* a0: build the fp32 copy of A on the device (also rebuilt
  * inside every mixed solve, timed).  EFP32RANGE on overflow. */
 int gmres_k_cast32(gmres_ctx* ctx);
-
-/* Developer microbenchmark (not part of the solve): `iters` repetitions of a
- * building block inside one cooperative launch on the solve grid; what = 0
- * grid barrier, 1 one-value all-reduce, 2 MGS sweep, 3/4/5 CGS tile passes
- * over ncols columns of d_V (ld ldv) and d_w (padded to ldv, zero padding).
- * *ns = elapsed device ns. */
-int gmres_k_micro(gmres_ctx* ctx, int32_t precision, int32_t what, int32_t iters, int32_t ncols, const void* d_V,
-                  int64_t ldv, void* d_w, double* ns);
-
-/* Device pointers of the context's matrix (for tests): any may be NULL. */
-int gmres_k_matrix(gmres_ctx* ctx, const int32_t** row_ptr, const int32_t** col, const double** val64,
-                   const float** val32, const double** dinv64);
 
 #ifdef __cplusplus
 }

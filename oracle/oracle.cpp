@@ -667,7 +667,8 @@ extern "C" int oracle_gmres_solve_orth(int64_t n, const int32_t* rp, const int32
                                        double* history, int32_t history_cap, double* inner, int32_t inner_cap,
                                        int policy, double stall_factor, double stall_frac, int orth_kind,
                                        double orth_thresh, double* orth_hist, int32_t orth_cap) {
-  if (policy < 0 || policy > 3 || !(stall_factor >= 1.0) || !(stall_frac > 0.0)) return ORACLE_EINVAL;
+  // StallDetect's factor must exceed 1 (1.001): with 1 the stall test never fires
+  if (policy < 0 || policy > 3 || !(stall_factor > 1.0) || !(stall_frac > 0.0)) return ORACLE_EINVAL;
   if (orth_kind < 0 || orth_kind > 1 || !(orth_thresh > 0.0)) return ORACLE_EINVAL;
   if (n < 1 || m < 1 || !(tol > 0.0) || !(delta >= 0.0) || max_cycles < 0) return ORACLE_EINVAL;
   if (rp[0] != 0) return ORACLE_EBADCSR;

@@ -128,6 +128,7 @@ struct gmres_ctx {
   int red_base = 0;
   bool linked = false, ipc = false;
   double normA2 = 0.0;                  // ‖A‖_F² of this context's rows (device-computed at create)
+  unsigned halo_full = 0;               // peers that receive whole row blocks (bit q)
   void* peer_w0[MAXR] = {}, *peer_w1[MAXR] = {};
   double* peer_x[MAXR] = {};
   double* peer_slots[MAXR] = {};
@@ -416,9 +417,16 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
     if (e != cudaSuccess) return bail(e);
   }
   if (ctx->dist() && ctx->linked) {  // per-CTA send lists (halo push)
+    // a peer that gathers at least half of this rank's rows (random-column matrices:
+    // ghosts ≈ every remote row) receives whole contiguous row blocks
+    // (an all-gather of the vector) instead of per-element pushes
+    ctx->halo_full = 0;
+    for (int q = 0; q < ctx->nranks; ++q)
+      if (q != ctx->rank && 2 * (int64_t)ctx->send_rows[q].size() >= ctx->n) ctx->halo_full |= 1u << q;
     std::vector<std::pair<int, int>> se;  // (local row, peer)
     for (int q = 0; q < ctx->nranks; ++q)
-      for (int32_t r : ctx->send_rows[q]) se.push_back({r, q});
+      if (!((ctx->halo_full >> q) & 1u))
+        for (int32_t r : ctx->send_rows[q]) se.push_back({r, q});
     std::sort(se.begin(), se.end());
     std::vector<int> buf(G + 1 + 2 * se.size());
     // offsets: CTA g pushes the entries with rb[g] <= row < rb[g+1]
@@ -1059,8 +1067,10 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   if (!std::isfinite(delta)) return fail(ctx, GMRES_EINVAL, "delta must be finite");
   const double stall_factor = (opts && opts->stall_factor > 0.0) ? opts->stall_factor : 1.001;
   const double stall_frac = (opts && opts->stall_frac > 0.0) ? opts->stall_frac : 0.05;
-  if (!(stall_factor >= 1.0) || !std::isfinite(stall_factor) || !(stall_frac <= 1.0))
-    return fail(ctx, GMRES_EINVAL, "stall_factor must be >= 1 and stall_frac in (0, 1]");
+  // f > 1: with f = 1 the stall test |s_{j+1}|·f > |s_{j+1−w}| can never fire (the Arnoldi
+  // residual does not increase) — StallDetect's factor
+  if (!(stall_factor > 1.0) || !std::isfinite(stall_factor) || !(stall_frac <= 1.0))
+    return fail(ctx, GMRES_EINVAL, "stall_factor must be > 1 and stall_frac in (0, 1]");
   const int max_cycles = (opts && opts->max_cycles > 0) ? opts->max_cycles : 10000;
   P.rec_inner = opts && opts->record_inner;
   int L = (opts && opts->lanes_per_row) ? opts->lanes_per_row : auto_lanes(ctx->n, ctx->nnz);
@@ -1075,7 +1085,12 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   const bool ilu32 = precond == GMRES_PRECOND_ILU0_FP32;
   if (ilu && (virt || ctx->dist())) return fail(ctx, GMRES_EINVAL, "ILU(0) needs a single-rank context");
   if (ilu && policy == 3) return fail(ctx, GMRES_EINVAL, "restart_policy 3 is not available with ILU(0)");
-  if ((virt || policy == 3 || ilu) && L != 1) L = 4;
+  // virtual ranks, the monitor and ILU kernels exist for 1 and 4 lanes per row only
+  if ((virt || policy == 3 || ilu) && L != 1 && L != 4) {
+    if (opts && opts->lanes_per_row)
+      return fail(ctx, GMRES_EINVAL, "lanes_per_row must be 1 or 4 with virtual ranks, restart_policy 3 or ILU(0)");
+    L = 4;
+  }
   P.st = stream ? (cudaStream_t)stream : ctx->stream;
   P.prec = precision;
   const cudaStream_t st = P.st;
@@ -1131,6 +1146,11 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   } else if (int rc = reset_flags(ctx, st)) {
     return rc;
   }
+  // a0, preconditioner construction inside the timed solve: the Jacobi
+  // diagonal (validated at create; rebuilt here — ~30 µs on C2)
+  dinv_kernel<<<ctx->sms * 8, 256, 0, st>>>((int)ctx->n, ctx->d_rp, ctx->d_ci, ctx->d_a64, ctx->d_dinv64,
+                                            ctx->d_dinv32, ctx->d_flags + 2, (long long)ctx->row_begin);
+  CK(cudaGetLastError());
   if (precision == GMRES_MIXED) {  // a0: rebuilt inside every timed solve;
     // overflow is flagged on the device and reported by the solve kernel
     if (int rc = launch_cast(ctx, st, ctx->d_flags + 1)) return rc;
@@ -1200,7 +1220,10 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
       d.vec_peer[1][q] = q < ctx->nranks ? ctx->peer_w1[q] : nullptr;
       d.vec_peer[2][q] = q < ctx->nranks ? (void*)ctx->peer_x[q] : nullptr;
     }
-    d.sys_scope = ctx->ipc ? 1 : 0;
+    // system-scope release/acquire between GPUs; tune bit 21 forces it for in-process
+    // (virtual) ranks so the single-GPU tests execute the multi-GPU memory-order path
+    d.sys_scope = (ctx->ipc || (opts && (opts->tune & 2097152))) ? 1 : 0;
+    d.halo_full = ctx->halo_full;
     d.row_base = ctx->row_begin;
     d.halo = 1;
     d.w0 = (char*)ctx->d_gw0 + wb * ctx->row_begin;
@@ -1593,17 +1616,6 @@ int gmres_k_cast32(gmres_ctx* ctx) {
   return ensure_a32(ctx, ctx->stream);
 }
 
-int gmres_k_matrix(gmres_ctx* ctx, const int32_t** row_ptr, const int32_t** col, const double** val64,
-                   const float** val32, const double** dinv64) {
-  if (!ctx) return fail(nullptr, GMRES_EINVAL, "ctx is NULL");
-  if (row_ptr) *row_ptr = ctx->d_rp;
-  if (col) *col = ctx->d_ci;
-  if (val64) *val64 = ctx->d_a64;
-  if (val32) *val32 = ctx->a32_ready ? ctx->d_a32 : nullptr;
-  if (dinv64) *dinv64 = ctx->d_dinv64;
-  return 0;
-}
-
 namespace {
 // common prologue of the component entry points: kernels, grid, partition, workspace
 int comp_setup(gmres_ctx* ctx, int prec, int m_req, int kind, int L, const void** kern, int* G, size_t* smem,
@@ -1782,39 +1794,6 @@ int gmres_k_xupdate(gmres_ctx* ctx, int32_t precision, int32_t J, const void* d_
   cudaFree(d_y);
   if (e != cudaSuccess) return fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
   return 0;
-}
-
-int gmres_k_micro(gmres_ctx* ctx, int32_t precision, int32_t what, int32_t iters, int32_t ncols, const void* d_V,
-                  int64_t ldv, void* d_w, double* ns) {
-  if (!ctx || !d_V || !d_w || !ns) return fail(ctx, GMRES_EINVAL, "null argument");
-  const int L = auto_lanes(ctx->n, ctx->nnz);
-  const void* kern0;
-  int G;
-  size_t smem;
-  int m;
-  if (int rc = comp_setup(ctx, precision, std::max(ncols, 1), 2, L, &kern0, &G, &smem, &m)) return rc;
-  const void* kern = pick_kernel(precision, 5, 1);
-  int Gk = 0;
-  if (int rc = grid_for(ctx, kern, smem, 0, &Gk)) return rc;
-  if (Gk < G) return fail(ctx, GMRES_ECUDA, "micro kernel occupancy below the solve grid");
-  Dev d = make_dev(ctx, m, precision, 0, G);
-  d.tune = what >> 8;
-  what &= 0xff;
-  unsigned long long* d_ns = nullptr;
-  CK(cudaMalloc(&d_ns, 16));
-  CK(cudaMemset(d_ns, 0, 16));
-  long long ld = ldv;
-  void* args[] = {&d, &what, &iters, &ncols, (void*)&d_V, &ld, &d_w, &d_ns};
-  int rc = launch_coop(ctx, kern, G, smem, args, ctx->stream);
-  unsigned long long h[2] = {0, 0};
-  if (rc == 0) {
-    cudaError_t e = cudaMemcpyAsync(h, d_ns, 16, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) rc = fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
-  }
-  cudaFree(d_ns);
-  *ns = (double)h[0];
-  return rc;
 }
 
 int gmres_k_hessenberg(gmres_ctx* ctx, int32_t m, int32_t J, const double* Hbar, double beta, double* R, double* s,

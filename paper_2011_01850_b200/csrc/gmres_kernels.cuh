@@ -114,6 +114,7 @@ struct Dev {
   // w1, x) by the CTA owning them, before the release of the next all-reduce.
   long long row_base;
   int halo;             // != 0: push halo rows (nranks > 1)
+  unsigned halo_full;   // bit q: rank q receives this rank's whole row blocks (contiguous pushes)
   // barrier epochs / all-reduce count at launch (row-partitioned solves keep
   // the arrival counters monotonic across launches instead of resetting them,
   // so no rank can wipe a faster rank's arrival); final values → epoch_out
@@ -625,6 +626,14 @@ __device__ __forceinline__ void halo_push(const Dev& d, const Shm& sh, const T* 
     const int row = d.send_row[e];
     T* pb = reinterpret_cast<T*>(d.vec_peer[which][d.send_peer[e]]);
     pb[d.row_base + row] = loc[row];
+  }
+  if (d.halo_full) {  // whole row block of this CTA, coalesced, to the peers that gather most rows
+    const int r0 = d.row_begin[sh.cta], r1 = min(d.row_begin[sh.cta + 1], d.n);
+    for (int q = 0; q < d.nranks; ++q) {
+      if (!((d.halo_full >> q) & 1u)) continue;
+      T* pb = reinterpret_cast<T*>(d.vec_peer[which][q]) + d.row_base;
+      for (int r = r0 + threadIdx.x; r < r1; r += NT) pb[r] = loc[r];
+    }
   }
 }
 template <class W>
@@ -2582,57 +2591,6 @@ __global__ void __launch_bounds__(NT, 1) k_xupdate_kernel(Dev d, int J, const W*
   const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
   double dummy = 0.0;
   rowtile_pass<W, 4>(d, sh, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
-}
-
-// Device microbenchmark of the solve's building blocks (dev tool): `iters`
-// repetitions of what = 0 grid barrier, 1 one-value grid all-reduce, 2 MGS
-// sweep (no reduction), 3 CGS tile pass MODE 1 over ncols columns, 4 tile
-// pass MODE 2, 5 tile pass MODE 3.  out_ns = CTA 0's %globaltimer span.
-template <class W>
-__global__ void __launch_bounds__(NT, 1) k_micro_kernel(Dev d, int what, int iters, int ncols, const W* V,
-                                                      long long ldv, W* w, unsigned long long* out_ns) {
-  G200_SMEM_CARVE(W)
-  const int r0 = d.row_begin[blockIdx.x], r1 = d.row_begin[blockIdx.x + 1];
-  for (int i = threadIdx.x; i < ncols; i += NT) { s_part[i] = 0.0; s_coefW[i] = (W)1e-3; }
-  for (int i = threadIdx.x; i < NW * d.kmax; i += NT) s_tmp[i] = 0.0;
-  if (!grid_sync(d, sh)) return;
-  const unsigned long long t0 = globaltimer();
-  double acc = 0.0;
-  for (int it = 0; it < iters; ++it) {
-    if (what == 0) {
-      if (!grid_sync(d, sh)) return;
-    } else if (what == 1) {
-      double h;
-      if (!allreduce1(d, sh, threadIdx.x == 0 ? 1.0 : 0.0, false, h)) return;
-      acc += h;
-    } else if (what == 2) {
-      acc += mgs_sweep<W>(r0, r1, w, V, (W)1e-3, V + ldv);
-      __syncthreads();
-    } else if (what == 6) {  // CSR stream without gathers (TMA streaming + epilogue)
-      const W* dinv = (const W*)d.dinvW;
-      auto gat = [&](int) -> W { return (W)1; };
-      auto pre = [&](int, W di) -> W { return di; };
-      auto epi = [&](int row, W a, W di, W) { w[row] = mulw(di, a); };
-      csr_any_stream<W, 1>(d, sh, s_tiles, (const W*)d.aW, dinv, gat, pre, epi);
-    } else if (what == 7) {  // full SpMV phase (gathers from V column 0), L = 1
-      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, (W*)nullptr, 0);
-    } else if (what == 8) {  // ... plus the fused V-column write (as in the solve)
-      spmv_phase<W, 1>(d, sh, s_tiles, V, 1.0, w, const_cast<W*>(V), 2);
-    } else if (what == 3) {
-      rowtile_pass<W, 1>(d, sh, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
-      __syncthreads();
-    } else if (what == 4) {
-      rowtile_pass<W, 2>(d, sh, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
-      __syncthreads();
-    } else {
-      rowtile_pass<W, 3>(d, sh, r0, r1, V, ldv, ncols, w, s_coefW, s_y, s_tmp, s_tiles, acc);
-      __syncthreads();
-    }
-  }
-  if (!grid_sync(d, sh)) return;
-  const unsigned long long t1 = globaltimer();
-  if (blockIdx.x == 0 && threadIdx.x == 0) out_ns[0] = t1 - t0;
-  if (acc == 12345.678) out_ns[1] = 1;  // keep the work alive
 }
 
 #ifdef G200_HOST_TU

@@ -27,7 +27,6 @@ void* ktab_comp_f32(int kind, int L) {
     case 6: return (void*)&k_ortho_kernel<float, 1>;  // chunk-ring MGS
     case 7: return (void*)&k_ortho_kernel<float, 2>;  // streamed MGS
     case 4: return (void*)&k_ilu_apply_kernel<float>;
-    case 5: return (void*)&k_micro_kernel<float>;
     default: return (void*)&k_xupdate_kernel<float>;
   }
 }

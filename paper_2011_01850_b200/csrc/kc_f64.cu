@@ -27,7 +27,6 @@ void* ktab_comp_f64(int kind, int L) {
     case 6: return (void*)&k_ortho_kernel<double, 1>;  // chunk-ring MGS
     case 7: return (void*)&k_ortho_kernel<double, 2>;  // streamed MGS
     case 4: return (void*)&k_ilu_apply_kernel<double>;
-    case 5: return (void*)&k_micro_kernel<double>;
     default: return (void*)&k_xupdate_kernel<double>;
   }
 }

@@ -15,7 +15,7 @@ void* ktab_solve_f64_hi(int L);
 void* ktab_solve_f32_ext(int variant, int L);
 void* ktab_solve_f64_ext(int variant, int L);
 // component kernels: kind 0 spmv, 1 resid, 2 ortho (resident MGS / sweep / CGSR), 3 xupdate, 4 ilu apply,
-// 5 micro, 6 ortho with the chunk-ring MGS, 7 ortho with the streamed MGS
+// 6 ortho with the chunk-ring MGS, 7 ortho with the streamed MGS
 void* ktab_comp_f32(int kind, int L);
 void* ktab_comp_f64(int kind, int L);
 }  // namespace g200

@@ -92,10 +92,8 @@ def load_library():
     L.gmres_k_xupdate.argtypes = [vp, i32, i32, vp, i64, vp, vp, i32]
     L.gmres_k_hessenberg.argtypes = [vp, i32, i32, vp, dbl, vp, vp, vp]
     L.gmres_k_cast32.argtypes = [vp]
-    L.gmres_k_micro.argtypes = [vp, i32, i32, i32, i32, vp, i64, vp, vp]
-    L.gmres_k_matrix.argtypes = [vp, vp, vp, vp, vp, vp]
     for f in ("gmres_k_spmv", "gmres_k_resid", "gmres_k_ortho", "gmres_k_ortho_ex", "gmres_k_xupdate", "gmres_k_hessenberg",
-              "gmres_k_cast32", "gmres_k_matrix", "gmres_k_micro"):
+              "gmres_k_cast32"):
         getattr(L, f).restype = ctypes.c_int
     p64 = ctypes.POINTER(i64)
     L.gmres_dist_partition.argtypes = [vp, i64, i32, i64, vp]
@@ -266,7 +264,7 @@ class Solver:
 
     def solve(self, b, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None, max_cycles=None,
               record_inner=False, lanes=0, ctas_per_sm=0, out=None, policy=THRESHOLD,
-              orth_thresh=0.0, precond=0, tune=0) -> SolveResult:
+              orth_thresh=0.0, precond=0, tune=0, stall_factor=0.0) -> SolveResult:
         """gmres_solve: host arrays in, host x out (h2d/d2h inside the call).  `out` may be a
         preallocated (e.g. pinned) float64 array of length n."""
         b = np.ascontiguousarray(b, np.float64)
@@ -281,7 +279,7 @@ class Solver:
         hl = ctypes.c_int32()
         res = _Result()
         o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, tune=tune, policy=policy,
-                       orth_thresh=orth_thresh, precond=precond)
+                       orth_thresh=orth_thresh, precond=precond, stall_factor=stall_factor)
         rc = self._lib.gmres_solve(self._h, _p(b), _p(x0c), _p(x), int(m), float(tol), _ortho(ortho),
                                    _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
                                    ctypes.byref(hl))
@@ -384,12 +382,6 @@ class Solver:
         y = np.ascontiguousarray(y, np.float64)
         self._ck(self._lib.gmres_k_xupdate(self._h, _prec(precision), int(J), _p(V), int(ldv), _p(y), _p(x),
                                            int(bool(blocked))))
-
-    def k_micro(self, precision, what, iters, ncols, V, ldv, w):
-        ns = np.zeros(1)
-        self._ck(self._lib.gmres_k_micro(self._h, _prec(precision), int(what), int(iters), int(ncols), _p(V),
-                                         int(ldv), _p(w), _p(ns)))
-        return float(ns[0])
 
     def k_hessenberg(self, m, J, Hbar, beta):
         Hc = np.asfortranarray(Hbar, np.float64)  # (m+1, m) column-major

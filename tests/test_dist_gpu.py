@@ -69,6 +69,23 @@ def test_virtual_ranks_solve(name, nranks, ortho, prec):
     assert res[0].final_relres == pytest.approx(rel, rel=1e-3, abs=1e-13)
 
 
+@pytest.mark.parametrize("name", ["C2mini", "C3mini"])
+@pytest.mark.parametrize("ortho", [G.MGS, G.CGSR])
+def test_virtual_ranks_system_scope(name, ortho):
+    """The multi-GPU memory-order path on one device: tune bit 21 forces the system-scope
+    release/acquire (red.release.sys / ld.acquire.sys) the IPC ranks use; same decisions and
+    the same x bit for bit as the GPU-scope run (only the ordering scope differs).  C3mini also
+    exercises the whole-row-block halo pushes (each rank gathers > half of the other's rows)."""
+    P = PROBS[name]()
+    kw = dict(m=40, tol=1e-10, ortho=ortho, precision=G.MIXED)
+    r_gpu, x_gpu, _ = dist_solve(P, 2, **kw)
+    r_sys, x_sys, _ = dist_solve(P, 2, tune=2097152, **kw)
+    assert all(r.status == 0 for r in r_sys)
+    assert [(r.cycles, r.inner_iters) for r in r_sys] == [(r.cycles, r.inner_iters) for r in r_gpu]
+    assert np.array_equal(x_sys, x_gpu)
+    assert np.linalg.norm(P.b - O.spmv64(P.A, x_sys)) / np.linalg.norm(P.b) <= 1e-10
+
+
 def test_virtual_ranks_match_single_rank():
     """Same matrix, 1 rank vs 2 ranks: same restart count and inner iterations (stencil, fp64)."""
     P = inputs.make("C2", 24)

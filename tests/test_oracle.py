@@ -342,6 +342,11 @@ def test_invalid_inputs():
         O.solve(bad, np.ones(2), m=2)
     with pytest.raises(OverflowError):
         O.cast32(np.array([1e39]))
+    # StallDetect's factor must exceed 1: with 1 the stall test can never fire
+    good = inputs.make("C1", 8)
+    with pytest.raises(RuntimeError):
+        O.solve(good.A, good.b, m=10, policy=O.STALL, stall_factor=1.0)
+    assert O.solve(good.A, good.b, m=10, policy=O.STALL, stall_factor=1.001).status == O.OK
 
 
 # ------------------------------------------------------ mixed-precision claims
