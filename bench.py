@@ -148,6 +148,60 @@ def oracle_sample(prob, budget_cycles=1):
                           f"(m={M}) on the full {WORKLOAD} matrix, oracle single-threaded, incl. its A32 cast")
 
 
+def golden_tts(cfg, m, variants=None):
+    """The oracle's full time-to-solution records (tests/golden/full_size, tools/make_golden.py)."""
+    out = {}
+    for prec in ("mixed", "fp64"):
+        for ortho in ("mgs", "cgsr"):
+            p = os.path.join(ROOT, "tests", "golden", "full_size", f"{cfg}_{prec}_{ortho}_m{m}.json")
+            if not os.path.exists(p):
+                continue
+            g = json.load(open(p))
+            rec = {"seconds": g["seconds"], "threads": g["threads"], "cycles": g["cycles"],
+                   "inner_iters": g["inner_iters"], "host_cpu": g.get("host_cpu")}
+            if variants and f"{prec}_{ortho}" in variants:
+                rec["gpu_cycles"] = variants[f"{prec}_{ortho}"]["cycles"]
+                rec["gpu_tts_ms"] = variants[f"{prec}_{ortho}"]["tts_ms"]
+            out[f"{prec}_{ortho}"] = rec
+    return out
+
+
+def extra_config(name, m, peak):
+    """One config of BASELINE.json at full size: every variant once (after a warm-up solve),
+    time-to-solution, restart counts next to the oracle's golden records, model GB/s and the
+    fraction of the measured HBM peak of the fused solve kernel."""
+    import torch
+    import inputs
+    from paper_2011_01850_b200 import gmres as G
+    P = inputs.make(name)
+    S = G.Solver.from_csr(P.A)
+    b = torch.from_numpy(P.b).cuda()
+    out = {"n": P.A.n, "nnz": P.A.nnz, "m": m}
+    for prec in (G.MIXED, G.FP64):
+        for ortho in (G.MGS, G.CGSR):
+            x = torch.zeros_like(b)
+            S.solve_device(b, x, m=m, tol=TOL, ortho=ortho, precision=prec, max_cycles=1)  # warm-up
+            x.zero_()
+            r = S.solve_device(b, x, m=m, tol=TOL, ortho=ortho, precision=prec)
+            wb = 4 if prec == G.MIXED else 8
+            mb = model_bytes(P.A.n, P.A.nnz, wb, ortho, r.cycle_iters)
+            key = ("mixed_" if prec == G.MIXED else "fp64_") + ("mgs" if ortho == 0 else "cgsr")
+            gold = golden_tts(name, m).get(key, {})
+            out[key] = {"status": r.status_name, "tts_ms": r.device_ms, "kernel_ms": r.kernel_ms,
+                        "cycles": r.cycles, "inner_iters": r.inner_iters, "final_relres": r.final_relres,
+                        "final_backward_err": r.final_backward_err, "oracle_cycles": gold.get("cycles"),
+                        "oracle_inner_iters": gold.get("inner_iters"), "model_GB": mb / 1e9,
+                        "model_GBps": mb / (r.kernel_ms * 1e-3) / 1e9,
+                        "frac_of_peak": mb / (r.kernel_ms * 1e-3) / 1e9 / peak,
+                        "mgs_variant": S.plan().get("mgs_variant") if ortho == 0 else None,
+                        "phase_ms": {k: v / 1e6 for k, v in zip(["resid", "spmv", "ortho", "givens", "update"],
+                                                                  r.phase_ns[:5])}}
+    out["mixed_over_fp64_tts_speedup"] = {o: out[f"fp64_{o}"]["tts_ms"] / out[f"mixed_{o}"]["tts_ms"]
+                                          for o in ("mgs", "cgsr")}
+    S.close()
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -265,6 +319,7 @@ def run_ours(args, rank, world, local_rank):
         name = "mixed_" + ("mgs" if ortho == 0 else "cgsr")
         variants[name] = {"tts_ms": r.device_ms, "kernel_ms": r.kernel_ms, "cycles": r.cycles,
                           "inner_iters": r.inner_iters, "final_relres": r.final_relres,
+                          "final_backward_err": r.final_backward_err,
                           "model_GBps": model_bytes(n, nnz, 4, ortho, r.cycle_iters, cast=True) / (r.device_ms * 1e-3) / 1e9,
                           "phase_ms": {k: v / 1e6 for k, v in zip(["resid", "spmv", "ortho", "givens", "update"],
                                                                     r.phase_ns[:5])}}
@@ -312,6 +367,16 @@ def run_ours(args, rank, world, local_rank):
                     "us_per_inner": 1e3 * r.kernel_ms / max(1, r.inner_iters), "final_relres": r.final_relres}
         ilu["levels"] = {"lower": lo, "upper": up}
 
+    # the paper's third arm: the fp64 solver with an fp32 ILU(0)
+    if world == 1 and not args.no_ilu:
+        for ortho in (G.MGS, G.CGSR):
+            xi = torch.zeros_like(x)
+            r = S.solve_device(b, xi, m=M, tol=TOL, ortho=ortho, precision=G.FP64, precond=G.ILU0_FP32)
+            assert r.status == 0, r.status_name
+            ilu["fp64_ilu32_" + ("mgs" if ortho == 0 else "cgsr")] = {
+                "tts_ms": r.device_ms, "cycles": r.cycles, "inner_iters": r.inner_iters,
+                "us_per_inner": 1e3 * r.kernel_ms / max(1, r.inner_iters), "final_relres": r.final_relres}
+
     # e2e through gmres_solve with pinned host buffers (h2d b, d2h x inside every call)
     hb = torch.from_numpy(prob.b[r0:r1].copy()).pin_memory()
     hb_np = hb.numpy()
@@ -338,7 +403,18 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         v, dt, sample = oracle_sample(prob, 1)
         cpu = {"value": v, "unit": "cycles/s", "cores": 1, "kind": "oracle", "sample": sample,
-               "seconds": dt, "host_cores": cpu_cores()}
+               "seconds": dt, "host_cores": cpu_cores(),
+               # the oracle's whole time-to-solution on this workload, recorded once by
+               # tools/make_golden.py (OpenMP build, bitwise equal to the 1-thread one),
+               # next to the GPU's restart counts of this run
+               "full_tts_recorded": golden_tts("C2", M, variants)}
+
+    # the other BASELINE.json configs at full size (untimed: one solve per variant after a warm-up)
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra:
+        S.close()
+        S = None
+        extra = {name: extra_config(name, m, peak) for name, m in (("C3", 50), ("C4", 100))}
 
     if rank == 0:
         cfg = config()
@@ -356,13 +432,15 @@ def run_ours(args, rank, world, local_rank):
             "variants": variants,
             "ilu0_untimed": ilu or None,
             "roofline": roofline,
+            "extra_configs": extra,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 4 * args.steps,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    S.close()
+    if S is not None:
+        S.close()
 
 
 def main():
@@ -373,6 +451,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-ilu", action="store_true", help="skip the untimed ILU(0) solves (§8 f2)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the untimed full-size C3 / C4 solves")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
