@@ -234,6 +234,8 @@ void* pick_solve_monitor(int prec, int L) { return pick_solve_ext(prec, 1, L); }
 void* pick_solve_chunked(int prec, int L) { return pick_solve_ext(prec, 2, L); }
 // streamed MGS launches (d.mgs_resident == 3): L ∈ {1, 4}
 void* pick_solve_stream(int prec, int L) { return pick_solve_ext(prec, 5, L); }
+// MGS global-sweep launches (d.mgs_resident == 0) of the kernels without a sweep: L ∈ {1, 4}
+void* pick_solve_sweep(int prec, int L) { return pick_solve_ext(prec, 6, L); }
 // ILU(0)-preconditioned launches (§8 f2): L ∈ {1, 4}
 void* pick_solve_ilu(int prec, int L) { return pick_solve_ext(prec, 3, L); }
 // virtual-rank launches (several row blocks on one device): L ∈ {1, 4}
@@ -1030,7 +1032,10 @@ int plan_mgs(gmres_ctx* ctx, int precision, int m, int G, int tile_bytes, int wa
       return 0;
     }
   }
-  if (any || want == 0) return 0;  // mgs_sweep
+  if (any || want == 0) {  // mgs_sweep (its own instantiation for the headline kernels)
+    if (!fits(out.kern, tile_bytes)) return fail(ctx, GMRES_ECUDA, "MGS sweep kernel cannot be resident");
+    return 0;
+  }
   return fail(ctx, GMRES_EINVAL, "the requested MGS variant does not fit this matrix / launch");
 }
 }  // extern "C++"
@@ -1118,7 +1123,8 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
     if (int rc = plan_mgs(ctx, precision, m, G, tile_bytes, want, tune, ext, opts ? opts->ctas_per_sm : 0,
                           [&](int v) -> const void* {
                             return v == 2 ? pick_solve_chunked(precision, L)
-                                 : v == 3 ? pick_solve_stream(precision, L) : kern;
+                                 : v == 3 ? pick_solve_stream(precision, L)
+                                 : v == 0 && ext ? pick_solve_sweep(precision, L) : kern;
                           }, mp))
       return rc;
     mgs_resident = mp.variant;

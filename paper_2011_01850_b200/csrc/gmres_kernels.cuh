@@ -358,6 +358,7 @@ struct Shm {
   double red[NW * 8];
   double red2[NW * 4];
   unsigned long long pmin, pmax;     // profile mode: all-reduce arrival spread (ar_probe)
+  unsigned long long tprev;          // CTA 0's phase timer: timestamp of the last phase boundary
 };
 
 // wait for stage s of group grp's TMA pipeline; watchdog on %globaltimer
@@ -1377,7 +1378,7 @@ __device__ __noinline__ double mgs_sweep(int r0, int r1, W* __restrict__ w, cons
                             const W* __restrict__ vnext) {
   using V4 = typename VecT<W>::T;
   constexpr int N = VecT<W>::N;
-  constexpr int UB = sizeof(W) == 4 ? 4 : 2;  // independent 16-byte loads in flight per array per thread (fp64: register budget)
+  constexpr int UB = 2;  // independent 16-byte loads in flight per array per thread (noinline: register budget)
   double acc = 0.0;
   const int q0 = r0 / N, q1 = r1 / N;
   for (int qb = q0 + threadIdx.x; qb < q1; qb += UB * NT) {
@@ -2164,11 +2165,11 @@ __device__ __forceinline__ bool final_norm(const Dev& d, Shm& sh, int r0, int r1
 // mgs_resident and mgs_sweep.  Each
 // MGS variant lives in its own kernel: inlined together they raise the register
 // pressure of every phase (tools/regcheck.sh).
-template <class W, bool MON = false, int CH = 0>
+template <class W, bool MON = false, int CH = 0, bool SW = true>
 __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv, W* w,
                             double* s_part, double* s_out, double* s_tmp, double* s_h, W* s_coefW, double* s_y,
                             char* s_tiles, double& NN) {
-  if constexpr (CH != 0) {
+  if constexpr (CH == 1 || CH == 2) {
     if (d.ortho == 0) {
       double nn = 0.0;
       if constexpr (CH == 2) {
@@ -2178,12 +2179,14 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
       }
       return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
     }
-  } else if (d.ortho == 0 && d.mgs_resident && !(d.tune & 4)) {
+  } else if (CH == 0 && d.ortho == 0 && (d.mgs_resident || !SW) && !(d.tune & 4)) {
+    // (!SW: the headline kernels carry no sweep — the planner sends every other MGS
+    // launch to the chunk-ring / streamed / sweep instantiations)
     double nn = 0.0;
     if (!mgs_resident<W>(d, sh, r0, r1, j, V, ldv, w, s_h, s_tiles, nn)) return false;
     return final_norm<W, MON>(d, sh, r0, r1, j, V, ldv, w, nn, s_part, s_out, s_tmp, s_coefW, s_y, s_tiles, NN);
   }
-  if (CH == 0 && d.ortho == 0) {
+  if (SW && (CH == 0 || CH == 3) && d.ortho == 0) {
     W hprev = (W)0;
     const bool pf = !(d.tune & 1) && r1 > r0;
     const unsigned pf_bytes = (unsigned)((r1 - r0) * (int)sizeof(W));
@@ -2305,9 +2308,11 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   W* const V = reinterpret_cast<W*>(d.V);
   const long long ldv = d.ldv;
   const bool lead = cta == 0 && threadIdx.x == 0;
-  unsigned long long tprev = lead ? globaltimer() : 0ull;
+  // phase timers of CTA 0 (the previous timestamp lives in shared memory: no register
+  // stays live across the phases for it)
+  if (lead) sh.tprev = globaltimer();
   auto tick = [&](int ph) {
-    if (lead) { const unsigned long long t = globaltimer(); d.prof[ph] += t - tprev; tprev = t; }
+    if (lead) { const unsigned long long t = globaltimer(); d.prof[ph] += t - sh.tprev; sh.tprev = t; }
   };
 
   int k = 0, total_inner = 0, inner_len = 0, status = ST_OK, J1 = 0;
@@ -2402,7 +2407,11 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       tick(PH_SPMV);
       // ------------ orthogonalise (line 101) and ‖w‖ (line 104)
       double NN;
-      if (!ortho_phase<W, MON, CH>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y, s_tiles, NN)) {
+      // the headline instantiations (L ∈ {1, 4}, no monitor / ILU / virtual ranks) carry no
+      // MGS sweep: its register budget spilled into the resident MGS (r02); CH = 3 is the sweep
+      constexpr bool SW = !((L == 1 || L == 4) && !VR && !MON && !PC && CH == 0);
+      if (!ortho_phase<W, MON, CH, SW>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y,
+                                       s_tiles, NN)) {
         fail = true;
         break;
       }

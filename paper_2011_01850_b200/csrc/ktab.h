@@ -11,7 +11,7 @@ void* ktab_solve_f32_hi(int L);   // default instantiation, L ∈ {8, 16, 32}
 void* ktab_solve_f64_lo(int L);
 void* ktab_solve_f64_hi(int L);
 // variant: 1 orthogonality monitor (MON), 2 chunk-ring MGS (CH = 1), 3 ILU(0) (PC), 4 virtual ranks (VR),
-// 5 streamed MGS (CH = 2); L ∈ {1, 4}
+// 5 streamed MGS (CH = 2), 6 MGS global sweep (CH = 3); L ∈ {1, 4}
 void* ktab_solve_f32_ext(int variant, int L);
 void* ktab_solve_f64_ext(int variant, int L);
 // component kernels: kind 0 spmv, 1 resid, 2 ortho (resident MGS / sweep / CGSR), 3 xupdate, 4 ilu apply,
