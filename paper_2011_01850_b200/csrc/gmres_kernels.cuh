@@ -359,6 +359,10 @@ struct Shm {
   double red2[NW * 4];
   unsigned long long pmin, pmax;     // profile mode: all-reduce arrival spread (ar_probe)
   unsigned long long tprev;          // CTA 0's phase timer: timestamp of the last phase boundary
+  unsigned long long tsub;           // profile mode: CGSR sub-phase / per-CTA SpMV timers
+  // cycle state that only thread 0 needs (kept out of every thread's registers)
+  double thr, beta;                  // restart threshold, β of the cycle
+  int jmax, J1, inner_len;           // max inner steps of the cycle, first cycle's J, recorded inner steps
 };
 
 // wait for stage s of group grp's TMA pipeline; watchdog on %globaltimer
@@ -2207,11 +2211,11 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
   }
   double nn = 0.0;
   const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
-  unsigned long long tp = lead ? globaltimer() : 0ull;
+  if (lead) sh.tsub = globaltimer();
   auto sub = [&](int slot) {
     if (d.profile) {
       grid_sync(d, sh);
-      if (lead) { const unsigned long long t = globaltimer(); d.prof[8 + slot] += t - tp; tp = t; }
+      if (lead) { const unsigned long long t = globaltimer(); d.prof[8 + slot] += t - sh.tsub; sh.tsub = t; }
     }
   };
   // serpentine passes (rowtile_pass: reuse): 1 in direction D, 2 reversed, 3 in D;
@@ -2303,8 +2307,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   if (threadIdx.x == 0) { sh.epoch = d.epoch0; sh.red_epoch = d.red0; }
   __syncthreads();
   const int r0 = d.row_begin[cta], r1 = d.row_begin[cta + 1];
-  W* const wb0 = reinterpret_cast<W*>(d.w0);
-  W* const wb1 = reinterpret_cast<W*>(d.w1);
+#define wb0 reinterpret_cast<W*>(d.w0)
   W* const V = reinterpret_cast<W*>(d.V);
   const long long ldv = d.ldv;
   const bool lead = cta == 0 && threadIdx.x == 0;
@@ -2315,7 +2318,8 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (lead) { const unsigned long long t = globaltimer(); d.prof[ph] += t - sh.tprev; sh.tprev = t; }
   };
 
-  int k = 0, total_inner = 0, inner_len = 0, status = ST_OK, J1 = 0;
+  int k = 0, total_inner = 0, status = ST_OK;
+  if (threadIdx.x == 0) { sh.J1 = 0; sh.inner_len = 0; }
   unsigned ilu_seq = 0;  // ILU applies so far (sync-free solve sequence numbers)
   (void)ilu_seq;
   // (every rank reads its own flag: the cast overflow check is the same on all
@@ -2379,29 +2383,32 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (!(beta > 0.0) || !isfinite(beta)) { status = ST_ENONFINITE; break; }
     // restart threshold (readings R6, R22): the two-stage policy drops δ after
     // the first cycle and restarts at the first cycle's iteration count J1
-    const bool repeat = d.policy == 1 && k > 0;
-    const double thr = beta * fmax(d.tol * nb / sqrt(ZZ), repeat ? 0.0 : d.delta);
-    const int jmax = repeat ? min(d.m, J1) : d.m;
     if (threadIdx.x == 0) {
+      const bool repeat = d.policy == 1 && k > 0;
+      sh.thr = beta * fmax(d.tol * nb / sqrt(ZZ), repeat ? 0.0 : d.delta);
+      sh.jmax = repeat ? min(d.m, sh.J1) : d.m;
+      sh.beta = beta;
       for (int i = 0; i <= d.m; ++i) s_s[i] = 0.0;
       s_s[0] = beta;
       s_rhs[0] = beta;  // |s| history of the cycle (stall policy; s_rhs is free until the back-solve)
     }
     double inv = 1.0 / beta;
-    W* src = wb0;
-    W* dst = wb1;
+    // v_j's unnormalised source and w alternate between the work vectors (by the parity of j,
+    // from the constant bank at each use: no pointer pair stays live in registers)
+    auto src = [&](int jj) { return reinterpret_cast<W*>((jj & 1) ? d.w0 : d.w1); };
+    auto dst = [&](int jj) { return reinterpret_cast<W*>((jj & 1) ? d.w1 : d.w0); };
     int J = 0;
     double mon_fro2 = 0.0;  // orthogonality monitor: ‖S‖_F² of this cycle (policy 3)
     bool fail = false;
     for (int j = 1; j <= d.m; ++j) {
       // ------------ w = M⁻¹ A v_j, v_j (own rows) → V   (lines 100, 105)
-      const unsigned long long ts0 = d.profile && threadIdx.x == 0 ? globaltimer() : 0ull;
-      spmv_phase<W, L>(d, sh, s_tiles, src, inv, dst, V, j - 1);
+      if (d.profile && threadIdx.x == 0) sh.tsub = globaltimer();
+      spmv_phase<W, L>(d, sh, s_tiles, src(j), inv, dst(j), V, j - 1);
       if constexpr (PC) {  // w = U⁻¹L⁻¹(A_W v_j) (line 100 with M = LU)
-        if (!grid_sync(d, sh) || !ilu_apply_any<W>(d, sh, dst, dst, ilu_seq++)) { fail = true; break; }
+        if (!grid_sync(d, sh) || !ilu_apply_any<W>(d, sh, dst(j), dst(j), ilu_seq++)) { fail = true; break; }
       }
       if (d.profile) {
-        if (threadIdx.x == 0) d.prof_cta[cta] += globaltimer() - ts0;
+        if (threadIdx.x == 0) d.prof_cta[cta] += globaltimer() - sh.tsub;
         if (!grid_sync(d, sh)) { fail = true; break; }
       }
       tick(PH_SPMV);
@@ -2410,7 +2417,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       // the headline instantiations (L ∈ {1, 4}, no monitor / ILU / virtual ranks) carry no
       // MGS sweep: its register budget spilled into the resident MGS (r02); CH = 3 is the sweep
       constexpr bool SW = !((L == 1 || L == 4) && !VR && !MON && !PC && CH == 0);
-      if (!ortho_phase<W, MON, CH, SW>(d, sh, r0, r1, j, V, ldv, dst, s_part, s_out, s_tmp, s_h, s_coefW, s_y,
+      if (!ortho_phase<W, MON, CH, SW>(d, sh, r0, r1, j, V, ldv, dst(j), s_part, s_out, s_tmp, s_h, s_coefW, s_y,
                                        s_tiles, NN)) {
         fail = true;
         break;
@@ -2427,24 +2434,23 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
         const double sabs = hess_step(j, s_h, s_cs, s_sn, s_s);
         if (cta == 0) {
           for (int i = 0; i <= j; ++i) d.R[(size_t)(j - 1) * (d.m + 1) + i] = s_h[i];
-          if (inner_len < d.inner_cap) d.inner_hist[inner_len] = sabs / beta;
+          if (sh.inner_len < d.inner_cap) d.inner_hist[sh.inner_len] = sabs / sh.beta;
         }
+        sh.inner_len++;
         s_rhs[j] = sabs;
         const bool stall = d.stall_w > 0 && j >= d.stall_w && sabs * d.stall_factor > s_rhs[j - d.stall_w];
-        sh.flag = (j == jmax) || (hn == 0.0) || (sabs <= thr) || stall || orth || !isfinite(hn);
+        sh.flag = (j == sh.jmax) || (hn == 0.0) || (sabs <= sh.thr) || stall || orth || !isfinite(hn);
       }
       __syncthreads();
-      inner_len++;
       tick(PH_GIVENS);
       J = j;
       if (!isfinite(hn)) { status = ST_ENONFINITE; fail = true; break; }
       if (sh.flag) break;
       inv = 1.0 / hn;
-      W* t = src; src = dst; dst = t;
     }
     if (fail) { if (status == ST_OK) status = ST_ETIMEOUT; break; }
     total_inner += J;
-    if (k == 0) J1 = J;
+    if (k == 0 && threadIdx.x == 0) sh.J1 = J;
     if (lead && k < d.hist_cap) d.cycle_J[k] = J;
     // ------------ y = R⁻¹ s, x ← x + V_J y  (lines 143–147)
     if (cta == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);
@@ -2462,9 +2468,10 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     d.out_int[0] = status;
     d.out_int[1] = k;
     d.out_int[2] = total_inner;
-    d.out_int[4] = inner_len;
+    d.out_int[4] = sh.inner_len;
     if (d.epoch_out) { d.epoch_out[0] = sh.epoch; d.epoch_out[1] = (unsigned long long)sh.red_epoch; }
   }
+#undef wb0
 }
 
 #ifdef G200_HOST_TU  // non-template kernels: defined once, in gmres_capi.cu
