@@ -2,6 +2,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ar_bench tools/ar_bench.cu
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -78,6 +79,57 @@ __global__ void __launch_bounds__(NT, 1) kern(Args a) {
         double s = 0; for (int w = 0; w < (G + 31) / 32; ++w) s += red2[w];
         acc_all += s;
       }
+    } else if (a.variant == 8 || a.variant == 9) {
+      // as 7 but the arrival carries its data: red.relaxed (8: CTA 0 alone releases, for
+      // its zeroing of the word two epochs ahead; 9: all release), relaxed polling and
+      // one acquire fence after the poll succeeds
+      v = warp_sum(v);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      if (warp == 1) {
+        double s = lane < NW ? red[lane] : 0.0;
+        for (int o = NW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+          unsigned long long* w = a.ctr + (size_t)(e3 & 3) * 32;
+          long long q = llrint(ldexp(s, 43 - 12));
+          const unsigned long long add = (1ull << 53) + (unsigned long long)(q + (1ll << 44));
+          if (a.variant == 9 || g == 0) red_rel(w, add); else red_rlx(w, add);
+          unsigned long long x;
+          while (((x = ld_rlx(w)) >> 53) < (unsigned long long)G) {}
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          const long long sum = (long long)(x & ((1ull << 53) - 1)) - (long long)G * (1ll << 44);
+          red2[0] = ldexp((double)sum, 12 - 43);
+          if (g == 0) st_rlx(a.ctr + (size_t)((e3 + 2) & 3) * 32, 0ull);
+        }
+      }
+      __syncthreads();
+      acc_all += red2[0];
+      e3 = e3 + 1;
+    } else if (a.variant == 7) {
+      // single-word fixed-point all-reduce: count in bits 53..63, offset-binary 43-bit
+      // quantised partials below (sum exact, order-independent); 4 rotating words,
+      // CTA 0 zeroes the word two epochs ahead; one round trip after the last arrival
+      v = warp_sum(v);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      if (warp == 1) {
+        double s = lane < NW ? red[lane] : 0.0;
+        for (int o = NW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+          unsigned long long* w = a.ctr + (size_t)(e3 & 3) * 32;
+          long long q = llrint(ldexp(s, 43 - 12));
+          const unsigned long long add = (1ull << 53) + (unsigned long long)(q + (1ll << 44));
+          red_rel(w, add);
+          unsigned long long x;
+          while (((x = ld_acq(w)) >> 53) < (unsigned long long)G) {}
+          const long long sum = (long long)(x & ((1ull << 53) - 1)) - (long long)G * (1ll << 44);
+          red2[0] = ldexp((double)sum, 12 - 43);
+          if (g == 0) st_rlx(a.ctr + (size_t)((e3 + 2) & 3) * 32, 0ull);
+        }
+      }
+      __syncthreads();
+      acc_all += red2[0];
+      e3 = e3 + 1;
     } else if (a.variant >= 10) {
       // counter + partial load with the arrivals spread over NC = variant-10 counters
       // (256 B apart: different L2 slices); warp 0 lane c polls counter c
@@ -156,7 +208,8 @@ __global__ void fill(unsigned long long* p, size_t n, unsigned long long v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int only = argc > 1 ? atoi(argv[1]) : -1;  // run one variant only
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int G = sms, iters = 2000;
   unsigned long long *ctr, *out; double *slots, *parts;
@@ -176,6 +229,9 @@ int main() {
     {5, 1, "slots release push + acquire fence, stride 8B"},
     {6, 1, "slots release push, warp-0 poll, stride 8B"},
     {6, 32, "slots release push, warp-0 poll, stride 256B"},
+    {7, 1, "fixed-point single word (count + sum), one round trip"},
+    {8, 1, "fixed-point word, relaxed arrivals (CTA 0 releases), relaxed poll + fence"},
+    {9, 1, "fixed-point word, release arrivals, relaxed poll + fence"},
     {11, 1, "counter x1 (warp-0 poll) + partial load"},
     {12, 1, "counters x2 + partial load"},
     {14, 1, "counters x4 + partial load"},
@@ -183,6 +239,7 @@ int main() {
     {26, 1, "counters x16 + partial load"},
   };
   for (auto& v : vs) {
+    if (only >= 0 && v.v != only) continue;
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(ctr, 0, 8 * 32 * 32);
       fill<<<64, 256>>>((unsigned long long*)slots, (size_t)3 * G * maxstride, SENT);
@@ -193,7 +250,7 @@ int main() {
       e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("run: %s\n", cudaGetErrorString(e)); return 1; }
       unsigned long long h[2]; cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
-      if (rep == 1) printf("%-55s %7.3f us/op  (check %.6e)\n", v.name, h[0] / 1e3 / iters, __builtin_bit_cast(double, h[1]));
+      if (rep == 1) { printf("%-55s %7.3f us/op  (check %.6e)\n", v.name, h[0] / 1e3 / iters, __builtin_bit_cast(double, h[1])); fflush(stdout); }
     }
   }
   return 0;
