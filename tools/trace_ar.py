@@ -1,4 +1,7 @@
-"""All-reduce timeline of a C2 mixed MGS solve (dev tool; needs the G200_TRACE build hook)."""
+"""All-reduce timeline of a C2 mixed MGS solve (dev tool).  Needs the G200_TRACE hook of
+commit 3 before the one that added this file (per-CTA timestamps written in allreduce1 and
+dumped by finish_solve); the hook is not in the product kernel (a branch in the hot
+all-reduce).  Result: profiles/r02_mgs_allreduce_trace.txt."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, inputs
