@@ -139,7 +139,8 @@ int gmres_get_phase_ns(gmres_ctx* ctx, double* buf, int32_t cap);
  * 1 whole-vector TMA ring, 2 chunk ring with w partly in shared memory),
  * [3] ring depth (vectors for 1, 8 KB chunk slots for 2), [4] chunks of w in
  * shared memory (variant 2), [5] staging bytes, [6] dynamic shared memory per
- * CTA, [7] block CSR stream (0/1), [8] CGSR row-tile height (0: column-major
+ * CTA, [7] CSR stream (0 per-warp chunks, 1 block stream for rows of ≤ 64
+ * non-zeros, 2 merge-path tiles for irregular rows), [8] CGSR row-tile height (0: column-major
  * basis).  buf is host memory of cap ≥ 0 entries; returns the count written
  * (≤ GMRES_PLAN_N), or GMRES_EINVAL for a null argument. */
 #define GMRES_PLAN_N 9

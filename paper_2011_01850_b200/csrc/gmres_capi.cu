@@ -98,10 +98,21 @@ struct gmres_ctx {
     int* d_send;
     int2* d_stages;
     int* d_stage_off;
+    int4* d_mtiles;   // merge-path tiles, their CTA offsets, split rows and offsets, carries
+    int* d_mt_off;
+    int4* d_msplit;
+    int* d_ms_off;
+    double* d_mcarry;
   };
   std::vector<Part> parts;
   int2* d_stages = nullptr;      // block-stream stages of the current partition
   int* d_stage_off = nullptr;
+  int4* d_mtiles = nullptr;      // merge-path stream of the current partition (irregular rows)
+  int* d_mt_off = nullptr;
+  int4* d_msplit = nullptr;
+  int* d_ms_off = nullptr;
+  double* d_mcarry = nullptr;
+  bool merge_ok = false;         // not block_ok: use the merge-path CSR stream (G200_NO_MERGE_STREAM: chunk stream)
   bool block_ok = false;         // every row has ≤ BS_MAXROW nonzeros: use the block CSR stream
   int part_max_rows = 0;  // largest CTA row block of the partition
   // last solve
@@ -354,6 +365,47 @@ void make_stages(const std::vector<int32_t>& rp, int64_t n, const std::vector<in
   off[G] = (int)ent.size();
 }
 
+// merge-path tiles of every CTA's non-zeros (gmres_kernels.cuh csr_merge_stream):
+// a tile starts at position s (its base A = s & ~7), ends at ne ≤ A + MT_CAP and
+// touches ≤ MT_RMAX rows (else it ends with its MT_RMAX-th row); rows may span
+// tiles.  Split rows: {local row, tile of its first position, tile of its last}.
+// Rows are non-empty (every row holds its diagonal, validated at create).
+void make_mtiles(const std::vector<int32_t>& rp, int64_t n, const std::vector<int>& rb, std::vector<int4>& ent,
+                 std::vector<int>& off, std::vector<int4>& split, std::vector<int>& soff) {
+  const int G = (int)rb.size() - 1;
+  ent.clear();
+  split.clear();
+  off.assign(G + 1, 0);
+  soff.assign(G + 1, 0);
+  for (int g = 0; g < G; ++g) {
+    off[g] = (int)ent.size();
+    soff[g] = (int)split.size();
+    const int64_t r0 = std::min<int64_t>(rb[g], n), r1 = std::min<int64_t>(rb[g + 1], n);
+    int64_t s = rp[r0], r = r0, open_tile = -1;
+    const int64_t E1 = rp[r1];
+    while (s < E1) {
+      const int64_t A = s & ~7LL;
+      int64_t ne = std::min<int64_t>(A + MT_CAP, E1);
+      int64_t rz = r;
+      while (rp[rz + 1] < ne) ++rz;  // row holding position ne − 1
+      if (rz - r + 1 > MT_RMAX) {
+        rz = r + MT_RMAX - 1;
+        ne = rp[rz + 1];
+      }
+      const int c = (int)ent.size();
+      ent.push_back(make_int4((int)r, (int)s, (int)(rz - r + 1), 0));
+      const bool open_l = rp[r] < s, open_r = rp[rz + 1] > ne;
+      if (open_l && rp[r + 1] <= ne) split.push_back(make_int4((int)r, (int)open_tile, c, 0));
+      if (open_r && !(open_l && rz == r)) open_tile = c;
+      s = ne;
+      r = rp[rz + 1] == ne ? rz + 1 : rz;
+    }
+    ent.push_back(make_int4((int)r1, (int)E1, 0, 0));  // sentinel (its y ends the last tile)
+  }
+  off[G] = (int)ent.size();
+  soff[G] = (int)split.size();
+}
+
 void free_parts(gmres_ctx* ctx) {
   for (auto& p : ctx->parts) {
     cudaFree(p.d_row_begin);
@@ -362,9 +414,19 @@ void free_parts(gmres_ctx* ctx) {
     cudaFree(p.d_send);
     cudaFree(p.d_stages);
     cudaFree(p.d_stage_off);
+    cudaFree(p.d_mtiles);
+    cudaFree(p.d_mt_off);
+    cudaFree(p.d_msplit);
+    cudaFree(p.d_ms_off);
+    cudaFree(p.d_mcarry);
   }
   ctx->d_stages = nullptr;
   ctx->d_stage_off = nullptr;
+  ctx->d_mtiles = nullptr;
+  ctx->d_mt_off = nullptr;
+  ctx->d_msplit = nullptr;
+  ctx->d_ms_off = nullptr;
+  ctx->d_mcarry = nullptr;
   ctx->parts.clear();
   ctx->d_row_begin = nullptr;
   ctx->d_chunks = nullptr;
@@ -382,6 +444,11 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
       ctx->d_send = p.d_send;
       ctx->d_stages = p.d_stages;
       ctx->d_stage_off = p.d_stage_off;
+      ctx->d_mtiles = p.d_mtiles;
+      ctx->d_mt_off = p.d_mt_off;
+      ctx->d_msplit = p.d_msplit;
+      ctx->d_ms_off = p.d_ms_off;
+      ctx->d_mcarry = p.d_mcarry;
       ctx->part_G = G;
       ctx->part_align = align;
       ctx->part_max_rows = p.max_rows;
@@ -391,7 +458,8 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
   if (ctx->parts.size() >= 4) free_parts(ctx);
   std::vector<int> rb;
   make_partition(ctx->h_rp, ctx->n, ctx->nvec, G, align, rb);
-  gmres_ctx::Part P{G, align, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  gmres_ctx::Part P{G, align, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, nullptr, nullptr, nullptr};
   for (int g = 0; g < G; ++g) P.max_rows = std::max(P.max_rows, rb[g + 1] - rb[g]);
   std::vector<int4> ent;
   std::vector<int> off;
@@ -399,6 +467,7 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
   auto bail = [&](cudaError_t e) {
     cudaFree(P.d_row_begin); cudaFree(P.d_chunks); cudaFree(P.d_chunk_off); cudaFree(P.d_send);
     cudaFree(P.d_stages); cudaFree(P.d_stage_off);
+    cudaFree(P.d_mtiles); cudaFree(P.d_mt_off); cudaFree(P.d_msplit); cudaFree(P.d_ms_off); cudaFree(P.d_mcarry);
     return fail(ctx, e == cudaErrorMemoryAllocation ? GMRES_ENOMEM : GMRES_ECUDA, cudaGetErrorString(e));
   };
   cudaError_t e = cudaMalloc(&P.d_row_begin, sizeof(int) * (G + 1));
@@ -416,6 +485,22 @@ int ensure_partition(gmres_ctx* ctx, int G, int align = ROWALIGN) {
     if (e == cudaSuccess) e = cudaMemcpy(P.d_stages, st.data(), sizeof(int2) * st.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&P.d_stage_off, sizeof(int) * (G + 1));
     if (e == cudaSuccess) e = cudaMemcpy(P.d_stage_off, soff.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(e);
+  }
+  if (ctx->merge_ok) {
+    std::vector<int4> mt, ms;
+    std::vector<int> mto, mso;
+    make_mtiles(ctx->h_rp, ctx->n, rb, mt, mto, ms, mso);
+    auto up = [&](void** dst, const void* src, size_t bytes) {
+      cudaError_t r = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+      if (r == cudaSuccess && bytes) r = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+      return r;
+    };
+    e = up((void**)&P.d_mtiles, mt.data(), sizeof(int4) * mt.size());
+    if (e == cudaSuccess) e = up((void**)&P.d_mt_off, mto.data(), sizeof(int) * mto.size());
+    if (e == cudaSuccess) e = up((void**)&P.d_msplit, ms.data(), sizeof(int4) * ms.size());
+    if (e == cudaSuccess) e = up((void**)&P.d_ms_off, mso.data(), sizeof(int) * mso.size());
+    if (e == cudaSuccess) e = cudaMalloc(&P.d_mcarry, sizeof(double) * 2 * mt.size());
     if (e != cudaSuccess) return bail(e);
   }
   if (ctx->dist() && ctx->linked) {  // per-CTA send lists (halo push)
@@ -744,6 +829,12 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.stages = ctx->d_stages;
   d.stage_off = ctx->d_stage_off;
   d.block_stream = (ctx->block_ok && ctx->d_stages) ? 1 : 0;
+  d.merge_stream = (!d.block_stream && ctx->merge_ok && ctx->d_mtiles) ? 1 : 0;
+  d.mtiles = ctx->d_mtiles;
+  d.mt_off = ctx->d_mt_off;
+  d.msplit = ctx->d_msplit;
+  d.ms_off = ctx->d_ms_off;
+  d.mcarry = ctx->d_mcarry;
   d.history = ctx->d_hist;
   d.cycle_J = ctx->d_cycJ;
   d.hist_cap = ctx->hist_cap;
@@ -821,6 +912,9 @@ int create_impl(const int32_t* row_ptr, const int32_t* col, const double* val, i
     int64_t mx = 0;
     for (int64_t i = 0; i < n; ++i) mx = std::max<int64_t>(mx, row_ptr[i + 1] - row_ptr[i]);
     ctx->block_ok = mx <= BS_MAXROW && !std::getenv("G200_NO_BLOCK_STREAM");
+    int64_t mn = n > 0 ? INT64_MAX : 0;
+    for (int64_t i = 0; i < n; ++i) mn = std::min<int64_t>(mn, row_ptr[i + 1] - row_ptr[i]);
+    ctx->merge_ok = !ctx->block_ok && mn >= 1 && !std::getenv("G200_NO_MERGE_STREAM");
   }
   ctx->nranks = nranks;
   ctx->rank = rank;
@@ -1210,6 +1304,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   }
   set_vlayout(d, vl);
   d.tune = opts ? opts->tune : 0;
+  if (d.tune & 4194304) d.merge_stream = 0;  // dev A/B: chunk stream instead of the merge-path stream
   if (ctx->dist()) {
     const size_t wb = precision == GMRES_MIXED ? 4 : 8;
     d.nranks = ctx->nranks;
@@ -1251,7 +1346,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   P.d = d;
   {
     const int32_t pl[GMRES_PLAN_N] = {G, L, d.mgs_resident, d.mgs_nbuf, d.mgs_wsm, tile_bytes, (int32_t)smem,
-                                      d.block_stream, vl.tb};
+                                      d.block_stream ? 1 : d.merge_stream ? 2 : 0, vl.tb};
     std::copy(pl, pl + GMRES_PLAN_N, ctx->plan);
   }
   ctx->last_m = m;

@@ -135,6 +135,12 @@ struct Dev {
   int block_stream;     // != 0: the CSR stream runs csr_block_stream (rows ≤ BS_MAXROW nnz)
   const int4* chunks;   // CSR chunks {row_begin, nnz_begin, direct, 0}; per CTA a sentinel
   const int* chunk_off; // G+1 offsets into chunks (CTA g: [off[g], off[g+1]-1) + sentinel)
+  int merge_stream;     // != 0 (and not block_stream): the CSR stream runs csr_merge_stream
+  const int4* mtiles;   // merge-path tiles {row_begin, nnz_begin, rows touched, 0}; per CTA a sentinel
+  const int* mt_off;    // G+1 offsets into mtiles
+  const int4* msplit;   // rows crossing a tile boundary {local row, first tile, last tile, 0}
+  const int* ms_off;    // G+1 offsets into msplit
+  double* mcarry;       // [2 · tiles] per-tile partial sums of the crossing rows
   double tol, delta;
   int max_cycles;
   int policy;           // restart policy (readings R22, R23): 0 threshold, 1 two-stage, 2 stall, 3 orth. loss
@@ -1038,19 +1044,298 @@ __device__ void csr_block_stream(const Dev& d, Shm& sh, char* s_stage, const AT*
   __syncthreads();
 }
 
+// ------------------------------------------------ merge-path CSR stream (a2)
+// Alg. 1 line 100 on irregular rows (BJ configs[2]: power-law
+// row lengths 4..2000, "load-imbalance stress for SpMV").  The host cuts each
+// CTA's non-zeros into tiles (make_mtiles): ≤ MT_CAP positions counted from an
+// 8-aligned base A, ≤ MT_RMAX rows touched; a row may span several tiles.
+// Per tile, lane t owns the 8 consecutive positions [A + 8t, A + 8t + 8) —
+// equal work per lane whatever the row lengths (a merge-path split of the
+// non-zeros) — and issues its 8 gathers together.  Only the column and value
+// slices are staged (two bulk copies per tile: the TMA engine paces small
+// copies, and the r02 four-copy tiles were bound by it); lane l holds
+// row_ptr[rb + l] (l ≤ nr) in a register and every lane reads row bounds with
+// shuffles.  A lane sums its positions row segment by row segment
+// (clo[u]: the segment that ended before slot u); a segmented scan across
+// lanes (5 shuffle steps, fixed order) carries a row's partial over lane
+// boundaries; lane l then takes row l's sum from the lane holding its last
+// element and runs its epilogue (coalesced, one row per lane).  A row crossing
+// a tile boundary leaves one partial per tile in d.mcarry ([2·tile]: the
+// tile's first row if it started earlier, [2·tile+1]: its last row if it
+// continues); after the CTA barrier the CTA's split-row list (d.msplit: row,
+// first tile, last tile) sums them in tile order and runs their epilogue —
+// deterministic, no atomics.  Every row has ≥ 1 non-zero (the diagonal,
+// validated at create).  diag(row) returns the gathered value at the diagonal
+// column (loaded directly: coalesced, L2).
+constexpr int MT_CAP = 256;   // positions per tile (32 lanes × 8)
+constexpr int MT_RMAX = 31;   // rows touched per tile (row_ptr[rb .. rb + nr] in one register per lane)
+constexpr int MT_OFF_A = MT_CAP * 4;  // stage layout (bytes): columns, then values
+static_assert(MT_OFF_A + MT_CAP * 4 <= ST_OFF_A + (CHUNK_CAP + 8) * 4, "fp32 merge stage");
+static_assert(MT_OFF_A + MT_CAP * 8 <= ST_OFF_A + (CHUNK_CAP + 8) * 8, "fp64 merge stage");
+
+struct MTile { int rb, s, nr, ne; };  // first row, first position, rows touched, end position
+struct MTWin {                        // tile metadata, 32 tiles per batch held one per lane (cf. MetaWin)
+  int base;
+  int cur[4], nxt[4];
+  __device__ __forceinline__ void load(const Dev& d, int c0, int c1, int grp, int kb, int (&m)[4]) {
+    const int c = c0 + grp + (kb + (int)(threadIdx.x & 31)) * NGRP;
+    if (c < c1) {
+      const int4 e = d.mtiles[c];
+      m[0] = e.x; m[1] = e.y; m[2] = e.z; m[3] = d.mtiles[c + 1].y;
+    } else {
+      m[0] = m[1] = m[2] = m[3] = 0;
+    }
+  }
+  __device__ __forceinline__ void init(const Dev& d, int c0, int c1, int grp) {
+    base = 0;
+    load(d, c0, c1, grp, 0, cur);
+    load(d, c0, c1, grp, 32, nxt);
+  }
+  __device__ __forceinline__ void advance(const Dev& d, int c0, int c1, int grp, int k) {
+    while (k >= base + 32) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cur[t] = nxt[t];
+      base += 32;
+      load(d, c0, c1, grp, base + 32, nxt);
+    }
+  }
+  __device__ __forceinline__ MTile get(int k) const {
+    const int idx = k - base;
+    int v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int a = __shfl_sync(0xffffffffu, cur[t], idx & 31);
+      const int b = __shfl_sync(0xffffffffu, nxt[t], idx & 31);
+      v[t] = idx < 32 ? a : b;
+    }
+    return MTile{v[0], v[1], v[2], v[3]};
+  }
+};
+
+__device__ __forceinline__ void lds8(const float* p, float (&a)[8]) {
+  const float4 x = reinterpret_cast<const float4*>(p)[0], y = reinterpret_cast<const float4*>(p)[1];
+  a[0] = x.x; a[1] = x.y; a[2] = x.z; a[3] = x.w; a[4] = y.x; a[5] = y.y; a[6] = y.z; a[7] = y.w;
+}
+__device__ __forceinline__ void lds8(const double* p, double (&a)[8]) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const double2 x = reinterpret_cast<const double2*>(p)[h];
+    a[2 * h] = x.x;
+    a[2 * h + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void lds8(const int* p, int (&a)[8]) {
+  const int4 x = reinterpret_cast<const int4*>(p)[0], y = reinterpret_cast<const int4*>(p)[1];
+  a[0] = x.x; a[1] = x.y; a[2] = x.z; a[3] = x.w; a[4] = y.x; a[5] = y.y; a[6] = y.z; a[7] = y.w;
+}
+
+template <class AT, int TB, class RT, class Gather, class Pre, class Diag, class Epi>
+__device__ void csr_merge_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __restrict__ vals,
+                                 const RT* __restrict__ rowv, Gather gat, Pre pre, Diag diag, Epi epi) {
+  using Ops = AccOps<AT>;
+  using PT = decltype(pre(0, (RT)0));
+  const int grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = d.mt_off[sh.cta], c1 = d.mt_off[sh.cta + 1] - 1;  // tiles [c0, c1) + a sentinel
+  const int nk = c1 - c0 > grp ? (c1 - c0 - grp + NGRP - 1) / NGRP : 0;  // tiles of this warp
+  constexpr int NS = NSTG<AT>(), SB = stage_bytes<AT>();
+  char* gbase = s_stage + grp * NS * SB;
+  MTWin mw;
+  mw.init(d, c0, c1, grp);
+  const unsigned long long pol_a = policy_evict_first();  // the CSR arrays are read once per SpMV
+  auto issue = [&](const MTile& m, int s) {               // lane 0
+    char* st = gbase + s * SB;
+    const int A = m.s & ~7, eb = (m.ne + 3) & ~3;
+    const unsigned b_ci = (unsigned)(eb - A) * 4u, b_a = (unsigned)(eb - A) * (unsigned)sizeof(AT);
+    mbar_expect_tx(&sh.mbar[grp][s], b_ci + b_a);
+    tma_load_1d_hint(st, d.ci + A, b_ci, &sh.mbar[grp][s], pol_a);
+    tma_load_1d_hint(st + MT_OFF_A, vals + A, b_a, &sh.mbar[grp][s], pol_a);
+  };
+  for (int t = 0; t < NS && t < nk; ++t) {
+    const MTile m = mw.get(t);
+    if (lane == 0) issue(m, t);
+  }
+  // TB tiles per iteration (fp32: two of the four staged tiles): their gathers
+  // and their latency chains (row search, segment pass, scan, lookups) overlap
+  static_assert(NS % TB == 0, "merge stream: ring depth must be a multiple of TB");
+  for (int k = 0; k < nk; k += TB) {
+    mw.advance(d, c0, c1, grp, k);
+    MTile m[TB];
+    bool val[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      val[t] = k + t < nk;
+      m[t] = mw.get(min(k + t, nk - 1));
+      if (!val[t]) { m[t].nr = 0; m[t].ne = m[t].s; }  // empty: no position, no row
+    }
+    // per-row operands of lane l's row rb + l, and row_ptr[rb + l] (l ≤ nr), from
+    // global memory before the stage wait: their latency runs under the wait
+    AT dgl[TB];
+    RT rvv[TB];
+    int rsv[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const bool own = lane < m[t].nr;
+      dgl[t] = own ? diag(m[t].rb + lane) : (AT)0;
+      rvv[t] = own ? __ldg(rowv + m[t].rb + lane) : (RT)0;
+      rsv[t] = lane <= m[t].nr ? __ldg(d.rp + m[t].rb + lane) : 0x7fffffff;
+    }
+#pragma unroll
+    for (int t = 0; t < TB; ++t)
+      if (val[t]) stage_wait(d, sh, grp, (k + t) % NS);
+    AT g[TB][8], a[TB][8];
+    int A[TB], p0[TB], pf[TB], pe[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const char* st = gbase + ((k + t) % NS) * SB;
+      A[t] = m[t].s & ~7;
+      p0[t] = A[t] + 8 * lane;
+      pf[t] = max(p0[t], m[t].s);
+      pe[t] = min(p0[t] + 8, m[t].ne);  // the lane's positions [pf, pe)
+      int cc[8];
+      lds8(reinterpret_cast<const int*>(st) + 8 * lane, cc);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) g[t][u] = (p0[t] + u >= pf[t] && p0[t] + u < pe[t]) ? gat(cc[u]) : (AT)0;
+    }
+    PT pv[TB];
+    int rs[TB], re[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const char* st = gbase + ((k + t) % NS) * SB;
+      lds8(reinterpret_cast<const AT*>(st + MT_OFF_A) + 8 * lane, a[t]);
+      rs[t] = rsv[t];
+      re[t] = __shfl_sync(0xffffffffu, rsv[t], (lane + 1) & 31);
+      pv[t] = lane < m[t].nr ? pre(m[t].rb + lane, rvv[t]) : PT{};
+    }
+    // row of the lane's first position: the last row starting at or before pf
+    // (binary search over row_ptr[rb .. rb + nr − 1] by shuffles; nr ≤ 31)
+    int lr[TB], hi[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) { lr[t] = 0; hi[t] = m[t].nr - 1; }
+#pragma unroll
+    for (int it = 0; it < 5; ++it) {
+#pragma unroll
+      for (int t = 0; t < TB; ++t) {
+        const int mid = (lr[t] + hi[t] + 1) >> 1;
+        const int v = __shfl_sync(0xffffffffu, rsv[t], mid & 31);
+        if (lr[t] < hi[t]) {
+          if (v <= pf[t]) lr[t] = mid; else hi[t] = mid - 1;
+        }
+      }
+    }
+    AT acc[TB], clo[TB][8];
+    bool f[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const int lr0 = lr[t];
+      const int st0 = __shfl_sync(0xffffffffu, rsv[t], lr0 & 31);
+      int end = __shfl_sync(0xffffffffu, rsv[t], (lr0 + 1) & 31);
+      acc[t] = (AT)0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        clo[t][u] = (AT)0;
+        const int nx = __shfl_sync(0xffffffffu, rsv[t], (lr[t] + 2) & 31);  // end of the next row
+        const int p = p0[t] + u;
+        if (p >= pf[t] && p < pe[t]) {
+          if (p == end) {  // the segment of row lr ended before slot u (rows are non-empty)
+            clo[t][u] = acc[t];
+            acc[t] = (AT)0;
+            ++lr[t];
+            end = nx;
+          }
+          acc[t] = Ops::add(acc[t], Ops::mul(a[t][u], g[t][u]));
+        }
+      }
+      // reset flag of the segmented scan: the lane holds no position, or its last
+      // segment starts in it
+      f[t] = !(pf[t] < pe[t]) || lr[t] > lr0 || st0 >= pf[t];
+    }
+    // segmented inclusive scan of the lanes' last segments: C = partial of that
+    // row from its first position in the tile
+    AT C[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) C[t] = pf[t] < pe[t] ? acc[t] : (AT)0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int t = 0; t < TB; ++t) {
+        const AT cv = __shfl_up_sync(0xffffffffu, C[t], o);
+        const bool fv = __shfl_up_sync(0xffffffffu, (int)f[t], o) != 0;
+        if (lane >= o) {
+          if (!f[t]) C[t] = Ops::add(cv, C[t]);
+          f[t] = f[t] || fv;
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      // row l's positions in the tile [ps, pq): its last segment is in lane kl
+      const bool own = lane < m[t].nr;
+      const int ps = max(rs[t], m[t].s), pq = min(re[t], m[t].ne);
+      const int kl = own ? ((pq - 1 - A[t]) >> 3) : 0, kf = own ? ((ps - A[t]) >> 3) : 0;
+      const int eu = pq - (A[t] + 8 * kl);  // 1..8: slot after the row's last position in lane kl
+      const bool fin = eu == 8 || pq == m[t].ne;
+      AT x = __shfl_sync(0xffffffffu, acc[t], kl);
+#pragma unroll
+      for (int u = 1; u < 8; ++u) {
+        const AT v = __shfl_sync(0xffffffffu, clo[t][u], kl);
+        if (!fin && eu == u) x = v;
+      }
+      const AT cp = __shfl_sync(0xffffffffu, C[t], (kl + 31) & 31);
+      if (own) {
+        if (kf < kl) x = Ops::add(cp, x);
+        const bool open_l = rs[t] < m[t].s, open_r = re[t] > m[t].ne;
+        if (!open_l && !open_r) epi(m[t].rb + lane, x, pv[t], dgl[t]);
+        else d.mcarry[2 * (c0 + grp + (k + t) * NGRP) + (open_l ? 0 : 1)] = (double)x;
+      }
+    }
+    __syncwarp();
+    MTile n[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) n[t] = mw.get(min(k + t + NS, nk - 1));
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < TB; ++t) {
+        if (!val[t]) continue;
+        const int s = (k + t) % NS;
+        sh.tma_phase[grp] ^= (1u << s);
+        if (k + t + NS < nk) issue(n[t], s);
+      }
+    }
+  }
+  __syncthreads();  // the tiles' carries are visible to the CTA
+  const int q0 = d.ms_off[sh.cta], q1 = d.ms_off[sh.cta + 1];
+  for (int q = q0 + (int)threadIdx.x; q < q1; q += NT) {
+    const int4 e = d.msplit[q];  // {row, first tile, last tile}
+    AT acc = (AT)d.mcarry[2 * e.y + 1];
+    for (int c = e.y + 1; c <= e.z; ++c) acc = Ops::add(acc, (AT)d.mcarry[2 * c]);
+    epi(e.x, acc, pre(e.x, rowv[e.x]), diag(e.x));
+  }
+  fence_proxy_async_global();
+  __syncthreads();
+}
+
 template <class AT, int L, class RT, class Gather, class Pre, class Epi>
 __device__ __forceinline__ void csr_any_stream(const Dev& d, Shm& sh, char* s_stage, const AT* __restrict__ vals,
                                                const RT* __restrict__ rowv, Gather gat, Pre pre, Epi epi) {
   if (d.block_stream) csr_block_stream<AT, L>(d, sh, s_stage, vals, rowv, gat, pre, epi);
   else csr_stream<AT, L>(d, sh, s_stage, vals, rowv, gat, pre, epi);
 }
+// The merge-path stream runs one tile per warp iteration (TB = 1).  Measured r02
+// on C3 (mixed, 30 SpMVs per solve): chunk stream 41.3 ms, merge tiles with four
+// bulk copies 28.9 ms, two tiles per iteration (TB = 2, twice the gathers in
+// flight) 28.9 ms, two copies per tile 30.3 ms — neither more gathers per warp
+// nor fewer TMA copies moves it: the random gathers (one L2 sector each,
+// 120 M per SpMV) are bound by the memory system's outstanding requests, not
+// by the warp's issue.  TB = 2 raised the register pressure of the whole
+// persistent kernel (spills moved into the resident MGS loop; as a __noinline__
+// call the ABI did the same), so it is kept as a compile-time option only.
 
 // ------------------------------------------------------------------ a1
 // Alg. 1 lines 86–90: z = b − A64 x in fp64, then
 // r = RN_W(dinv_W · RN_W(z)) (reading R10).  fp64 row sums.
-template <class W, int L>
-__device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict__ r_out, double& zz, double& rr,
-                            double& bb, double& xx, int& err) {
+template <class W, int L, bool MERGE>
+__device__ __forceinline__ void resid_body(const Dev& d, Shm& sh, char* s_stage, W* __restrict__ r_out, double& zz,
+                                           double& rr, double& bb, double& xx, int& err) {
   const W* dinv = (const W*)d.dinvW;
   const double* __restrict__ xg = d.x - d.row_base;  // global-index view (CSR columns are global)
   struct P2 { double b; W di; };
@@ -1069,7 +1354,15 @@ __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict_
     r_out[row] = ri;
     rr += (double)ri * (double)ri;
   };
-  csr_any_stream<double, L>(d, sh, s_stage, d.a64, dinv, gat, pre, epi);
+  auto dg = [&](int row) -> double { return d.x[row]; };
+  if (MERGE) csr_merge_stream<double, 1>(d, sh, s_stage, d.a64, dinv, gat, pre, dg, epi);
+  else csr_any_stream<double, L>(d, sh, s_stage, d.a64, dinv, gat, pre, epi);
+}
+template <class W, int L>
+__device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict__ r_out, double& zz, double& rr,
+                            double& bb, double& xx, int& err) {
+  if (!d.block_stream && d.merge_stream) resid_body<W, L, true>(d, sh, s_stage, r_out, zz, rr, bb, xx, err);
+  else resid_body<W, L, false>(d, sh, s_stage, r_out, zz, rr, bb, xx, err);
 }
 
 // ------------------------------------------------------------------ a2
@@ -1078,9 +1371,9 @@ __device__ void resid_phase(const Dev& d, Shm& sh, char* s_stage, W* __restrict_
 // the fly from the unnormalised previous vector (line 105 fused into the
 // gather: identical bits to normalising first).  The epilogue also stores the
 // CTA's own rows of v_j into V[:, j−1].
-template <class W, int L>
-__device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
-                           W* __restrict__ dst, W* __restrict__ V, int vc) {
+template <class W, int L, bool MERGE>
+__device__ __forceinline__ void spmv_body(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
+                                          W* __restrict__ dst, W* __restrict__ V, int vc) {
   const W* dinv = (const W*)d.dinvW;
   const W* __restrict__ srcg = src - d.row_base;  // global-index view (CSR columns are global)
   const W invW = RN<W>(inv);
@@ -1091,7 +1384,15 @@ __device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __rest
     dst[row] = mulw(di, acc);
     if (V) *v_at(d, V, row, vc) = vj;  // v_j at the diagonal = RN_W(src_row · inv), gathered above
   };
-  csr_any_stream<W, L>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, epi);
+  auto dg = [&](int row) -> W { return mulw(ld_pol(src + row, pol_g), invW); };
+  if (MERGE) csr_merge_stream<W, 1>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, dg, epi);
+  else csr_any_stream<W, L>(d, sh, s_stage, (const W*)d.aW, dinv, gat, pre, epi);
+}
+template <class W, int L>
+__device__ void spmv_phase(const Dev& d, Shm& sh, char* s_stage, const W* __restrict__ src, double inv,
+                           W* __restrict__ dst, W* __restrict__ V, int vc) {
+  if (!d.block_stream && d.merge_stream) spmv_body<W, L, true>(d, sh, s_stage, src, inv, dst, V, vc);
+  else spmv_body<W, L, false>(d, sh, s_stage, src, inv, dst, V, vc);
 }
 
 // ------------------------------------------------------------------ f2: ILU(0)

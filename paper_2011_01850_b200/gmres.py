@@ -334,7 +334,7 @@ class Solver:
             raise self._err(rc)
         return lo.value, up.value
 
-    PLAN_KEYS = ("ctas", "lanes", "mgs_variant", "ring", "w_smem_chunks", "stage_bytes", "smem", "block_stream",
+    PLAN_KEYS = ("ctas", "lanes", "mgs_variant", "ring", "w_smem_chunks", "stage_bytes", "smem", "csr_stream",
                  "row_tile")
 
     def plan(self) -> dict:
