@@ -181,6 +181,22 @@ int gmres_dist_ghosts(const int32_t* row_ptr, const int32_t* col, int64_t n_loca
                       int64_t cap, int64_t* count);
 int gmres_dist_sends(int64_t row_begin, int64_t n_local, const int32_t* peer_ghosts, int64_t n_peer_ghosts,
                      int32_t* rows, int64_t cap, int64_t* count);
+/* Host-only: the merge-path tiles of the CSR stream for irregular rows (§8 a2;
+ * PAPER.md:100, Alg. 1), as the solves build them for a grid of G CTAs
+ * owning rows [cta_rows[g], cta_rows[g+1]) (host arrays, G+1 entries).  A tile
+ * starts at non-zero position s, ends at ne ≤ (s & ~7) + 256 and touches ≤ 31
+ * rows; rows may span tiles.  tiles: 4 int32 per entry {first row, s, rows
+ * touched, 0}, per CTA its tiles then a sentinel {row end, nnz end, 0, 0}
+ * (the next entry's s is a tile's ne); tile_off[g] (G+1 entries) = index of
+ * CTA g's first entry.  splits: 4 int32 per row that spans tiles {row, tile of
+ * its first non-zero, tile of its last, 0} (tile = global entry index);
+ * split_off[g] (G+1) likewise.  At most tiles_cap / splits_cap entries are
+ * written, *n_tiles / *n_splits receive the full counts; tile_off / split_off
+ * may be NULL.  GMRES_EINVAL for an empty row (every row must hold its
+ * diagonal) or bad arguments. */
+int gmres_plan_mtiles(const int32_t* row_ptr, int64_t n, const int32_t* cta_rows, int32_t G, int32_t* tiles,
+                      int64_t tiles_cap, int64_t* n_tiles, int32_t* tile_off, int32_t* splits, int64_t splits_cap,
+                      int64_t* n_splits, int32_t* split_off);
 
 /* One rank's share of the matrix (host arrays, copied): n_local rows from
  * global row row_begin (a multiple of 256; n_local a multiple of 256 unless

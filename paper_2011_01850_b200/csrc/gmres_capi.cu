@@ -1509,6 +1509,31 @@ int gmres_dist_partition(const int32_t* row_ptr, int64_t n, int32_t nranks, int6
   return 0;
 }
 
+int gmres_plan_mtiles(const int32_t* row_ptr, int64_t n, const int32_t* cta_rows, int32_t G, int32_t* tiles,
+                      int64_t tiles_cap, int64_t* n_tiles, int32_t* tile_off, int32_t* splits, int64_t splits_cap,
+                      int64_t* n_splits, int32_t* split_off) {
+  if (!row_ptr || !cta_rows || !n_tiles || !n_splits || n < 1 || G < 1) return fail(nullptr, GMRES_EINVAL, "bad arguments");
+  for (int64_t i = 0; i < n; ++i)
+    if (row_ptr[i + 1] <= row_ptr[i]) return fail(nullptr, GMRES_EINVAL, "merge-path tiles need non-empty rows");
+  for (int g = 0; g < G; ++g)
+    if (cta_rows[g] < 0 || cta_rows[g + 1] < cta_rows[g]) return fail(nullptr, GMRES_EINVAL, "bad CTA row boundaries");
+  std::vector<int32_t> rp(row_ptr, row_ptr + n + 1);
+  std::vector<int> rb(cta_rows, cta_rows + G + 1), off, soff;
+  std::vector<int4> ent, sp;
+  make_mtiles(rp, n, rb, ent, off, sp, soff);
+  *n_tiles = (int64_t)ent.size();
+  *n_splits = (int64_t)sp.size();
+  for (int64_t i = 0; i < std::min<int64_t>(tiles_cap, (int64_t)ent.size()); ++i) {
+    tiles[4 * i] = ent[i].x; tiles[4 * i + 1] = ent[i].y; tiles[4 * i + 2] = ent[i].z; tiles[4 * i + 3] = ent[i].w;
+  }
+  for (int64_t i = 0; i < std::min<int64_t>(splits_cap, (int64_t)sp.size()); ++i) {
+    splits[4 * i] = sp[i].x; splits[4 * i + 1] = sp[i].y; splits[4 * i + 2] = sp[i].z; splits[4 * i + 3] = sp[i].w;
+  }
+  if (tile_off) std::copy(off.begin(), off.end(), tile_off);
+  if (split_off) std::copy(soff.begin(), soff.end(), split_off);
+  return 0;
+}
+
 int gmres_create_dist(const int32_t* row_ptr, const int32_t* col, const double* val, int64_t n_global,
                       int64_t row_begin, int64_t n_local, int32_t nranks, int32_t rank, gmres_ctx** out) {
   if (nranks < 2 || nranks > MAXR || rank < 0 || rank >= nranks) return fail(nullptr, GMRES_EINVAL, "bad nranks/rank");

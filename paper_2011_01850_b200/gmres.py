@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libgmres.so")
+_LIB_PATH = os.environ.get("G200_LIB") or os.path.join(_HERE, "libgmres.so")  # (G200_LIB: dev A/B builds)
 _lib = None
 
 MGS, CGSR = 0, 1
@@ -99,12 +99,13 @@ def load_library():
     L.gmres_dist_partition.argtypes = [vp, i64, i32, i64, vp]
     L.gmres_dist_ghosts.argtypes = [vp, vp, i64, i64, vp, i64, p64]
     L.gmres_dist_sends.argtypes = [i64, i64, vp, i64, vp, i64, p64]
+    L.gmres_plan_mtiles.argtypes = [vp, i64, vp, i32, vp, i64, p64, vp, vp, i64, p64, vp]
     L.gmres_create_dist.argtypes = [vp, vp, vp, i64, i64, i64, i32, i32, ctypes.POINTER(vp)]
     L.gmres_dist_export.argtypes = [vp, vp, i64, p64]
     L.gmres_dist_import.argtypes = [vp, vp, vp]
     L.gmres_dist_link_local.argtypes = [vp, i32]
     L.gmres_solve_virtual.argtypes = [vp, i32, vp, vp, vp, i32, dbl, i32, i32, pO, vp]
-    for f in ("gmres_dist_partition", "gmres_dist_ghosts", "gmres_dist_sends", "gmres_create_dist",
+    for f in ("gmres_dist_partition", "gmres_dist_ghosts", "gmres_dist_sends", "gmres_plan_mtiles", "gmres_create_dist",
               "gmres_dist_export", "gmres_dist_import", "gmres_dist_link_local", "gmres_solve_virtual"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -404,6 +405,29 @@ def dist_partition(row_ptr, nranks: int, align: int = 256) -> np.ndarray:
     if rc != 0:
         raise GmresError(rc, L.gmres_last_error(None).decode())
     return out
+
+
+def plan_mtiles(row_ptr, cta_rows):
+    """gmres_plan_mtiles: merge-path tiles of a G-CTA row split (host) →
+    (tiles (T, 4), tile_off (G+1), splits (S, 4), split_off (G+1))."""
+    L = load_library()
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    rb = np.ascontiguousarray(cta_rows, np.int32)
+    G = rb.size - 1
+    nt, ns = ctypes.c_int64(), ctypes.c_int64()
+    rc = L.gmres_plan_mtiles(_p(rp), rp.size - 1, _p(rb), G, None, 0, ctypes.byref(nt), None, None, 0,
+                             ctypes.byref(ns), None)
+    if rc != 0:
+        raise GmresError(rc, L.gmres_last_error(None).decode())
+    tiles = np.zeros((nt.value, 4), np.int32)
+    splits = np.zeros((max(ns.value, 1), 4), np.int32)
+    toff = np.zeros(G + 1, np.int32)
+    soff = np.zeros(G + 1, np.int32)
+    rc = L.gmres_plan_mtiles(_p(rp), rp.size - 1, _p(rb), G, _p(tiles), nt.value, ctypes.byref(nt), _p(toff),
+                             _p(splits), ns.value, ctypes.byref(ns), _p(soff))
+    if rc != 0:
+        raise GmresError(rc, L.gmres_last_error(None).decode())
+    return tiles, toff, splits[:ns.value], soff
 
 
 def dist_ghosts(row_ptr, col, row_begin: int) -> np.ndarray:
