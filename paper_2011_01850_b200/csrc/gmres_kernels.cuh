@@ -368,6 +368,9 @@ struct Shm {
   unsigned long long tsub;           // profile mode: CGSR sub-phase / per-CTA SpMV timers
   // cycle state that only thread 0 needs (kept out of every thread's registers)
   double thr, beta;                  // restart threshold, β of the cycle
+  double inv;                        // 1/‖v_j's source‖ of the next SpMV (read by every thread, written by thread 0)
+  int kcyc, total_inner;             // cycles done, inner iterations done
+  int r0, r1;                        // this CTA's row block
   int jmax, J1, inner_len;           // max inner steps of the cycle, first cycle's J, recorded inner steps
 };
 
@@ -2604,14 +2607,22 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   W* const s_coefW = reinterpret_cast<W*>(dsm + d.soff[9]);
   char* const s_tiles = dsm + d.soff[10];
   init_shm(sh, (int)blockIdx.x - vr * ds.G);
-  const int cta = sh.cta;
-  if (threadIdx.x == 0) { sh.epoch = d.epoch0; sh.red_epoch = d.red0; }
+  if (threadIdx.x == 0) {
+    sh.epoch = d.epoch0;
+    sh.red_epoch = d.red0;
+    sh.r0 = d.row_begin[sh.cta];
+    sh.r1 = d.row_begin[sh.cta + 1];
+  }
   __syncthreads();
-  const int r0 = d.row_begin[cta], r1 = d.row_begin[cta + 1];
+  // (CTA index, row block and lead flag re-read from shared memory at each use:
+  // kept in registers they lived across every phase and spilled)
+#define cta_ (sh.cta)
+#define r0_ (sh.r0)
+#define r1_ (sh.r1)
+#define lead (sh.cta == 0 && threadIdx.x == 0)
 #define wb0 reinterpret_cast<W*>(d.w0)
   W* const V = reinterpret_cast<W*>(d.V);
   const long long ldv = d.ldv;
-  const bool lead = cta == 0 && threadIdx.x == 0;
   // phase timers of CTA 0 (the previous timestamp lives in shared memory: no register
   // stays live across the phases for it)
   if (lead) sh.tprev = globaltimer();
@@ -2619,8 +2630,10 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (lead) { const unsigned long long t = globaltimer(); d.prof[ph] += t - sh.tprev; sh.tprev = t; }
   };
 
-  int k = 0, total_inner = 0, status = ST_OK;
-  if (threadIdx.x == 0) { sh.J1 = 0; sh.inner_len = 0; }
+  // loop state in shared memory (cycle count, inner total, 1/h): values live across
+  // the phases otherwise spill (r02: the headline kernel's last local-memory ops)
+  int status = ST_OK;
+  if (threadIdx.x == 0) { sh.J1 = 0; sh.inner_len = 0; sh.kcyc = 0; sh.total_inner = 0; }
   unsigned ilu_seq = 0;  // ILU applies so far (sync-free solve sequence numbers)
   (void)ilu_seq;
   // (every rank reads its own flag: the cast overflow check is the same on all
@@ -2633,7 +2646,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
   for (; status == ST_OK;) {
     // ---------------- residual, stop test (Alg. 1 lines 86–92)
     // ‖z‖², ‖r‖², ‖b‖², ‖x‖² and (CTA 0 of each rank) this rank's ‖A‖_F²
-    double v3[5] = {0.0, 0.0, 0.0, 0.0, cta == 0 && threadIdx.x == 0 ? d.normA2 : 0.0};
+    double v3[5] = {0.0, 0.0, 0.0, 0.0, cta_ == 0 && threadIdx.x == 0 ? d.normA2 : 0.0};
     int err = 0;
     resid_phase<W, L>(d, sh, s_tiles, wb0, v3[0], v3[1], v3[2], v3[3], err);
     if (err) atomicOr(d.err_flag, err);
@@ -2652,15 +2665,15 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     const double ZZ = s_out[0], RR = s_out[1], nb = sqrt(s_out[2]);
     const int ef = *(volatile int*)d.err_flag;  // (other ranks' errors arrive as NaN/Inf in ZZ/RR)
     if (nb == 0.0) {  // b = 0 → x = 0, no cycle (reading R13)
-      for (int i = r0 + threadIdx.x; i < min(r1, d.n); i += NT) d.x[i] = 0.0;
+      for (int i = r0_ + threadIdx.x; i < min(r1_, d.n); i += NT) d.x[i] = 0.0;
       if (lead) { if (d.hist_cap > 0) d.history[0] = 0.0; d.out_int[3] = 1; d.out_dbl[0] = 0.0; d.out_dbl[1] = 0.0; }
       status = ST_OK;
       break;
     }
     const double rho = sqrt(ZZ) / nb;
     if (lead) {
-      if (k < d.hist_cap) d.history[k] = rho;
-      d.out_int[3] = k + 1;
+      if (sh.kcyc < d.hist_cap) d.history[sh.kcyc] = rho;
+      d.out_int[3] = sh.kcyc + 1;
       d.out_dbl[0] = rho;
       // normwise backward error ‖b − Ax‖/(‖A‖_F‖x‖ + ‖b‖) of this iterate (report only)
       d.out_dbl[1] = sqrt(ZZ) / (sqrt(s_out[4]) * sqrt(s_out[3]) + nb);
@@ -2669,12 +2682,12 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     if (ef & ERRF_NONFINITE || !isfinite(ZZ) || !isfinite(nb)) { status = ST_ENONFINITE; break; }
     if ((ef & ERRF_RANGE) || RR > DBL_MAX) { status = ST_EFP32RANGE; break; }
     if (rho <= d.tol) { status = ST_OK; break; }
-    if (k >= d.max_cycles) { status = ST_NOT_CONVERGED; break; }
+    if (sh.kcyc >= d.max_cycles) { status = ST_NOT_CONVERGED; break; }
     double RRp = RR;
     if constexpr (PC) {  // line 90 with M = LU (reading R24): r = U⁻¹L⁻¹ RN_W(z), then ‖r‖²
       if (!ilu_apply_any<W>(d, sh, wb0, wb0, ilu_seq++)) { status = ST_ETIMEOUT; break; }
       double p = 0.0;
-      for (int i = r0 + threadIdx.x; i < min(r1, d.n); i += NT) {
+      for (int i = r0_ + threadIdx.x; i < min(r1_, d.n); i += NT) {
         const double v = (double)__ldcg(wb0 + i);
         p += v * v;
       }
@@ -2685,15 +2698,16 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     // restart threshold (readings R6, R22): the two-stage policy drops δ after
     // the first cycle and restarts at the first cycle's iteration count J1
     if (threadIdx.x == 0) {
-      const bool repeat = d.policy == 1 && k > 0;
+      const bool repeat = d.policy == 1 && sh.kcyc > 0;
       sh.thr = beta * fmax(d.tol * nb / sqrt(ZZ), repeat ? 0.0 : d.delta);
       sh.jmax = repeat ? min(d.m, sh.J1) : d.m;
       sh.beta = beta;
       for (int i = 0; i <= d.m; ++i) s_s[i] = 0.0;
       s_s[0] = beta;
       s_rhs[0] = beta;  // |s| history of the cycle (stall policy; s_rhs is free until the back-solve)
+      sh.inv = 1.0 / beta;
     }
-    double inv = 1.0 / beta;
+    __syncthreads();
     // v_j's unnormalised source and w alternate between the work vectors (by the parity of j,
     // from the constant bank at each use: no pointer pair stays live in registers)
     auto src = [&](int jj) { return reinterpret_cast<W*>((jj & 1) ? d.w0 : d.w1); };
@@ -2704,12 +2718,12 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     for (int j = 1; j <= d.m; ++j) {
       // ------------ w = M⁻¹ A v_j, v_j (own rows) → V   (lines 100, 105)
       if (d.profile && threadIdx.x == 0) sh.tsub = globaltimer();
-      spmv_phase<W, L>(d, sh, s_tiles, src(j), inv, dst(j), V, j - 1);
+      spmv_phase<W, L>(d, sh, s_tiles, src(j), sh.inv, dst(j), V, j - 1);
       if constexpr (PC) {  // w = U⁻¹L⁻¹(A_W v_j) (line 100 with M = LU)
         if (!grid_sync(d, sh) || !ilu_apply_any<W>(d, sh, dst(j), dst(j), ilu_seq++)) { fail = true; break; }
       }
       if (d.profile) {
-        if (threadIdx.x == 0) d.prof_cta[cta] += globaltimer() - sh.tsub;
+        if (threadIdx.x == 0) d.prof_cta[cta_] += globaltimer() - sh.tsub;
         if (!grid_sync(d, sh)) { fail = true; break; }
       }
       tick(PH_SPMV);
@@ -2718,7 +2732,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       // the headline instantiations (L ∈ {1, 4}, no monitor / ILU / virtual ranks) carry no
       // MGS sweep: its register budget spilled into the resident MGS (r02); CH = 3 is the sweep
       constexpr bool SW = !((L == 1 || L == 4) && !VR && !MON && !PC && CH == 0);
-      if (!ortho_phase<W, MON, CH, SW>(d, sh, r0, r1, j, V, ldv, dst(j), s_part, s_out, s_tmp, s_h, s_coefW, s_y,
+      if (!ortho_phase<W, MON, CH, SW>(d, sh, r0_, r1_, j, V, ldv, dst(j), s_part, s_out, s_tmp, s_h, s_coefW, s_y,
                                        s_tiles, NN)) {
         fail = true;
         break;
@@ -2726,14 +2740,14 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       tick(PH_ORTHO);
       // ------------ orthogonality monitor (policy 3, reading R23): the new column
       // of S_k = (I+U_k)⁻¹U_k by unit upper back-substitution, ‖S‖_F² accumulated
-      if (MON && d.policy == 3 && NN > 0.0) mon_fro2 += orth_column(d.Umat, d.m + 1, j, cta == 0, s_y, sh, s_part);
+      if (MON && d.policy == 3 && NN > 0.0) mon_fro2 += orth_column(d.Umat, d.m + 1, j, cta_ == 0, s_y, sh, s_part);
       const bool orth = MON && d.policy == 3 && sqrt(mon_fro2) >= d.orth_thresh;
       // ------------ h_{j+1,j}, Givens, exit test (lines 104, 108–140, 98)
       const double hn = sqrt(NN);
       if (threadIdx.x == 0) {
         s_h[j] = hn;
         const double sabs = hess_step(j, s_h, s_cs, s_sn, s_s);
-        if (cta == 0) {
+        if (cta_ == 0) {
           for (int i = 0; i <= j; ++i) d.R[(size_t)(j - 1) * (d.m + 1) + i] = s_h[i];
           if (sh.inner_len < d.inner_cap) d.inner_hist[sh.inner_len] = sabs / sh.beta;
         }
@@ -2741,38 +2755,45 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
         s_rhs[j] = sabs;
         const bool stall = d.stall_w > 0 && j >= d.stall_w && sabs * d.stall_factor > s_rhs[j - d.stall_w];
         sh.flag = (j == sh.jmax) || (hn == 0.0) || (sabs <= sh.thr) || stall || orth || !isfinite(hn);
+        sh.inv = 1.0 / hn;
       }
       __syncthreads();
       tick(PH_GIVENS);
       J = j;
       if (!isfinite(hn)) { status = ST_ENONFINITE; fail = true; break; }
       if (sh.flag) break;
-      inv = 1.0 / hn;
     }
     if (fail) { if (status == ST_OK) status = ST_ETIMEOUT; break; }
-    total_inner += J;
-    if (k == 0 && threadIdx.x == 0) sh.J1 = J;
-    if (lead && k < d.hist_cap) d.cycle_J[k] = J;
+    if (threadIdx.x == 0) {
+      if (sh.kcyc == 0) sh.J1 = J;
+      sh.total_inner += J;
+    }
+    if (lead && sh.kcyc < d.hist_cap) d.cycle_J[sh.kcyc] = J;
     // ------------ y = R⁻¹ s, x ← x + V_J y  (lines 143–147)
-    if (cta == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);
+    if (cta_ == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     for (int i = threadIdx.x; i < J; i += NT) s_y[i] = __ldcg(d.y + i);
     __syncthreads();
     double dummy = 0.0;
-    rowtile_pass<W, 4>(d, sh, r0, r1, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
+    rowtile_pass<W, 4>(d, sh, r0_, r1_, V, ldv, J, nullptr, s_coefW, s_y, s_tmp, s_tiles, dummy);
     halo_push(d, sh, (const double*)d.x, 2);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     tick(PH_UPDATE);
-    ++k;
+    if (threadIdx.x == 0) sh.kcyc++;
+    __syncthreads();
   }
   if (lead) {
     d.out_int[0] = status;
-    d.out_int[1] = k;
-    d.out_int[2] = total_inner;
+    d.out_int[1] = sh.kcyc;
+    d.out_int[2] = sh.total_inner;
     d.out_int[4] = sh.inner_len;
     if (d.epoch_out) { d.epoch_out[0] = sh.epoch; d.epoch_out[1] = (unsigned long long)sh.red_epoch; }
   }
 #undef wb0
+#undef cta_
+#undef r0_
+#undef r1_
+#undef lead
 }
 
 #ifdef G200_HOST_TU  // non-template kernels: defined once, in gmres_capi.cu
