@@ -45,6 +45,7 @@ MATS = {
     "c2mini": lambda: inputs.make("C2", 17).A,             # 7-pt 17³ (ragged n = 4913)
     "c4mini": lambda: inputs.make("C4", 9).A,              # 27-pt
     "random": lambda: random_dd_csr(3001, 5),              # irregular rows and levels
+    "c3mini": lambda: inputs.make("C3", 6000).A,           # power-law rows (up to 1902 non-zeros)
 }
 
 
@@ -90,6 +91,7 @@ E2E = {
     "C1": lambda: inputs.make("C1"),
     "C2mini": lambda: inputs.make("C2", 24),
     "C4mini": lambda: inputs.make("C4", 12),
+    "C3mini": lambda: inputs.make("C3", 6000),             # power-law rows: the merge-path SpMV + ILU kernels
 }
 
 
