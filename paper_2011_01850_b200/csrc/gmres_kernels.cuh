@@ -550,24 +550,34 @@ __device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool
       if (d.profile) slot_row(d, d.slot_peer[0], buf, gc)[1] = __longlong_as_double((long long)globaltimer());
     }
     const bool ok = arrive_wait(d, sh);  // (the partial store precedes lane 0's release)
+    // the polling warp sums the GG partials right after it sees the count (lane l: CTAs
+    // l, l+32, … in order, all loads in flight together; then a fixed shuffle tree):
+    // one CTA barrier after the detection instead of two (C2 mixed MGS −1.5 ms)
+    double x = 0.0;
+    if (ok) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int g = lane + 32 * u;
+        v[u] = g < d.GG ? __ldcg(slot_row(d, d.slots, buf, g)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x += v[u];
+      for (int g = lane + 256; g < d.GG; g += 32) x += __ldcg(slot_row(d, d.slots, buf, g));
+    }
+    x = warp_sum(x);
     if (lane == 0) {
+      sh.red2[0] = x;
       sh.abort = ok ? 0 : 1;
       sh.red_epoch++;
     }
   }
-  __syncthreads();
-  double x = 0.0;
-  for (int g = threadIdx.x; g < d.GG; g += NT) x += __ldcg(slot_row(d, d.slots, buf, g));
-  const int nwp = min(NW, (d.GG + 31) >> 5);
-  if (warp < nwp) {
-    x = warp_sum(x);
-    if (lane == 0) sh.red2[warp] = x;
+  if (d.profile && sh.cta == 0) {
+    __syncthreads();
+    ar_probe(d, sh, buf);
   }
-  if (d.profile && sh.cta == 0) ar_probe(d, sh, buf);
   __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < nwp; ++w) s += sh.red2[w];
-  out = s;
+  out = sh.red2[0];
   if (d.profile && sh.cta == 0 && threadIdx.x == 0) {  // prof[11] Σ arrival spread, [12] Σ last arrival → result, [13] count
     d.prof[11] += sh.pmax - sh.pmin;
     d.prof[12] += globaltimer() - sh.pmax;
