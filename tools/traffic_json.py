@@ -40,3 +40,6 @@ for ortho, rep in (("mgs", sys.argv[1]), ("cgsr", sys.argv[2])):
                   "ratio": (rd + wr) / alg, "kernel_ms": t * 1e3, "algorithmic_GBps": alg / t / 1e9,
                   "dram_GBps": (rd + wr) / t / 1e9}
 print(json.dumps(out, indent=1))
+with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json"), "w") as f:
+    json.dump(out, f, indent=1)
+    f.write("\n")
