@@ -84,7 +84,7 @@ typedef struct {
   double stall_factor;    /* ≤ 0 → 1.001; else must be > 1 (EINVAL)      */
   double stall_frac;      /* ≤ 0 → 0.05                                */
   double orth_thresh;     /* restart_policy 3 ORTHLOSS: THRESHOLD plus a restart when
-                             ‖S_k‖_F ≥ orth_thresh, S_k = (I+U_k)⁻¹U_k, U_k = strict upper
+                             ‖S_k‖ ≥ orth_thresh (orth_norm), S_k = (I+U_k)⁻¹U_k, U_k = strict upper
                              part of V_kᵀV_k; ≤ 0 → 1.0.  Adds
                              one pass over the basis per inner iteration               */
   int32_t precond;        /* left preconditioner M: GMRES_PRECOND_JACOBI (0, default;
@@ -95,6 +95,9 @@ typedef struct {
                              ILU(0) of RN32(A), applied as RN32(in) → fp32 solves → fp64:
                              the paper's "single-precision ILU" arm, PAPER.md:428, 444,
                              463).  ILU(0): single-rank contexts, restart policies 0–2  */
+  int32_t orth_norm;      /* restart_policy 3: the norm of S_k — 0 Frobenius (default), 1
+                             spectral, estimated by 10 power iterations on S_kᵀS_k from
+                             x = (1,…,1)/√k; EINVAL otherwise            */
 } gmres_opts;
 
 #define GMRES_PRECOND_JACOBI 0

@@ -74,6 +74,7 @@ struct gmres_ctx {
   size_t slots_count = 0;
   double* d_R = nullptr;
   double* d_umat = nullptr;  // orthogonality monitor U (policy 3)
+  double* d_smat = nullptr;  // ... and S = (I+U)⁻¹U (spectral norm)
   double* d_y = nullptr;
   int* d_flags = nullptr;  // [0] abort [1] err [2] scratch
   int* d_out_int = nullptr;
@@ -557,6 +558,7 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   const size_t oR = take(sizeof(double) * kmax * m);
   const size_t oy = take(sizeof(double) * kmax);
   const size_t oum = take(sizeof(double) * (m + 1) * (m + 1));
+  const size_t osm = take(sizeof(double) * (m + 1) * (m + 1));
   const size_t ofl = take(sizeof(int) * 8);
   const size_t ooi = take(sizeof(int) * 8);
   const size_t ood = take(sizeof(double) * 4);
@@ -579,6 +581,7 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   ctx->d_R = (double*)(ctx->d_ws + oR);
   ctx->d_y = (double*)(ctx->d_ws + oy);
   ctx->d_umat = (double*)(ctx->d_ws + oum);
+  ctx->d_smat = (double*)(ctx->d_ws + osm);
   ctx->d_flags = (int*)(ctx->d_ws + ofl);
   ctx->d_out_int = (int*)(ctx->d_ws + ooi);
   ctx->d_out_dbl = (double*)(ctx->d_ws + ood);
@@ -1161,6 +1164,8 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   const int policy = opts ? opts->restart_policy : 0;
   if (policy < 0 || policy > 3) return fail(ctx, GMRES_EINVAL, "restart_policy must be 0, 1, 2 or 3");
   const double orth_thresh = (opts && opts->orth_thresh > 0.0) ? opts->orth_thresh : 1.0;
+  const int orth_norm = opts ? opts->orth_norm : 0;
+  if (orth_norm != 0 && orth_norm != 1) return fail(ctx, GMRES_EINVAL, "orth_norm must be 0 (Frobenius) or 1 (spectral)");
   double delta = (opts && opts->delta >= 0.0) ? opts->delta
                                               : (precision == GMRES_MIXED && policy != 2 ? 1e-6 : 0.0);
   if (!std::isfinite(delta)) return fail(ctx, GMRES_EINVAL, "delta must be finite");
@@ -1288,6 +1293,8 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   d.stall_factor = stall_factor;
   d.orth_thresh = orth_thresh;
   d.Umat = ctx->d_umat;
+  d.Smat = ctx->d_smat;
+  d.orth_spec = orth_norm;
   d.inner_cap = inner_cap_dev;
   d.profile = (opts && opts->profile) ? 1 : 0;
   d.tile_bytes = tile_bytes;

@@ -146,6 +146,8 @@ struct Dev {
   int policy;           // restart policy (readings R22, R23): 0 threshold, 1 two-stage, 2 stall, 3 orth. loss
   double orth_thresh;   // policy 3: restart when ‖S_k‖_F ≥ orth_thresh
   double* Umat;         // policy 3: strict upper part of V_kᵀV_k, (m+1)×(m+1) column-major (CTA 0 writes)
+  double* Smat;         // policy 3, spectral: S_k's columns, same layout (CTA 0 writes)
+  int orth_spec;        // policy 3: 0 ‖S_k‖_F, 1 ‖S_k‖₂ by 10 power iterations
   int stall_w;          // stall window (inner iterations), policy 2
   double stall_factor;  // stall improvement factor, policy 2
   double* history; int hist_cap;
@@ -2608,6 +2610,50 @@ __device__ __forceinline__ double orth_column(double* Umat, int ldu, int l, bool
   return s_part[0];
 }
 
+// Spectral norm of S_k (policy 3, orth_norm 1, reading R23): 10
+// power iterations on SᵀS from x = (1,…,1)/√k, k = l + 1, columns 0..l−1 of S
+// from Smat (stored by CTA 0 in earlier inner steps, published by the
+// all-reduces since), column l = s_col (this step's, in shared memory); then
+// ‖S x‖ — the oracle's OrthMonitor::append step by step (each element's sum in
+// the same order; the norms as block sums).  Identical in every CTA.  s_x, s_v:
+// shared scratch of k doubles each.
+static __device__ __noinline__ double spec_norm(const double* Smat, int ld, int l, const double* s_col, double* s_x,
+                                         double* s_v, Shm& sh, double* s_part) {
+  const int k = l + 1;
+  auto S = [&](int i, int q) -> double { return q == l ? s_col[i] : __ldcg(Smat + (size_t)q * ld + i); };
+  const double x0 = 1.0 / sqrt((double)k);
+  for (int i = threadIdx.x; i < k; i += NT) s_x[i] = x0;
+  __syncthreads();
+  for (int it = 0; it < 10; ++it) {
+    for (int i = threadIdx.x; i < k; i += NT) {  // y = S x (S strictly upper triangular)
+      double t = 0.0;
+      for (int q = i + 1; q < k; ++q) t += S(i, q) * s_x[q];
+      s_v[i] = t;
+    }
+    __syncthreads();
+    double f[1] = {0.0};
+    for (int q = threadIdx.x; q < k; q += NT) {  // x = Sᵀ y
+      double t = 0.0;
+      for (int i = 0; i < q; ++i) t += S(i, q) * s_v[i];
+      s_x[q] = t;
+      f[0] += t * t;
+    }
+    block_sum<1>(f, sh, s_part);  // (its barriers also publish s_x)
+    const double nx = sqrt(s_part[0]);
+    if (nx == 0.0) return 0.0;
+    for (int q = threadIdx.x; q < k; q += NT) s_x[q] /= nx;
+    __syncthreads();
+  }
+  double f[1] = {0.0};
+  for (int i = threadIdx.x; i < k; i += NT) {
+    double t = 0.0;
+    for (int q = i + 1; q < k; ++q) t += S(i, q) * s_x[q];
+    f[0] += t * t;
+  }
+  block_sum<1>(f, sh, s_part);
+  return sqrt(s_part[0]);
+}
+
 // ---------------------------------------------------------- the solve
 // One launch runs the whole restarted solve of one rank (d = ds.d[0], G CTAs)
 // or of ds.nv "virtual ranks" on one device (rank v = CTAs [v·G, (v+1)·G)):
@@ -2773,8 +2819,17 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       tick(PH_ORTHO);
       // ------------ orthogonality monitor (policy 3, reading R23): the new column
       // of S_k = (I+U_k)⁻¹U_k by unit upper back-substitution, ‖S‖_F² accumulated
-      if (MON && d.policy == 3 && NN > 0.0) mon_fro2 += orth_column(d.Umat, d.m + 1, j, cta_ == 0, s_y, sh, s_part);
-      const bool orth = MON && d.policy == 3 && sqrt(mon_fro2) >= d.orth_thresh;
+      double mon_spec = 0.0;
+      if (MON && d.policy == 3 && NN > 0.0) {
+        mon_fro2 += orth_column(d.Umat, d.m + 1, j, cta_ == 0, s_y, sh, s_part);
+        if (d.orth_spec) {  // S's new column j (rows 0..j−1, in s_y): store it (CTA 0), then ‖S‖₂
+          mon_spec = spec_norm(d.Smat, d.m + 1, j, s_y, s_tmp, s_tmp + d.kmax + 1, sh, s_part);
+          if (cta_ == 0)
+            for (int i = threadIdx.x; i < j; i += NT) d.Smat[(size_t)j * (d.m + 1) + i] = s_y[i];
+          __syncthreads();
+        }
+      }
+      const bool orth = MON && d.policy == 3 && (d.orth_spec ? mon_spec : sqrt(mon_fro2)) >= d.orth_thresh;
       // ------------ h_{j+1,j}, Givens, exit test (lines 104, 108–140, 98)
       const double hn = sqrt(NN);
       if (threadIdx.x == 0) {

@@ -20,6 +20,7 @@ _lib = None
 MGS, CGSR = 0, 1
 JACOBI, ILU0, ILU0_FP32 = 0, 1, 2   # preconditioners (gmres_opts.precond; ILU0_FP32: fp64 solver, fp32 ILU)
 THRESHOLD, TWOSTAGE, STALL, ORTHLOSS = 0, 1, 2, 3   # restart policies (gmres_opts.restart_policy)
+FROBENIUS, SPECTRAL = 0, 1                          # gmres_opts.orth_norm (policy 3)
 FP64, MIXED = 0, 1
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "EBADCSR", -3: "EZERODIAG", -4: "EFP32RANGE",
           -5: "ENONFINITE", -6: "ENOMEM", -7: "ECUDA", -8: "ETIMEOUT"}
@@ -41,7 +42,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("delta", ctypes.c_double), ("max_cycles", ctypes.c_int32), ("record_inner", ctypes.c_int32),
                 ("lanes_per_row", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32), ("profile", ctypes.c_int32),
                 ("tune", ctypes.c_int32), ("restart_policy", ctypes.c_int32), ("stall_factor", ctypes.c_double),
-                ("stall_frac", ctypes.c_double), ("orth_thresh", ctypes.c_double), ("precond", ctypes.c_int32)]
+                ("stall_frac", ctypes.c_double), ("orth_thresh", ctypes.c_double), ("precond", ctypes.c_int32),
+                ("orth_norm", ctypes.c_int32)]
 
 
 def library_path() -> str:
@@ -228,8 +230,9 @@ class Solver:
 
     @staticmethod
     def _opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, profile=False, tune=0, policy=0,
-              stall_factor=0.0, stall_frac=0.0, orth_thresh=0.0, precond=0):
+              stall_factor=0.0, stall_frac=0.0, orth_thresh=0.0, precond=0, orth_norm=0):
         o = _Opts()
+        o.orth_norm = int(orth_norm)
         o.precond = int(precond)
         o.orth_thresh = float(orth_thresh)
         o.restart_policy = int(policy)
@@ -265,7 +268,7 @@ class Solver:
 
     def solve(self, b, x0=None, m=30, tol=1e-10, ortho=CGSR, precision=MIXED, delta=None, max_cycles=None,
               record_inner=False, lanes=0, ctas_per_sm=0, out=None, policy=THRESHOLD,
-              orth_thresh=0.0, precond=0, tune=0, stall_factor=0.0) -> SolveResult:
+              orth_thresh=0.0, precond=0, tune=0, stall_factor=0.0, orth_norm=0) -> SolveResult:
         """gmres_solve: host arrays in, host x out (h2d/d2h inside the call).  `out` may be a
         preallocated (e.g. pinned) float64 array of length n."""
         b = np.ascontiguousarray(b, np.float64)
@@ -280,7 +283,7 @@ class Solver:
         hl = ctypes.c_int32()
         res = _Result()
         o = self._opts(delta, max_cycles, record_inner, lanes, ctas_per_sm, tune=tune, policy=policy,
-                       orth_thresh=orth_thresh, precond=precond, stall_factor=stall_factor)
+                       orth_thresh=orth_thresh, precond=precond, stall_factor=stall_factor, orth_norm=orth_norm)
         rc = self._lib.gmres_solve(self._h, _p(b), _p(x0c), _p(x), int(m), float(tol), _ortho(ortho),
                                    _prec(precision), ctypes.byref(o), ctypes.byref(res), _p(hist), hist.size,
                                    ctypes.byref(hl))

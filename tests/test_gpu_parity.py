@@ -486,14 +486,18 @@ def test_stall_policy_matches_oracle(ortho):
         assert stall[0] == J[0]
 
 
-@pytest.mark.parametrize("thresh", [0.05, 1.0])
-def test_orthloss_policy_matches_oracle(thresh):
-    """f3 (reading R23): the device's Frobenius monitor ends the MGS cycles where the oracle's does."""
+@pytest.mark.parametrize("norm,thresh", [(0, 0.05), (0, 1.0), (1, 0.05), (1, 0.5)],
+                         ids=["fro-0.05", "fro-1.0", "spec-0.05", "spec-0.5"])
+def test_orthloss_policy_matches_oracle(norm, thresh):
+    """f3 (reading R23): the device's monitor — ‖S_k‖_F or ‖S_k‖₂ by 10 power iterations
+     — ends the MGS cycles where the oracle's does."""
     P = inputs.make("C2", 24)
     S = G.Solver.from_csr(P.A)
     m = 150
-    r = S.solve(P.b, m=m, ortho=G.MGS, precision=G.MIXED, policy=G.ORTHLOSS, orth_thresh=thresh, delta=0.0)
-    ref = O.solve(P.A, P.b, m=m, ortho=O.MGS, prec=O.MIXED, policy=O.ORTHLOSS, orth_thresh=thresh, delta=0.0)
+    r = S.solve(P.b, m=m, ortho=G.MGS, precision=G.MIXED, policy=G.ORTHLOSS, orth_thresh=thresh, delta=0.0,
+                orth_norm=norm)
+    ref = O.solve(P.A, P.b, m=m, ortho=O.MGS, prec=O.MIXED, policy=O.ORTHLOSS, orth_thresh=thresh, delta=0.0,
+                  orth_kind=norm)
     assert r.status == 0 and check_solution(P.A, P.b, r.x) <= 1e-10
     J, Jo = list(r.cycle_iters), _cycle_lengths(ref.inner)
     assert abs(J[0] - Jo[0]) <= 2, (J, Jo)
