@@ -1923,14 +1923,18 @@ __device__ __forceinline__ void combine_acc(const Dev& d, const double* s_acc, i
 // ------------------------------------------------------------------ a6
 // Alg. 1 lines 108–140 for step j (1-based) on h[0..j] (fp64, reading R4/R7):
 // apply rotations 1..j−1, form rotation j, rotate s.  Returns |s_{j+1}|.
-__device__ __forceinline__ double hess_step(int j, double* h, double* cs, double* sn, double* s) {
+// (the rotated h[i] is carried to the next rotation in a register: the chain no longer
+// goes through a shared-memory store and load per rotation — same operations)
+__device__ __forceinline__ double hess_step(int j, double* __restrict__ h, double* __restrict__ cs,
+                                            double* __restrict__ sn, double* __restrict__ s) {
+  double t1 = h[0];
   for (int i = 1; i <= j - 1; ++i) {
-    const double t1 = h[i - 1], t2 = h[i];
+    const double t2 = h[i];
     const double c = cs[i - 1], sg = sn[i - 1];
     h[i - 1] = __dadd_rn(__dmul_rn(c, t1), __dmul_rn(sg, t2));
-    h[i] = __dadd_rn(__dmul_rn(-sg, t1), __dmul_rn(c, t2));
+    t1 = __dadd_rn(__dmul_rn(-sg, t1), __dmul_rn(c, t2));
   }
-  const double a = h[j - 1], b = h[j];
+  const double a = t1, b = h[j];
   double c, sg, rho;
   if (b == 0.0) {
     c = 1.0; sg = 0.0; rho = a;
@@ -2835,10 +2839,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
       if (threadIdx.x == 0) {
         s_h[j] = hn;
         const double sabs = hess_step(j, s_h, s_cs, s_sn, s_s);
-        if (cta_ == 0) {
-          for (int i = 0; i <= j; ++i) d.R[(size_t)(j - 1) * (d.m + 1) + i] = s_h[i];
-          if (sh.inner_len < d.inner_cap) d.inner_hist[sh.inner_len] = sabs / sh.beta;
-        }
+        if (cta_ == 0 && sh.inner_len < d.inner_cap) d.inner_hist[sh.inner_len] = sabs / sh.beta;
         sh.inner_len++;
         s_rhs[j] = sabs;
         const bool stall = d.stall_w > 0 && j >= d.stall_w && sabs * d.stall_factor > s_rhs[j - d.stall_w];
@@ -2846,6 +2847,9 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
         sh.inv = 1.0 / hn;
       }
       __syncthreads();
+      // R's column j (CTA 0, all threads; s_h is next written after the next SpMV's barrier)
+      if (cta_ == 0)
+        for (int i = threadIdx.x; i <= j; i += NT) d.R[(size_t)(j - 1) * (d.m + 1) + i] = s_h[i];
       tick(PH_GIVENS);
       J = j;
       if (!isfinite(hn)) { status = ST_ENONFINITE; fail = true; break; }
@@ -2858,6 +2862,7 @@ __global__ void __launch_bounds__(NT, 1) solve_kernel(const __grid_constant__ De
     }
     if (lead && sh.kcyc < d.hist_cap) d.cycle_J[sh.kcyc] = J;
     // ------------ y = R⁻¹ s, x ← x + V_J y  (lines 143–147)
+    __syncthreads();  // (R's last column, stored by CTA 0's threads)
     if (cta_ == 0) backsolve_cta(J, d.R, d.m + 1, s_s, s_rhs, d.y, s_y);
     if (!grid_sync(d, sh)) { status = ST_ETIMEOUT; break; }
     for (int i = threadIdx.x; i < J; i += NT) s_y[i] = __ldcg(d.y + i);
