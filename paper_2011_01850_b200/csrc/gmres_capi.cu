@@ -553,7 +553,7 @@ int ensure_ws(gmres_ctx* ctx, int m, int prec, int G, int hist_cap, int inner_ca
   const size_t ow0 = take(wb * ctx->ldv);
   const size_t ow1 = take(wb * ctx->ldv);
   const size_t kst = (kmax + 3) & ~size_t(3);
-  const size_t oP = take(sizeof(double) * 2 * G * kst);
+  const size_t oP = take(sizeof(double) * (2 * G * kst + 2 * G));  // + the one-value partials
   const size_t octr = take(sizeof(unsigned long long) * 4);
   const size_t oR = take(sizeof(double) * kmax * m);
   const size_t oy = take(sizeof(double) * kmax);
@@ -812,6 +812,7 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
   d.w0 = ctx->d_w0;
   d.w1 = ctx->d_w1;
   d.slots = ctx->d_slots;
+  d.s1off = (long long)ctx->slots_count;  // the one-value partials follow the K-value rows
   d.ctr = ctx->d_ctr;
   for (int q = 0; q < MAXR; ++q) { d.slot_peer[q] = ctx->d_slots; d.ctr_peer[q] = ctx->d_ctr; }
   d.kst = (d.kmax + 3) & ~3;
@@ -984,7 +985,7 @@ int create_impl(const int32_t* row_ptr, const int32_t* col, const double* val, i
       CK(cudaMemset(ctx->d_gw0, 0, gb));
       CK(cudaMemset(ctx->d_gw1, 0, gb));
       CK(cudaMemset(ctx->d_gx, 0, gb));
-      const size_t sb = sizeof(double) * 2 * (size_t)nranks * ctx->sms * KST_MAX;
+      const size_t sb = sizeof(double) * (2 * (size_t)nranks * ctx->sms * KST_MAX + 2 * (size_t)nranks * ctx->sms);
       CK(cudaMalloc(&ctx->d_dslots, sb));
       CK(cudaMalloc(&ctx->d_dctr, 256));
       CK(cudaMemset(ctx->d_dctr, 0, 256));
@@ -1320,6 +1321,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
     d.GG = ctx->nranks * G;
     d.kst = (d.kmax + 3) & ~3;
     d.slots = ctx->d_dslots;
+    d.s1off = 2ll * ctx->nranks * ctx->sms * KST_MAX;
     d.ctr = ctx->d_dctr;
     for (int q = 0; q < MAXR; ++q) {
       d.slot_peer[q] = q < ctx->nranks ? ctx->peer_slots[q] : nullptr;
