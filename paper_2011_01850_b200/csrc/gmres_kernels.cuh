@@ -601,9 +601,9 @@ __device__ __forceinline__ bool grid_allreduce(const Dev& d, Shm& sh, const doub
   const int buf = sh.red_epoch & 1;
   push_partials(d, sh, s_part, K, buf);
   __syncthreads();
-  if (threadIdx.x < 32) {
+  if ((threadIdx.x >> 5) == 1) {  // warp 1 arrives and polls (warp 0 issues the row-tile passes' bulk copies)
     const bool ok = arrive_wait(d, sh);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 32) {
       sh.abort = ok ? 0 : 1;
       sh.red_epoch++;
     }
