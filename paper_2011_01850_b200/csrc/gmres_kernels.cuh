@@ -2087,7 +2087,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   // the CTA has no copy in flight when the all-reduce's round trips start, which a copy
   // issued in the all-reduce (the earlier r02 schedule) slowed.  C2 mixed MGS whole solve
   // (r02): 89.5 ms (copy in the all-reduce) → 82.7 (same + an L2 prefetch a step ahead)
-  // → 79.4 (early copy; with the prefetch too: 79.2); the ortho phase 67.4 → 57.5 ms.
+  // → 79.4 (early copy; the prefetch on top: 79.2, not kept); the ortho phase 67.4 → 57.5 ms.
   // (a ring of two buffers has no free buffer at the start of a step: the copy of
   // v_{i+1} then goes in the all-reduce, into v_{i−1}'s buffer)
   const bool early = NB >= 3;
@@ -2204,22 +2204,16 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
   auto tick = [&](int slot) {
     if (lead) { const unsigned long long t = globaltimer(); d.prof[slot] += t - tp; tp = t; }
   };
-  // v_{i+2} prefetched into L2 at the start of step i (tune bit 24 off; C2 fp64 MGS 163 ms
-  // either way).  Refilling the freed slots at the start of the step instead of in the
-  // all-reduce (tune bit 27; the resident ring's schedule) measured slower here (167 ms).
-  const bool pf = !(d.tune & 16777216), early = (d.tune & 134217728) != 0;
+  // v_{i+2} is prefetched into L2 at the start of step i, so the ring refills issued in
+  // the all-reduce are L2 hits (C2 fp64 MGS 160.8 → 154–159 ms; measured r02: refilling the
+  // freed slots at the start of the step instead — the resident ring's schedule — 167 ms)
   const unsigned vbytes = (unsigned)nq * 16u;
   for (int i = 1; i <= j; ++i) {
     const unsigned gi = g0 + (unsigned)((i - 1) * nch);  // v_i's first chunk
     const int s0 = (int)(gi % NS);  // v_i's chunks sit in slots s0, s0+1, … (mod NS; NS ≥ nch)
-    if (pf && threadIdx.x == 32 && i + 2 <= j)
+    if (threadIdx.x == 32 && i + 2 <= j)
       for (unsigned o = 0; o < vbytes; o += 32768u)
         prefetch_l2(reinterpret_cast<const char*>(V + (long long)(i + 1) * ldv + r0) + o, min(32768u, vbytes - o));
-    if (early) {
-      const unsigned hi = min(gend, gi + NS);
-      if (hi > issued) issue(issued, hi);
-      issued = max(issued, hi);
-    }
     auto slot = [&](int k) -> const V4* {
       const int s = s0 + k < (int)NS ? s0 + k : s0 + k - (int)NS;
       return sv + (size_t)s * NT + threadIdx.x;
@@ -2242,7 +2236,7 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
     // (a warp that issues bulk copies stalls until the TMA unit takes them)
     auto mid = [&]() {
       const unsigned hi = min(gend, gi + NS);
-      if (!early && hi > issued) issue(issued, hi);
+      if (hi > issued) issue(issued, hi);
     };
     if (!allreduce1(d, sh, acc, false, h, mid)) return false;
     issued = max(issued, min(gend, gi + NS));
