@@ -2356,6 +2356,11 @@ __device__ __forceinline__ bool mgs_stream(const Dev& d, Shm& sh, int r0, int r1
   const unsigned gend = g0 + 2u * (unsigned)j * (unsigned)nit;
   const unsigned long long pol_last = policy_evict_last();
   const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
+  // pass B runs over the items in reverse (tune bit 23: forward): it starts on the v_i
+  // and w rows pass A touched last — the ones still in L2 — and ends where the next
+  // pass A starts; the last step keeps the forward order (its ‖w‖² partial order).
+  // C4 mixed MGS (r02): ortho 1512 → 1391 ms
+  const bool rev = !((d.tune >> 23) & 1);
   // ---- producer (thread 0): cursor over (step ci, pass cp: 0 A / 1 B, item ck)
   unsigned issued = g0;
   int ci = 1, cp = 0, ck = 0;
@@ -2377,8 +2382,9 @@ __device__ __forceinline__ bool mgs_stream(const Dev& d, Shm& sh, int r0, int r1
     for (; issued < gend && issued < limit; ++issued) {
       const unsigned s = issued % NS;
       if (issued >= NS && !wait_bar(&sh.mbar_e[s], ((issued / NS) - 1u) & 1u)) return;
-      const unsigned bytes = (unsigned)min(MGS_IC * NT, nq - ck * MGS_IC * NT) * 16u;
-      const V4* src = reinterpret_cast<const V4*>(V + (long long)(ci - 1) * ldv + r0) + (size_t)ck * MGS_IC * NT;
+      const int cx = (cp && rev && ci < j) ? nit - 1 - ck : ck;  // B reversed (not the last step: ‖w‖² order)
+      const unsigned bytes = (unsigned)min(MGS_IC * NT, nq - cx * MGS_IC * NT) * 16u;
+      const V4* src = reinterpret_cast<const V4*>(V + (long long)(ci - 1) * ldv + r0) + (size_t)cx * MGS_IC * NT;
       mbar_expect_tx(&sh.mbar_v[s], bytes);
       tma_load_1d_hint(sv + (size_t)s * MGS_IC * NT, src, bytes, &sh.mbar_v[s], cp ? pol_first : pol_norm);
       if (++ck == nit) {
@@ -2411,82 +2417,81 @@ __device__ __forceinline__ bool mgs_stream(const Dev& d, Shm& sh, int r0, int r1
   }
   double nn = 0.0;
   for (int i = 1; i <= j; ++i) {
-    // ---- pass A: h_i = w·v_i
+    // ---- pass A (B = 0): h_i = w·v_i; pass B (B = 1): w ← w − h_i v_i (and ‖w‖²
+    // after the last step).  Global w is prefetched two items ahead in two register
+    // sets (one item ahead left the loads' L2 latency exposed once per item).
     double acc = 0.0;
-    {
-      V4 pf[MGS_IC];  // global w: the next item's vectors in flight
-      auto prefetch = [&](int it) {
-#pragma unroll
-        for (int c = 0; c < MGS_IC; ++c) {
-          const int t = (it * MGS_IC + c) * NT + threadIdx.x;
-          if (it < nit && it * MGS_IC >= MG && t < nq) pf[c] = ld_hint(wg + t, pol_last);
-        }
-      };
-      prefetch(MG / MGS_IC);
-      for (int it = 0; it < nit; ++it) {
-        V4 wv[MGS_IC];
-        const bool glob = it * MGS_IC >= MG;
-        if (glob) {
-#pragma unroll
-          for (int c = 0; c < MGS_IC; ++c) wv[c] = pf[c];
-          prefetch(it + 1);
-        } else {
-#pragma unroll
-          for (int c = 0; c < MGS_IC; ++c)
-            if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) wv[c] = ws[(it * MGS_IC + c) * NT + threadIdx.x];
-        }
-        const V4* x = acquire();
-#pragma unroll
-        for (int c = 0; c < MGS_IC; ++c)
-          if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) acc += dotv(wv[c], x[c * NT]);
-        release();
+    W hw = (W)0;
+    for (int B = 0; B < 2; ++B) {
+      if (B) {
+        double h;
+        auto mid = [&]() {
+          if (threadIdx.x == 0) pump(g + NS);  // A's items are all consumed: fill the ring with B's
+        };
+        const unsigned long long ta0 = lead ? globaltimer() : 0ull;
+        if (!allreduce1(d, sh, acc, false, h, mid)) return false;
+        if (lead) d.prof[13] += globaltimer() - ta0;  // profile: all-reduce (incl. the refill)
+        if (threadIdx.x == 0) s_h[i - 1] = h;
+        hw = RN<W>(h);
       }
-    }
-    double h;
-    auto mid = [&]() {
-      if (threadIdx.x == 0) pump(g + NS);  // A's items are all consumed: fill the ring with B's
-    };
-    const unsigned long long ta0 = lead ? globaltimer() : 0ull;
-    if (!allreduce1(d, sh, acc, false, h, mid)) return false;
-    if (lead) d.prof[13] += globaltimer() - ta0;  // profile: all-reduce (incl. the refill)
-    if (threadIdx.x == 0) s_h[i - 1] = h;
-    const W hw = RN<W>(h);
-    // ---- pass B: w ← w − h_i v_i (and ‖w‖² after the last step)
-    {
-      const bool last = i == j;
-      V4 pf[MGS_IC];
-      auto prefetch = [&](int it) {
+      const bool last = B && i == j;
+      const bool rb = B && rev && i < j;
+      V4 pf0[MGS_IC], pf1[MGS_IC];
 #pragma unroll
-        for (int c = 0; c < MGS_IC; ++c) {
-          const int t = (it * MGS_IC + c) * NT + threadIdx.x;
-          if (it < nit && it * MGS_IC >= MG && t < nq) pf[c] = ld_hint(wg + t, pol_last);
-        }
-      };
-      prefetch(MG / MGS_IC);
-      for (int it = 0; it < nit; ++it) {
-        V4 wv[MGS_IC];
-        const bool glob = it * MGS_IC >= MG;
-        if (glob) {
+      for (int o = 0; o < 2; ++o) {
+        V4(&pf)[MGS_IC] = o ? pf1 : pf0;
+        const int it = rb ? nit - 1 - o : o;
+        if (o < nit && it * MGS_IC >= MG) {
 #pragma unroll
-          for (int c = 0; c < MGS_IC; ++c) wv[c] = pf[c];
-          prefetch(it + 1);
-        } else {
-#pragma unroll
-          for (int c = 0; c < MGS_IC; ++c)
-            if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) wv[c] = ws[(it * MGS_IC + c) * NT + threadIdx.x];
-        }
-        const V4* x = acquire();
-#pragma unroll
-        for (int c = 0; c < MGS_IC; ++c) {
-          const int t = (it * MGS_IC + c) * NT + threadIdx.x;
-          if (t < nq) {
-            sub_scaled(wv[c], x[c * NT], hw);
-            if (last) nn += dotv(wv[c], wv[c]);
-            if (glob) st_hint(wg + t, wv[c], pol_last);
-            else ws[t] = wv[c];
+          for (int c = 0; c < MGS_IC; ++c) {
+            const int t = (it * MGS_IC + c) * NT + threadIdx.x;
+            if (t < nq) pf[c] = ld_hint(wg + t, pol_last);
           }
         }
-        release();
+      }
+      for (int i2 = 0; i2 < nit; i2 += 2) {
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          if (i2 + o < nit) {
+            V4(&pf)[MGS_IC] = o ? pf1 : pf0;
+            const int it = rb ? nit - 1 - (i2 + o) : i2 + o;
+            V4 wv[MGS_IC];
+            const bool glob = it * MGS_IC >= MG;
+            if (glob) {
+#pragma unroll
+              for (int c = 0; c < MGS_IC; ++c) wv[c] = pf[c];
+            } else {
+#pragma unroll
+              for (int c = 0; c < MGS_IC; ++c)
+                if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) wv[c] = ws[(it * MGS_IC + c) * NT + threadIdx.x];
+            }
+            const int n2 = i2 + o + 2;  // the item two ahead, into the set just read
+            const int itn = rb ? nit - 1 - n2 : n2;
+            if (n2 < nit && itn * MGS_IC >= MG) {
+#pragma unroll
+              for (int c = 0; c < MGS_IC; ++c) {
+                const int t = (itn * MGS_IC + c) * NT + threadIdx.x;
+                if (t < nq) pf[c] = ld_hint(wg + t, pol_last);
+              }
+            }
+            const V4* x = acquire();
+#pragma unroll
+            for (int c = 0; c < MGS_IC; ++c) {
+              const int t = (it * MGS_IC + c) * NT + threadIdx.x;
+              if (t < nq) {
+                if (!B) {
+                  acc += dotv(wv[c], x[c * NT]);
+                } else {
+                  sub_scaled(wv[c], x[c * NT], hw);
+                  if (last) nn += dotv(wv[c], wv[c]);
+                  if (glob) st_hint(wg + t, wv[c], pol_last);
+                  else ws[t] = wv[c];
+                }
+              }
+            }
+            release();
+          }
+        }
       }
     }
   }
