@@ -49,6 +49,7 @@ struct Args {
 __global__ void __launch_bounds__(NT, 1) kern(Args a) {
   __shared__ double red[NW], red2[NW];
   __shared__ unsigned long long epoch;
+  __shared__ double cred[8], cres;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = blockIdx.x, G = a.G;
   if (threadIdx.x == 0) epoch = 0;
   __syncthreads();
@@ -130,6 +131,59 @@ __global__ void __launch_bounds__(NT, 1) kern(Args a) {
       __syncthreads();
       acc_all += red2[0];
       e3 = e3 + 1;
+    } else if (a.variant >= 40) {
+      // cluster pre-reduction (C = variant mod 10 CTAs per cluster): CTA sums → DSMEM
+      // store into the leader's shared slot → cluster barrier → the leader pushes the
+      // cluster partial and arrives (G/C arrivals).  40+C: every CTA polls the counter
+      // and loads the G/C partials; 50+C: only the leaders do, then broadcast the
+      // result over DSMEM (second cluster barrier)
+      const int C = a.variant % 10;
+      const bool bcast = a.variant >= 50;
+      unsigned crank, cid;
+      asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+      asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+      v = warp_sum(v);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0; for (int w = 0; w < NW; ++w) s += red[w];
+        const unsigned loc = (unsigned)__cvta_generic_to_shared(&cred[crank]);
+        unsigned rem;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rem) : "r"(loc), "r"(0));
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rem), "d"(s) : "memory");
+      }
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+      const int GC = G / C;
+      double* P = a.parts + (size_t)(it & 1) * G;
+      const bool poll = !bcast || crank == 0;
+      if (warp == 0 && lane == 0) {
+        if (crank == 0) {
+          double s = 0; for (int r = 0; r < C; ++r) s += cred[r];
+          P[cid] = s;
+          red_rel(a.ctr, 1);
+        }
+        epoch += 1;
+        if (poll) { const unsigned long long target = epoch * (unsigned long long)GC; while (ld_acq(a.ctr) < target) {} }
+      }
+      __syncthreads();
+      double s = 0.0;
+      if (poll) {
+        double x = threadIdx.x < GC ? __ldcg(P + threadIdx.x) : 0.0;
+        if (warp < (GC + 31) / 32) { x = warp_sum(x); if (lane == 0) red2[warp] = x; }
+        __syncthreads();
+        for (int w = 0; w < (GC + 31) / 32; ++w) s += red2[w];
+      }
+      if (bcast) {
+        if (crank == 0 && threadIdx.x < C) {
+          const unsigned loc = (unsigned)__cvta_generic_to_shared(&cres);
+          unsigned rem;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rem) : "r"(loc), "r"(threadIdx.x));
+          asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rem), "d"(s) : "memory");
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        s = cres;
+      }
+      acc_all += s;
     } else if (a.variant >= 10) {
       // counter + partial load with the arrivals spread over NC = variant-10 counters
       // (256 B apart: different L2 slices); warp 0 lane c polls counter c
@@ -237,6 +291,10 @@ int main(int argc, char** argv) {
     {14, 1, "counters x4 + partial load"},
     {18, 1, "counters x8 + partial load"},
     {26, 1, "counters x16 + partial load"},
+    {42, 1, "cluster 2 pre-reduction, all CTAs poll + load"},
+    {44, 1, "cluster 4 pre-reduction, all CTAs poll + load"},
+    {52, 1, "cluster 2 pre-reduction, leader polls, DSMEM broadcast"},
+    {54, 1, "cluster 4 pre-reduction, leader polls, DSMEM broadcast"},
   };
   for (auto& v : vs) {
     if (only >= 0 && v.v != only) continue;
@@ -245,7 +303,23 @@ int main(int argc, char** argv) {
       fill<<<64, 256>>>((unsigned long long*)slots, (size_t)3 * G * maxstride, SENT);
       Args a{v.v, iters, G, v.stride, ctr, slots, parts, out};
       void* args[] = {&a};
-      cudaError_t e = cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(NT), args, 0, 0);
+      cudaError_t e;
+      if (v.v >= 40) {  // cooperative launch in clusters of C
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G); cfg.blockDim = dim3(NT);
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = v.v % 10; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeCooperative; at[1].val.cooperative = 1;
+        cfg.attrs = at; cfg.numAttrs = 2;
+        int ncl = 0;
+        cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg);
+        if (rep == 0) printf("  (max active clusters of %d: %d, need %d)\n", v.v % 10, ncl, G / (v.v % 10));
+        if (ncl * (v.v % 10) < G) { printf("%-55s cannot co-schedule %d CTAs\n", v.name, G); break; }
+        e = cudaLaunchKernelEx(&cfg, kern, a);
+      } else {
+        e = cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(NT), args, 0, 0);
+      }
       if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return 1; }
       e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("run: %s\n", cudaGetErrorString(e)); return 1; }
