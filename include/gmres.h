@@ -74,7 +74,9 @@ typedef struct {
                              only (EINVAL otherwise)                                  */
   int32_t ctas_per_sm;    /* 0 = auto (occupancy)                                       */
   int32_t profile;        /* != 0: grid barrier after each phase for clean phase timers */
-  int32_t tune;           /* developer A/B switches; 0 = production defaults            */
+  int32_t tune;           /* developer A/B switches; 0 = production defaults (bit 25: the
+                             mixed MGS projections use the fp64 partial all-reduce instead
+                             of the exact fixed-point word of DESIGN.md reading R27)       */
   int32_t restart_policy; /* 0 THRESHOLD: restart at j = m or |s_{j+1}| ≤ β·max(tol‖b‖/‖z‖, δ)
                              (PAPER.md:257-264); 1 TWOSTAGE: the first cycle as THRESHOLD,
                              later cycles at the first cycle's iteration count (PAPER.md:
@@ -244,7 +246,10 @@ int gmres_k_resid(gmres_ctx* ctx, int32_t precision, const double* d_b, const do
  * the j columns of d_V (column-major, leading dimension ldv ≥ round_up(n, 256),
  * ldv % 64 == 0, rows ≥ n zero) with MGS or CGSR; h_out (host) receives
  * h_{1..j} and h_out[j] = ‖w‖₂.  CGSR copies V into the row-blocked layout a
- * CGSR solve keeps its basis in and runs on that copy. */
+ * CGSR solve keeps its basis in and runs on that copy.  Mixed MGS reduces the
+ * projections as the mixed solve does (reading R27: exact fixed-point
+ * sums, bound B = 2^⌈log2(2‖w‖₂)⌉ from this call's w, for orthonormal V);
+ * GMRES_ENONFINITE if a partial falls outside that bound (non-finite data). */
 int gmres_k_ortho(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j, const void* d_V, int64_t ldv,
                   void* d_w, double* h_out);
 /* The same with the MGS variant chosen: mgs_variant −1 = the one a solve on this

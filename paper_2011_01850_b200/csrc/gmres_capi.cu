@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -71,6 +72,8 @@ struct gmres_ctx {
   void* d_w1 = nullptr;
   double* d_slots = nullptr;      // grid all-reduce partials [2][G][kst]
   unsigned long long* d_ctr = nullptr;  // arrival counter
+  unsigned long long* d_fx = nullptr;   // fixed-point projection all-reduce words (reading R27), 1 KB
+  int fx_exp = INT_MIN;                 // B = 2^fx_exp ≥ 2·√(‖D⁻¹A‖₁‖D⁻¹A‖∞) (single-rank contexts)
   size_t slots_count = 0;
   double* d_R = nullptr;
   double* d_umat = nullptr;  // orthogonality monitor U (policy 3)
@@ -858,6 +861,7 @@ Dev make_dev(gmres_ctx* ctx, int m, int prec, int ortho, int G) {
 
 int reset_flags(gmres_ctx* ctx, cudaStream_t st) {
   CK(cudaMemsetAsync(ctx->d_ctr, 0, sizeof(unsigned long long) * 4, st));
+  if (ctx->d_fx) CK(cudaMemsetAsync(ctx->d_fx, 0, 1024, st));
   CK(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * 8, st));
   return 0;
 }
@@ -972,6 +976,30 @@ int create_impl(const int32_t* row_ptr, const int32_t* col, const double* val, i
       CK(cudaStreamSynchronize(ctx->stream));
       cudaFree(d_part);
     }
+    if (nranks == 1 && n > 0) {
+      // reading R27: a power-of-two bound B on every CTA partial of an MGS projection
+      // h = w·v_i of the mixed Jacobi solve: |w_c·v_c| ≤ ‖w‖‖v_i‖ and w = D⁻¹A v_j, so
+      // ‖w‖ ≤ ‖D⁻¹A‖₂ ≤ √(‖D⁻¹A‖₁‖D⁻¹A‖∞) (v normalised); ×2 covers the fp32 rounding
+      std::vector<double> csum((size_t)n, 0.0);
+      double rmax = 0.0;
+      for (int64_t i = 0; i < n; ++i) {
+        double di = 0.0, rs = 0.0;
+        for (int32_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+          rs += std::fabs(val[k]);
+          if (col[k] == i) di = val[k];
+        }
+        const double inv = 1.0 / std::fabs(di);
+        rmax = std::max(rmax, rs * inv);
+        for (int32_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) csum[(size_t)col[k]] += std::fabs(val[k]) * inv;
+      }
+      const double cmax = *std::max_element(csum.begin(), csum.end());
+      const double bnd = 2.0 * std::sqrt(cmax * rmax);
+      if (std::isfinite(bnd) && bnd > 0.0) {
+        ctx->fx_exp = (int)std::ceil(std::log2(bnd));
+        CK(cudaMalloc(&ctx->d_fx, 1024));
+        CK(cudaMemset(ctx->d_fx, 0, 1024));
+      }
+    }
     if (nranks > 1) {
       // ghost columns (host) and the buffers peers push into / read from
       for (int64_t i = 0; i < nnz; ++i)
@@ -1010,6 +1038,7 @@ void gmres_destroy(gmres_ctx* ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_rp);
+  cudaFree(ctx->d_fx);
   cudaFree(ctx->d_ci);
   cudaFree(ctx->d_a64);
   cudaFree(ctx->d_a32);
@@ -1313,6 +1342,13 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   set_vlayout(d, vl);
   d.tune = opts ? opts->tune : 0;
   if (d.tune & 4194304) d.merge_stream = 0;  // dev A/B: chunk stream instead of the merge-path stream
+  // reading R27: exact fixed-point MGS projections in the mixed Jacobi solve on one rank
+  // (tune bit 25: the fp64 partial all-reduce instead, dev A/B)
+  if (precision == GMRES_MIXED && !ilu && !virt && !ctx->dist() && ctx->d_fx && G <= 600 && !(d.tune & 33554432)) {
+    d.fx = 1;
+    d.fx_exp = ctx->fx_exp;
+    d.fx_words = ctx->d_fx;
+  }
   if (ctx->dist()) {
     const size_t wb = precision == GMRES_MIXED ? 4 : 8;
     d.nranks = ctx->nranks;
@@ -1858,6 +1894,21 @@ int gmres_k_ortho_ex(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j
   Dev d = make_dev(ctx, m, precision, ortho, G);
   set_vlayout(d, vl);
   if (vl.tb) d_V = ctx->d_V;
+  if (precision == GMRES_MIXED && ortho == GMRES_MGS && ctx->d_fx) {
+    // the mixed solve's fixed-point projections (reading R27), with the bound taken from
+    // this call's w (the callers pass orthonormal bases, ‖v_i‖ ≤ 1): B = 2^⌈log2(2‖w‖)⌉
+    std::vector<float> hw((size_t)ctx->n);
+    CK(cudaMemcpy(hw.data(), d_w, sizeof(float) * ctx->n, cudaMemcpyDeviceToHost));
+    double ss = 0.0;
+    for (float v : hw) ss += (double)v * (double)v;
+    const double bnd = 2.0 * std::sqrt(ss);
+    if (bnd > 0.0 && std::isfinite(bnd)) {
+      d.fx = 1;
+      d.fx_exp = (int)std::ceil(std::log2(bnd));
+      d.fx_words = ctx->d_fx;
+      CK(cudaMemsetAsync(ctx->d_fx, 0, 1024, ctx->stream));
+    }
+  }
   int used = -1;
   if (ortho == GMRES_MGS) {  // the MGS variant the solve would run (or the one requested)
     MgsPlan mp;
@@ -1888,9 +1939,10 @@ int gmres_k_ortho_ex(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j
     if (e != cudaSuccess) rc = fail(ctx, GMRES_ECUDA, cudaGetErrorString(e));
   }
   cudaFree(d_h);
-  int fl = 0;
-  cudaMemcpy(&fl, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost);
-  if (rc == 0 && fl) rc = fail(ctx, GMRES_ETIMEOUT, "device watchdog fired");
+  int fl[2] = {0, 0};
+  cudaMemcpy(fl, ctx->d_flags, sizeof(int) * 2, cudaMemcpyDeviceToHost);
+  if (rc == 0 && fl[0]) rc = fail(ctx, GMRES_ETIMEOUT, "device watchdog fired");
+  if (rc == 0 && fl[1]) rc = fail(ctx, GMRES_ENONFINITE, "a projection partial exceeded its fixed-point bound (non-finite data)");
   return rc;
 }
 

@@ -184,6 +184,11 @@ struct Dev {
   double normA2;           // ‖A‖_F² of this rank's rows (backward-error report)
   int ilu32;               // fp64 solver with fp32 factors: iluW / ilu_rec are fp32
   float* ilu_s32[2];       // ... and its fp32 scratch vectors (right-hand side, solution)
+  // exact fixed-point MGS projections (reading R27; mixed, Jacobi, one rank): 4 words
+  // 256 B apart, zeroed before each launch; partials quantised to 2^(fx_exp−42)
+  int fx;                  // != 0: the MGS projection all-reduces use allreduce1's fixed-point word
+  int fx_exp;              // B = 2^fx_exp ≥ 2·√(‖D⁻¹A‖₁‖D⁻¹A‖∞) ≥ |every CTA partial|
+  unsigned long long* fx_words;
 };
 
 // ------------------------------------------------------------ primitives
@@ -364,6 +369,7 @@ struct Shm {
   unsigned long long epoch;          // grid barriers passed by this CTA (thread 0)
   int cta;                           // CTA index within its rank (blockIdx.x unless virtual ranks)
   int red_epoch;                     // all-reduces done (partial buffer parity; thread 0 writes)
+  unsigned fx_epoch;                 // fixed-point projection all-reduces done (word e mod 4)
   double red[NW * 8];
   double red2[NW * 4];
   unsigned long long pmin, pmax;     // profile mode: all-reduce arrival spread (ar_probe)
@@ -400,6 +406,7 @@ __device__ __forceinline__ void init_shm(Shm& sh, int cta) {
     sh.cta = cta;
     sh.epoch = 0;
     sh.red_epoch = 0;
+    sh.fx_epoch = 0;
     sh.abort = 0;
     sh.flag = 0;
     sh.vg = 0;
@@ -534,7 +541,54 @@ static __device__ __noinline__ void ar_probe(const Dev& d, Shm& sh, int buf) {
 struct NoMid { __device__ __forceinline__ void operator()() const {} };
 // mid() runs in every thread right after the CTA barrier that follows the
 // local contributions (e.g. to reuse a buffer the contributions were read from)
-template <class Mid = NoMid>
+// Fixed-point variant (FX, MGS projections only, d.fx: reading R27): the CTA partial s
+// is quantised to q = RN(s·2^(42−e)), |q| ≤ 2^42 (B = 2^e bounds every partial), and
+// one 64-bit red.add carries the arrival and the value: count in bits 53–63, the
+// offset-binary sum Σ(q + 2^43) below (< 2^51 for ≤ 600 CTAs).  The integer sum is
+// exact, so every CTA reads the same word and gets the same h whatever the order of
+// arrival — one round trip after the last arrival instead of the partial store's
+// release, the counter and the partial loads (tools/ar_bench.cu 1.33 vs 1.80–1.99 µs).
+// Words rotate mod 4; CTA 0 zeroes the word two epochs ahead (all CTAs finished
+// reading it) and alone arrives with release, which orders that zeroing before the
+// adds of the epoch that reuses the word (the pollers acquire by a fence).
+__device__ __forceinline__ void red_relaxed_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool fx_arrive_wait(const Dev& d, Shm& sh, double s, double& out) {  // one thread
+  const unsigned e = sh.fx_epoch;
+  unsigned long long* wd = d.fx_words + (size_t)(e & 3u) * 32;
+  long long q = 0;
+  if (fabs(s) <= ldexp(1.0, d.fx_exp)) q = llrint(ldexp(s, 42 - d.fx_exp));
+  else atomicOr(d.err_flag, ERRF_NONFINITE);  // non-finite (the bound holds for finite data)
+  const unsigned long long add = (1ull << 53) + (unsigned long long)(q + (1ll << 43));
+  if (sh.cta == 0) red_release_add(wd, add, false);
+  else red_relaxed_add(wd, add);
+  const unsigned long long GG = (unsigned long long)d.GG;
+  unsigned long long x;
+  unsigned it = 0;
+  unsigned long long t0 = 0;
+  bool ok = true;
+  while (((x = ld_relaxed_u64(wd)) >> 53) < GG) {
+    if (((++it) & 1023u) == 0u) {
+      if (*(volatile int*)d.abort_flag) { ok = false; break; }
+      const unsigned long long t = globaltimer();
+      if (t0 == 0) t0 = t;
+      else if ((long long)(t - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); ok = false; break; }
+    }
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  const long long sum = (long long)(x & ((1ull << 53) - 1)) - (long long)GG * (1ll << 43);
+  out = ldexp((double)sum, d.fx_exp - 42);
+  if (sh.cta == 0) *(volatile unsigned long long*)(d.fx_words + (size_t)((e + 2u) & 3u) * 32) = 0ull;
+  sh.fx_epoch = e + 1u;
+  return ok && *(volatile int*)d.abort_flag == 0;
+}
+template <bool FX = false, class Mid = NoMid>
 __device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool /*acq*/, double& out,
                                            Mid mid = Mid()) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -543,6 +597,22 @@ __device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool
   if (lane == 0) sh.red[warp] = v;
   __syncthreads();
   mid();
+  if (FX && d.fx) {
+    if (warp == 1) {
+      double s = lane < NW ? sh.red[lane] : 0.0;
+#pragma unroll
+      for (int o = NW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        double x = 0.0;
+        const bool ok = fx_arrive_wait(d, sh, s, x);
+        sh.red2[0] = x;
+        sh.abort = ok ? 0 : 1;
+      }
+    }
+    __syncthreads();
+    out = sh.red2[0];
+    return sh.abort == 0;
+  }
   if (warp == 1) {  // (warp 1 releases: warp 0 may hold in-flight bulk copies, see mgs_resident)
     double s = lane < NW ? sh.red[lane] : 0.0;  // fixed shuffle tree over the warps
 #pragma unroll
@@ -2138,7 +2208,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     auto mid = [&]() {
       if (!early && threadIdx.x == TMA_T && i + NB - 1 <= j) issue(i + NB - 1);  // into v_{i−1}'s buffer
     };
-    if (!allreduce1(d, sh, acc, false, h, mid)) return false;
+    if (!allreduce1<true>(d, sh, acc, false, h, mid)) return false;
     if (threadIdx.x == 0) s_h[i - 1] = h;
     hprev = RN<W>(h);
     tick(10);
@@ -2264,7 +2334,7 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
       const unsigned hi = min(gend, gi + NS);
       if (hi > issued) issue(issued, hi);
     };
-    if (!allreduce1(d, sh, acc, false, h, mid)) return false;
+    if (!allreduce1<true>(d, sh, acc, false, h, mid)) return false;
     issued = max(issued, min(gend, gi + NS));
     if (threadIdx.x == 0) s_h[i - 1] = h;
     const W hw = RN<W>(h);
@@ -2326,6 +2396,10 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
 // Same operations and order per element and per thread partial as mgs_sweep /
 // mgs_resident (bit-identical solves).
 constexpr int MGS_IC = 4;                       // chunks per streamed item (32 KB)
+#ifndef G200_PS
+#define G200_PS 2
+#endif
+constexpr int MGS_PS = G200_PS;                 // register sets of global w in flight (items ahead)
 constexpr int MGS_ITEM = MGS_IC * MGS_CHUNK;
 __device__ __forceinline__ float4 ld_hint(const float4* p, unsigned long long pol) {
   float4 v;
@@ -2429,17 +2503,17 @@ __device__ __forceinline__ bool mgs_stream(const Dev& d, Shm& sh, int r0, int r1
           if (threadIdx.x == 0) pump(g + NS);  // A's items are all consumed: fill the ring with B's
         };
         const unsigned long long ta0 = lead ? globaltimer() : 0ull;
-        if (!allreduce1(d, sh, acc, false, h, mid)) return false;
+        if (!allreduce1<true>(d, sh, acc, false, h, mid)) return false;
         if (lead) d.prof[13] += globaltimer() - ta0;  // profile: all-reduce (incl. the refill)
         if (threadIdx.x == 0) s_h[i - 1] = h;
         hw = RN<W>(h);
       }
       const bool last = B && i == j;
       const bool rb = B && rev && i < j;
-      V4 pf0[MGS_IC], pf1[MGS_IC];
+      V4 pfs[MGS_PS][MGS_IC];
 #pragma unroll
-      for (int o = 0; o < 2; ++o) {
-        V4(&pf)[MGS_IC] = o ? pf1 : pf0;
+      for (int o = 0; o < MGS_PS; ++o) {
+        V4(&pf)[MGS_IC] = pfs[o];
         const int it = rb ? nit - 1 - o : o;
         if (o < nit && it * MGS_IC >= MG) {
 #pragma unroll
@@ -2449,11 +2523,11 @@ __device__ __forceinline__ bool mgs_stream(const Dev& d, Shm& sh, int r0, int r1
           }
         }
       }
-      for (int i2 = 0; i2 < nit; i2 += 2) {
+      for (int i2 = 0; i2 < nit; i2 += MGS_PS) {
 #pragma unroll
-        for (int o = 0; o < 2; ++o) {
+        for (int o = 0; o < MGS_PS; ++o) {
           if (i2 + o < nit) {
-            V4(&pf)[MGS_IC] = o ? pf1 : pf0;
+            V4(&pf)[MGS_IC] = pfs[o];
             const int it = rb ? nit - 1 - (i2 + o) : i2 + o;
             V4 wv[MGS_IC];
             const bool glob = it * MGS_IC >= MG;
@@ -2465,7 +2539,7 @@ __device__ __forceinline__ bool mgs_stream(const Dev& d, Shm& sh, int r0, int r1
               for (int c = 0; c < MGS_IC; ++c)
                 if ((it * MGS_IC + c) * NT + (int)threadIdx.x < nq) wv[c] = ws[(it * MGS_IC + c) * NT + threadIdx.x];
             }
-            const int n2 = i2 + o + 2;  // the item two ahead, into the set just read
+            const int n2 = i2 + o + MGS_PS;  // the item MGS_PS ahead, into the set just read
             const int itn = rb ? nit - 1 - n2 : n2;
             if (n2 < nit && itn * MGS_IC >= MG) {
 #pragma unroll
@@ -2573,7 +2647,7 @@ __device__ bool ortho_phase(const Dev& d, Shm& sh, int r0, int r1, int j, const 
       // (issued by warp 1: warp 0's release fence in the all-reduce must not wait on it)
       if (pf && i < j && threadIdx.x == 32) prefetch_l2(V + (long long)i * ldv + r0, pf_bytes);
       double h;
-      if (!allreduce1(d, sh, acc, false, h)) return false;
+      if (!allreduce1<true>(d, sh, acc, false, h)) return false;
       if (threadIdx.x == 0) s_h[i - 1] = h;
       hprev = RN<W>(h);
     }

@@ -523,3 +523,54 @@ def test_table1_stall_points_match_oracle(name, scale, m):
         assert abs(a - b) <= max(2, 0.2 * b), row      # ±20 %
     assert max(g) - min(g) <= max(3, 0.2 * max(g)), row   # about the same after each restart
 
+
+
+# ------------------------------------------------------------------ reading R27
+FX_OFF = 1 << 25  # tune bit: the fp64 partial all-reduce instead of the fixed-point word
+
+
+@pytest.mark.parametrize("name,scale,rowscale", [("C1", None, 1.0), ("C2", 24, 1.0), ("C3", 20000, 1.0),
+                                                 ("C1", None, 1e8)], ids=["c1", "c2mini", "c3mini", "c1_scaled"])
+def test_fixed_point_projections(name, scale, rowscale):
+    """Reading R27: the mixed solve's MGS projections sum per-CTA partials quantised to
+    2^-42·B (B ≥ 2√(‖D⁻¹A‖₁‖D⁻¹A‖∞), a power of two) as exact integers.  Against the fp64
+    partial all-reduce (tune bit 25) and the oracle: same cycles, the first cycle's Arnoldi
+    residuals equal far inside the fp32 rounding of w, x to 1e-10.  Rows scaled by 1e8 leave
+    D⁻¹A — and so B and the quantisation — unchanged (the bound is Jacobi-scale invariant)."""
+    P = inputs.make(name, scale)
+    A, b = P.A, P.b
+    if rowscale != 1.0:
+        rs = rowscale ** np.linspace(0.0, 1.0, A.n)  # rows scaled by 1 … 1e8
+        A = inputs.CSR(A.row_ptr, A.col, A.val * np.repeat(rs, np.diff(A.row_ptr)))
+        b = b * rs
+    S = G.Solver.from_csr(A)
+    m = min(P.m, 50)
+    r_fx = S.solve(b, m=m, ortho=G.MGS, precision=G.MIXED, record_inner=True)
+    r_64 = S.solve(b, m=m, ortho=G.MGS, precision=G.MIXED, record_inner=True, tune=FX_OFF)
+    ref = O.solve(A, b, m=m, tol=1e-10, ortho=G.MGS, prec=G.MIXED)
+    assert r_fx.status == 0 and r_64.status == 0, (r_fx.status_name, r_64.status_name)
+    assert check_solution(A, b, r_fx.x) <= 1e-10
+    assert r_fx.cycles == r_64.cycles
+    assert abs(r_fx.cycles - ref.cycles) <= 0.1 * ref.cycles, (r_fx.cycles, ref.cycles)
+    J = int(r_fx.cycle_iters[0])
+    a, c = r_fx.inner[:J], r_64.inner[:J]
+    mask = c > 1e-5 * c[0]
+    assert np.all(np.abs(a[mask] - c[mask]) <= 1e-4 * c[mask])
+
+
+def test_fixed_point_projection_nonfinite_flagged():
+    """Reading R27: a partial outside the bound (only non-finite data can produce one) sets
+    the error flag; the component entry point reports GMRES_ENONFINITE."""
+    A = inputs.make("C1").A
+    S = G.Solver.from_csr(A)
+    n, j = A.n, 4
+    ld = G.ld_for(n)
+    rng = np.random.default_rng(5)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, j)))
+    Vpad = np.zeros((j, ld), np.float32)
+    Vpad[:, :n] = Q.T
+    Vpad[2, 7] = np.nan
+    w0 = rng.standard_normal(n).astype(np.float32)
+    with pytest.raises(G.GmresError) as e:
+        S.k_ortho(G.MIXED, G.MGS, j, tdev(Vpad), ld, tdev(w0))
+    assert "fixed-point" in str(e.value) or "NONFINITE" in str(e.value).upper()
