@@ -228,6 +228,18 @@ VLayout vlayout_for(int ortho, int m, int wb, int tile_bytes) {
   return L;
 }
 
+// fixed-point projection all-reduce (reading R27): B = 2^e and its exact scalings; the
+// exponent range keeps 2^(42−e) and 2^(e−42) normal (else the fp64 all-reduce is used)
+void set_fx(Dev& d, int e, unsigned long long* words) {
+  if (e < -900 || e > 900) return;
+  d.fx = 1;
+  d.fx_exp = e;
+  d.fx_bnd = std::ldexp(1.0, e);
+  d.fx_up = std::ldexp(1.0, 42 - e);
+  d.fx_dn = std::ldexp(1.0, e - 42);
+  d.fx_words = words;
+}
+
 void set_vlayout(Dev& d, const VLayout& vl) {
   d.vtb = vl.tb;
   d.vtp = vl.tp;
@@ -1345,9 +1357,7 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   // reading R27: exact fixed-point MGS projections in the mixed Jacobi solve on one rank
   // (tune bit 25: the fp64 partial all-reduce instead, dev A/B)
   if (precision == GMRES_MIXED && !ilu && !virt && !ctx->dist() && ctx->d_fx && G <= 600 && !(d.tune & 33554432)) {
-    d.fx = 1;
-    d.fx_exp = ctx->fx_exp;
-    d.fx_words = ctx->d_fx;
+    set_fx(d, ctx->fx_exp, ctx->d_fx);
   }
   if (ctx->dist()) {
     const size_t wb = precision == GMRES_MIXED ? 4 : 8;
@@ -1903,9 +1913,7 @@ int gmres_k_ortho_ex(gmres_ctx* ctx, int32_t precision, int32_t ortho, int32_t j
     for (float v : hw) ss += (double)v * (double)v;
     const double bnd = 2.0 * std::sqrt(ss);
     if (bnd > 0.0 && std::isfinite(bnd)) {
-      d.fx = 1;
-      d.fx_exp = (int)std::ceil(std::log2(bnd));
-      d.fx_words = ctx->d_fx;
+      set_fx(d, (int)std::ceil(std::log2(bnd)), ctx->d_fx);
       CK(cudaMemsetAsync(ctx->d_fx, 0, 1024, ctx->stream));
     }
   }

@@ -184,10 +184,11 @@ struct Dev {
   double normA2;           // ‖A‖_F² of this rank's rows (backward-error report)
   int ilu32;               // fp64 solver with fp32 factors: iluW / ilu_rec are fp32
   float* ilu_s32[2];       // ... and its fp32 scratch vectors (right-hand side, solution)
-  // exact fixed-point MGS projections (reading R27; mixed, Jacobi, one rank): 4 words
+  // exact fixed-point MGS projections (reading R27; mixed, Jacobi, one rank): 2 words
   // 256 B apart, zeroed before each launch; partials quantised to 2^(fx_exp−42)
   int fx;                  // != 0: the MGS projection all-reduces use allreduce1's fixed-point word
   int fx_exp;              // B = 2^fx_exp ≥ 2·√(‖D⁻¹A‖₁‖D⁻¹A‖∞) ≥ |every CTA partial|
+  double fx_bnd, fx_up, fx_dn;  // 2^fx_exp, 2^(42−fx_exp), 2^(fx_exp−42)
   unsigned long long* fx_words;
 };
 
@@ -369,7 +370,8 @@ struct Shm {
   unsigned long long epoch;          // grid barriers passed by this CTA (thread 0)
   int cta;                           // CTA index within its rank (blockIdx.x unless virtual ranks)
   int red_epoch;                     // all-reduces done (partial buffer parity; thread 0 writes)
-  unsigned fx_epoch;                 // fixed-point projection all-reduces done (word e mod 4)
+  unsigned fx_epoch;                 // parity of the fixed-point projection all-reduces done (the word used next)
+  unsigned long long fx_prev[2];     // full value last read from each word (thread 32 only)
   double red[NW * 8];
   double red2[NW * 4];
   unsigned long long pmin, pmax;     // profile mode: all-reduce arrival spread (ar_probe)
@@ -407,6 +409,7 @@ __device__ __forceinline__ void init_shm(Shm& sh, int cta) {
     sh.epoch = 0;
     sh.red_epoch = 0;
     sh.fx_epoch = 0;
+    sh.fx_prev[0] = sh.fx_prev[1] = 0ull;
     sh.abort = 0;
     sh.flag = 0;
     sh.vg = 0;
@@ -548,9 +551,15 @@ struct NoMid { __device__ __forceinline__ void operator()() const {} };
 // exact, so every CTA reads the same word and gets the same h whatever the order of
 // arrival — one round trip after the last arrival instead of the partial store's
 // release, the counter and the partial loads (tools/ar_bench.cu 1.33 vs 1.80–1.99 µs).
-// Words rotate mod 4; CTA 0 zeroes the word two epochs ahead (all CTAs finished
-// reading it) and alone arrives with release, which orders that zeroing before the
-// adds of the epoch that reuses the word (the pollers acquire by a fence).
+// Two words alternate and only ever grow (mod 2^64, zeroed by the host before the
+// launch): every CTA keeps the full value it last read from a word (the same value in
+// every CTA) and takes this epoch's count and sum from the difference.  Nothing is
+// stored or zeroed, so nothing needs a release or an acquire fence: a CTA's add of
+// epoch e+2 (same word) depends on its poll of epoch e+1, which completes only after
+// every CTA arrived there, i.e. after every CTA's poll of epoch e returned (the r02
+// rotation of four zeroed words needed CTA 0's release and a fence.acq_rel after each
+// poll: ≈ 0.4 µs per projection in the polling thread, profiles/r02_ncu_*_source_top).
+// The scalings are exact power-of-two multiplies (|s·2^(42−e)| ≤ 2^42; host: |e| ≤ 900).
 __device__ __forceinline__ void red_relaxed_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -560,20 +569,19 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   return v;
 }
 __device__ __forceinline__ bool fx_arrive_wait(const Dev& d, Shm& sh, double s, double& out) {  // one thread
-  const unsigned e = sh.fx_epoch;
-  unsigned long long* wd = d.fx_words + (size_t)(e & 3u) * 32;
+  const unsigned e = sh.fx_epoch & 1u;
+  unsigned long long* wd = d.fx_words + (size_t)e * 32;
+  const unsigned long long prev = sh.fx_prev[e];
   long long q = 0;
-  if (fabs(s) <= ldexp(1.0, d.fx_exp)) q = llrint(ldexp(s, 42 - d.fx_exp));
+  if (fabs(s) <= d.fx_bnd) q = __double2ll_rn(s * d.fx_up);
   else atomicOr(d.err_flag, ERRF_NONFINITE);  // non-finite (the bound holds for finite data)
-  const unsigned long long add = (1ull << 53) + (unsigned long long)(q + (1ll << 43));
-  if (sh.cta == 0) red_release_add(wd, add, false);
-  else red_relaxed_add(wd, add);
+  red_relaxed_add(wd, (1ull << 53) + (unsigned long long)(q + (1ll << 43)));
   const unsigned long long GG = (unsigned long long)d.GG;
   unsigned long long x;
   unsigned it = 0;
   unsigned long long t0 = 0;
   bool ok = true;
-  while (((x = ld_relaxed_u64(wd)) >> 53) < GG) {
+  while ((((x = ld_relaxed_u64(wd)) - prev) >> 53) < GG) {
     if (((++it) & 1023u) == 0u) {
       if (*(volatile int*)d.abort_flag) { ok = false; break; }
       const unsigned long long t = globaltimer();
@@ -581,12 +589,11 @@ __device__ __forceinline__ bool fx_arrive_wait(const Dev& d, Shm& sh, double s, 
       else if ((long long)(t - t0) > d.timeout_ns) { atomicExch(d.abort_flag, 1); ok = false; break; }
     }
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  const long long sum = (long long)(x & ((1ull << 53) - 1)) - (long long)GG * (1ll << 43);
-  out = ldexp((double)sum, d.fx_exp - 42);
-  if (sh.cta == 0) *(volatile unsigned long long*)(d.fx_words + (size_t)((e + 2u) & 3u) * 32) = 0ull;
-  sh.fx_epoch = e + 1u;
-  return ok && *(volatile int*)d.abort_flag == 0;
+  const long long sum = (long long)((x - prev) & ((1ull << 53) - 1)) - (long long)GG * (1ll << 43);
+  out = (double)sum * d.fx_dn;
+  sh.fx_prev[e] = x;
+  sh.fx_epoch = e ^ 1u;
+  return ok;  // (a CTA that aborted elsewhere never arrives again: the next poll sees the flag)
 }
 template <bool FX = false, class Mid = NoMid>
 __device__ __forceinline__ bool allreduce1(const Dev& d, Shm& sh, double v, bool /*acq*/, double& out,
@@ -2173,6 +2180,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     }
   }
   W hprev = (W)0;
+  const int nk = (nq + NT - 1) / NT;  // vectors per thread that hold rows (of thread 0; ≤ MGS_MV)
   const bool lead = d.profile && sh.cta == 0 && threadIdx.x == 0;
   unsigned long long tp = lead ? globaltimer() : 0ull;
   auto tick = [&](int slot) {
@@ -2193,14 +2201,30 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     wait(b);
     tick(8);
     const V4* X = sv + (size_t)b * nqa;                       // v_i
-    const V4* Y = sv + (size_t)((i - 2 + NB) % NB) * nqa;     // v_{i−1} (i > 1)
+    // v_{i−1}; at i = 1 there is no update: h = 0 against v_1 leaves w as it is
+    // (RN_W(w − RN_W(0·v)) = w), so the loop below carries no branch on i
+    const V4* Y = i > 1 ? sv + (size_t)((i - 2 + NB) % NB) * nqa : X;
     double acc = 0.0;
+    // Pairs of this thread's vectors: the four shared-memory loads of a pair are issued
+    // together from clamped indices (no branch between them — with `if (t < nq)` around
+    // each vector the eight iterations ran strictly one after the other, two dependent
+    // LDS latencies each: the step was latency-bound at 4 warps per scheduler), a thread
+    // past the end of the row block just does not add its product.  Same operations on
+    // every valid element and the same order of the fp64 adds as before.
 #pragma unroll
-    for (int k = 0; k < MGS_MV; ++k) {
-      const int t = threadIdx.x + k * NT;
-      if (t < nq) {
-        if (i > 1) sub_scaled(wr[k], Y[t], hprev);
-        acc += dotv(wr[k], X[t]);
+    for (int k = 0; k < MGS_MV; k += 2) {
+      if (k < nk) {  // (CTA-uniform)
+        const int t0 = threadIdx.x + k * NT, t1 = t0 + NT;
+        const int c0 = min(t0, nq - 1), c1 = min(t1, nq - 1);
+        const V4 y0 = Y[c0], x0 = X[c0], y1 = Y[c1], x1 = X[c1];
+        sub_scaled(wr[k], y0, hprev);
+        const double p0 = dotv(wr[k], x0);
+        if (t0 < nq) acc += p0;
+        if (k + 1 < nk) {
+          sub_scaled(wr[k + 1], y1, hprev);
+          const double p1 = dotv(wr[k + 1], x1);
+          if (t1 < nq) acc += p1;
+        }
       }
     }
     tick(9);

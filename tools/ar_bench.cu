@@ -50,14 +50,16 @@ __global__ void __launch_bounds__(NT, 1) kern(Args a) {
   __shared__ double red[NW], red2[NW];
   __shared__ unsigned long long epoch;
   __shared__ double cred[8], cres;
+  __shared__ unsigned long long fxprev[2];
+  __shared__ int stuckf;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = blockIdx.x, G = a.G;
-  if (threadIdx.x == 0) epoch = 0;
+  if (threadIdx.x == 0) { epoch = 0; fxprev[0] = fxprev[1] = 0; stuckf = 0; }
   __syncthreads();
   double acc_all = 0.0;
   int e3 = 0;
   const unsigned long long t0 = gtime();
   for (int it = 0; it < a.iters; ++it) {
-    double v = (double)(g + 1) * 1e-3 + it;
+    double v = (double)(g + 1) * 1e-3 + (it & 3);  // CTA sums < 2^12: inside the fixed-point variants' bound
     if (a.variant <= 2) {
       // counter barrier + load partials (old design); 0: red.release+ld.acquire, 1: relaxed red + fence, 2: barrier only
       v = warp_sum(v);
@@ -104,6 +106,46 @@ __global__ void __launch_bounds__(NT, 1) kern(Args a) {
         }
       }
       __syncthreads();
+      acc_all += red2[0];
+      e3 = e3 + 1;
+    } else if (a.variant >= 60 && a.variant <= 62) {
+      // as 8 without the zeroing: two alternating words that only ever grow (mod 2^64);
+      // each CTA keeps the word's previous full value and reads count and sum from the
+      // difference — no store, no release and (60, 61) no fence: the next add of a CTA
+      // depends on its poll's result.  61/62: power-of-two multiplies instead of ldexp.
+      v = warp_sum(v);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      if (warp == 1) {
+        double s = lane < NW ? red[lane] : 0.0;
+        for (int o = NW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+          unsigned long long* w = a.ctr + (size_t)(e3 & 1) * 32;
+          const unsigned long long prev = fxprev[e3 & 1];
+          long long q = a.variant == 60 ? llrint(ldexp(s, 43 - 12)) : __double2ll_rn(s * 2147483648.0);
+          const unsigned long long add = (1ull << 53) + (unsigned long long)(q + (1ll << 44));
+          red_rlx(w, add);
+          unsigned long long x;
+          unsigned spin = 0;
+          while ((((x = ld_rlx(w)) - prev) >> 53) < (unsigned long long)G) {
+            if ((++spin & 0xfffffu) == 0u) {  // stuck (≈ 1 s): report and release everybody
+              if (spin >= 0x1000000u || ld_rlx(a.ctr + 512)) {
+                if (!atomicExch(a.ctr + 512, 1ull))
+                  printf("stuck: cta %d it %d word %d x %llx prev %llx other %llx\n", g, it, e3 & 1, x, prev,
+                         ld_rlx(a.ctr + (size_t)((e3 + 1) & 1) * 32));
+                stuckf = 1;
+                break;
+              }
+            }
+          }
+          if (a.variant == 62) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          fxprev[e3 & 1] = x;
+          const long long sum = (long long)((x - prev) & ((1ull << 53) - 1)) - (long long)G * (1ll << 44);
+          red2[0] = a.variant == 60 ? ldexp((double)sum, 12 - 43) : (double)sum * (1.0 / 2147483648.0);
+        }
+      }
+      __syncthreads();
+      if (stuckf) break;
       acc_all += red2[0];
       e3 = e3 + 1;
     } else if (a.variant == 7) {
@@ -286,6 +328,9 @@ int main(int argc, char** argv) {
     {7, 1, "fixed-point single word (count + sum), one round trip"},
     {8, 1, "fixed-point word, relaxed arrivals (CTA 0 releases), relaxed poll + fence"},
     {9, 1, "fixed-point word, release arrivals, relaxed poll + fence"},
+    {60, 1, "fixed-point 2 growing words, all relaxed, no fence"},
+    {61, 1, "same, power-of-two multiplies instead of ldexp"},
+    {62, 1, "same as 61 + acquire fence after the poll"},
     {11, 1, "counter x1 (warp-0 poll) + partial load"},
     {12, 1, "counters x2 + partial load"},
     {14, 1, "counters x4 + partial load"},
@@ -304,7 +349,7 @@ int main(int argc, char** argv) {
       Args a{v.v, iters, G, v.stride, ctr, slots, parts, out};
       void* args[] = {&a};
       cudaError_t e;
-      if (v.v >= 40) {  // cooperative launch in clusters of C
+      if (v.v >= 40 && v.v < 60) {  // cooperative launch in clusters of C
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(G); cfg.blockDim = dim3(NT);
         cudaLaunchAttribute at[2];
