@@ -76,7 +76,9 @@ typedef struct {
   int32_t profile;        /* != 0: grid barrier after each phase for clean phase timers */
   int32_t tune;           /* developer A/B switches; 0 = production defaults (bit 25: the
                              mixed MGS projections use the fp64 partial all-reduce instead
-                             of the exact fixed-point word of DESIGN.md reading R27)       */
+                             of the exact fixed-point word of DESIGN.md reading R27; bit 28:
+                             the resident MGS ring copies the next vector inside the step's
+                             all-reduce instead of at the start of the step)               */
   int32_t restart_policy; /* 0 THRESHOLD: restart at j = m or |s_{j+1}| ≤ β·max(tol‖b‖/‖z‖, δ)
                              (PAPER.md:257-264); 1 TWOSTAGE: the first cycle as THRESHOLD,
                              later cycles at the first cycle's iteration count (PAPER.md:

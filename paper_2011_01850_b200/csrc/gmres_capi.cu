@@ -228,6 +228,8 @@ VLayout vlayout_for(int ortho, int m, int wb, int tile_bytes) {
   return L;
 }
 
+constexpr bool kMgsCopyInAllreduce = false;
+
 // fixed-point projection all-reduce (reading R27): B = 2^e and its exact scalings; the
 // exponent range keeps 2^(42−e) and 2^(e−42) normal (else the fp64 all-reduce is used)
 void set_fx(Dev& d, int e, unsigned long long* words) {
@@ -1353,6 +1355,10 @@ int plan_solve(gmres_ctx* ctx, const double* d_b, const double* d_x0, double* d_
   }
   set_vlayout(d, vl);
   d.tune = opts ? opts->tune : 0;
+  // resident MGS ring: the copy of the next vector at the start of the step (default) or inside the
+  // step's all-reduce (tune bit 28 flips the default; the kernel reads bit 29)
+  d.tune &= ~536870912;
+  if (kMgsCopyInAllreduce != bool(d.tune & 268435456)) d.tune |= 536870912;
   if (d.tune & 4194304) d.merge_stream = 0;  // dev A/B: chunk stream instead of the merge-path stream
   // reading R27: exact fixed-point MGS projections in the mixed Jacobi solve on one rank
   // (tune bit 25: the fp64 partial all-reduce instead, dev A/B)

@@ -2137,6 +2137,10 @@ __host__ inline void set_smem_offsets(Dev& d) {
 // the all-reduce and no register holds an in-flight load across it.  Same
 // operations and order per element as mgs_sweep.
 constexpr int MGS_MV = 8;  // 16-byte vectors of w per thread in registers (both resident variants)
+#ifndef G200_MGS_GRP
+#define G200_MGS_GRP 4
+#endif
+constexpr int MGS_GRP = G200_MGS_GRP;  // vectors whose shared-memory loads are issued together (mgs_resident)
 template <class W>
 __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int r1, int j, const W* V, long long ldv,
                                              W* w, double* s_h, char* s_tiles, double& NN) {
@@ -2194,10 +2198,12 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   // → 79.4 (early copy; the prefetch on top: 79.2, not kept); the ortho phase 67.4 → 57.5 ms.
   // (a ring of two buffers has no free buffer at the start of a step: the copy of
   // v_{i+1} then goes in the all-reduce, into v_{i−1}'s buffer)
-  const bool early = NB >= 3;
+  const bool early = NB >= 3 && !(d.tune & 536870912);  // (bit 29, set by the host: copy in the all-reduce)
   for (int i = 1; i <= j; ++i) {
     const int b = (i - 1) % NB;
     if (early && threadIdx.x == TMA_T && i >= 2 && i + NB - 2 <= j) issue(i + NB - 2);
+    // (r02, measured and not kept: an L2 prefetch of the vector after it — no change, 55.9 vs
+    // 55.3 ms; the copy inside the step's all-reduce instead, tune bit 28 — 57.4 ms)
     wait(b);
     tick(8);
     const V4* X = sv + (size_t)b * nqa;                       // v_i
@@ -2212,18 +2218,20 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     // past the end of the row block just does not add its product.  Same operations on
     // every valid element and the same order of the fp64 adds as before.
 #pragma unroll
-    for (int k = 0; k < MGS_MV; k += 2) {
+    for (int k = 0; k < MGS_MV; k += MGS_GRP) {
       if (k < nk) {  // (CTA-uniform)
-        const int t0 = threadIdx.x + k * NT, t1 = t0 + NT;
-        const int c0 = min(t0, nq - 1), c1 = min(t1, nq - 1);
-        const V4 y0 = Y[c0], x0 = X[c0], y1 = Y[c1], x1 = X[c1];
-        sub_scaled(wr[k], y0, hprev);
-        const double p0 = dotv(wr[k], x0);
-        if (t0 < nq) acc += p0;
-        if (k + 1 < nk) {
-          sub_scaled(wr[k + 1], y1, hprev);
-          const double p1 = dotv(wr[k + 1], x1);
-          if (t1 < nq) acc += p1;
+        V4 ys[MGS_GRP], xs[MGS_GRP];
+#pragma unroll
+        for (int u = 0; u < MGS_GRP; ++u) {
+          const int c = min((int)threadIdx.x + (k + u) * NT, nq - 1);
+          ys[u] = Y[c];
+          xs[u] = X[c];
+        }
+#pragma unroll
+        for (int u = 0; u < MGS_GRP; ++u) {  // (no branch on k + u < nk: the compiler sinks the loads under it)
+          sub_scaled(wr[k + u], ys[u], hprev);
+          const double p = dotv(wr[k + u], xs[u]);
+          if ((int)threadIdx.x + (k + u) * NT < nq) acc += p;
         }
       }
     }
