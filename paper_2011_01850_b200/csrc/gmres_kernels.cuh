@@ -2154,14 +2154,14 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   unsigned ph = sh.vphase;
   // copies are issued by warp 0 (TMA_T): warp 1 performs the all-reduce's release
   constexpr int TMA_T = 0;
-  auto issue = [&](int c) {  // one thread: v_c (1-based) → buffer (c−1) mod NB
-    const int b = (c - 1) % NB;
+  auto issue_to = [&](int c, int b) {  // one thread: v_c (1-based) → buffer b = (c−1) mod NB
     char* dst = reinterpret_cast<char*>(sv + (size_t)b * nqa);
     const char* src = reinterpret_cast<const char*>(V + (long long)(c - 1) * ldv + r0);
     mbar_expect_tx(&sh.mbar_v[b], bytes);
     for (unsigned o = 0; o < bytes; o += 32768u)
       tma_load_1d(dst + o, src + o, min(32768u, bytes - o), &sh.mbar_v[b]);
   };
+  auto issue = [&](int c) { issue_to(c, (c - 1) % NB); };
   auto wait = [&](int b) -> bool {
     const unsigned par = (ph >> b) & 1u;
     ph ^= (1u << b);
@@ -2199,9 +2199,13 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   // (a ring of two buffers has no free buffer at the start of a step: the copy of
   // v_{i+1} then goes in the all-reduce, into v_{i−1}'s buffer)
   const bool early = NB >= 3 && !(d.tune & 536870912);  // (bit 29, set by the host: copy in the all-reduce)
+  // (b, bp: the ring buffers of v_i and v_{i−1}, stepped without the runtime modulo that sat on
+  // every step's critical path — 5.6 % of the MGS launch's stall samples, ncu r02)
+  int b = NB - 1, bp = NB - 2;
   for (int i = 1; i <= j; ++i) {
-    const int b = (i - 1) % NB;
-    if (early && threadIdx.x == TMA_T && i >= 2 && i + NB - 2 <= j) issue(i + NB - 2);
+    bp = b;
+    b = b + 1 == NB ? 0 : b + 1;
+    if (early && threadIdx.x == TMA_T && i >= 2 && i + NB - 2 <= j) issue_to(i + NB - 2, b >= 2 ? b - 2 : b - 2 + NB);
     // (r02, measured and not kept: an L2 prefetch of the vector after it — no change, 55.9 vs
     // 55.3 ms; the copy inside the step's all-reduce instead, tune bit 28 — 57.4 ms)
     wait(b);
@@ -2209,7 +2213,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
     const V4* X = sv + (size_t)b * nqa;                       // v_i
     // v_{i−1}; at i = 1 there is no update: h = 0 against v_1 leaves w as it is
     // (RN_W(w − RN_W(0·v)) = w), so the loop below carries no branch on i
-    const V4* Y = i > 1 ? sv + (size_t)((i - 2 + NB) % NB) * nqa : X;
+    const V4* Y = i > 1 ? sv + (size_t)bp * nqa : X;
     double acc = 0.0;
     // Pairs of this thread's vectors: the four shared-memory loads of a pair are issued
     // together from clamped indices (no branch between them — with `if (t < nq)` around
@@ -2248,7 +2252,7 @@ __device__ __forceinline__ bool mgs_resident(const Dev& d, Shm& sh, int r0, int 
   // final update w ← w − h_j v_j, ‖w‖², w back to global for the next SpMV
   double nn = 0.0;
   {
-    const V4* X = sv + (size_t)((j - 1) % NB) * nqa;
+    const V4* X = sv + (size_t)b * nqa;  // v_j (j ≥ 1)
     V4* wg = reinterpret_cast<V4*>(w) + q0;
 #pragma unroll
     for (int k = 0; k < MGS_MV; ++k) {

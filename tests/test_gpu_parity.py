@@ -403,7 +403,8 @@ def test_mgs_variants_agree(prec, k, variant):
     # tune bit 2: force the global sweep; bit 19: force the streamed MGS (w in shared + global memory);
     # bit 8: a two-buffer ring for the resident MGS (its copies go in the all-reduce, not at the
     # start of the step: another schedule, the same arithmetic)
-    cases = ((0, variant), (4, 0), (524288, 3)) + (((256, 1),) if variant == 1 else ())
+    # bit 28: the three-buffer ring's copies in the all-reduce too (gmres.h)
+    cases = ((0, variant), (4, 0), (524288, 3)) + (((256, 1), (268435456, 1)) if variant == 1 else ())
     for tune, want in cases:
         xd = torch.zeros_like(bd)
         r = S.solve_device(bd, xd, m=30, ortho=G.MGS, precision=prec, max_cycles=3, tol=1e-14, tune=tune)
