@@ -2312,8 +2312,7 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
         tma_load_1d(sv + (size_t)s * NT, V + (long long)c * ldv + r0 + (long long)k * NT * N, bytes, &sh.mbar_v[s]);
       }
   };
-  auto wait = [&](unsigned g) -> bool {
-    const unsigned s = g % NS, par = (g / NS) & 1u;
+  auto wait = [&](unsigned s, unsigned par) -> bool {  // slot and parity of a stream chunk
     if (mbar_try_wait(&sh.mbar_v[s], par)) return true;
     const unsigned long long t0 = globaltimer();
     for (;;) {
@@ -2340,9 +2339,20 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
   // the all-reduce are L2 hits (C2 fp64 MGS 160.8 → 154–159 ms; measured r02: refilling the
   // freed slots at the start of the step instead — the resident ring's schedule — 167 ms)
   const unsigned vbytes = (unsigned)nq * 16u;
+  int sv0 = (int)(g0 % NS);
+  unsigned qv0 = g0 / NS;
   for (int i = 1; i <= j; ++i) {
     const unsigned gi = g0 + (unsigned)((i - 1) * nch);  // v_i's first chunk
-    const int s0 = (int)(gi % NS);  // v_i's chunks sit in slots s0, s0+1, … (mod NS; NS ≥ nch)
+    // v_i's chunks sit in slots s0, s0+1, … (mod NS; NS ≥ nch); s0 = gi mod NS and qv = gi / NS
+    // are stepped (no runtime division per chunk wait)
+    const int s0 = sv0;
+    const unsigned q0v = qv0;
+    auto wait_k = [&](int k) -> bool {
+      const int sk = s0 + k;
+      return sk < (int)NS ? wait((unsigned)sk, q0v & 1u) : wait((unsigned)(sk - (int)NS), (q0v + 1u) & 1u);
+    };
+    sv0 += nch;
+    if (sv0 >= (int)NS) { sv0 -= (int)NS; ++qv0; }
     if (threadIdx.x == 32 && i + 2 <= j)
       for (unsigned o = 0; o < vbytes; o += 32768u)
         prefetch_l2(reinterpret_cast<const char*>(V + (long long)(i + 1) * ldv + r0) + o, min(32768u, vbytes - o));
@@ -2354,12 +2364,12 @@ __device__ __forceinline__ bool mgs_chunked(const Dev& d, Shm& sh, int r0, int r
 #pragma unroll
     for (int k = 0; k < MGS_MV; ++k) {
       if (k < nch) {
-        if (!wait(gi + k)) return false;
+        if (!wait_k(k)) return false;
         if (threadIdx.x + k * NT < nq) acc += dotv(wr[k], *slot(k));
       }
     }
     for (int k = MGS_MV; k < nch; ++k) {
-      if (!wait(gi + k)) return false;
+      if (!wait_k(k)) return false;
       if (threadIdx.x + k * NT < nq) acc += dotv(ws[k * NT + threadIdx.x], *slot(k));
     }
     tick(9);
